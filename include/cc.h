@@ -1,0 +1,235 @@
+/*
+ * cc.h -- C ABI of the B200-native colour-coding hot path
+ *         (Chen et al., "High-Performance Massive Subgraph Counting using
+ *          Pipelined Adaptive-Group Communication", arXiv 1804.09764;
+ *          cited as PAPER.md line numbers).
+ *
+ * Library: paper_1804_09764_b200/libcc.so (CUDA for sm_100a + C++ host code).
+ * No torch types cross this boundary: plain host pointers and sizes.
+ *
+ * Problem: given a graph G and a tree
+ * template T on k vertices, estimate #emb(T, G).  One colouring of G with k
+ * colours is followed by the per-colouring dynamic
+ * program of Eq. 1 / Eq. 2:
+ *     C(v, T_i, S) = sum_{u in N(v)} sum_{S = S1 u S2} C(v, T_i', S1) * C(u, T_i'', S2)
+ * computed here as "aggregate, then combine" (exact algebra):
+ *     N(v, S2) = sum_{u in N(v)} C(u, T_i'', S2)          (SpMM-shaped gather)
+ *     C(v, T_i, S) = sum_{(S1,S2) split of S} C(v, T_i', S1) * N(v, S2)
+ * and the colourful total X = sum_v C(v, T, [k]) (Eq. 3 without its scale,
+ * PAPER.md line 176).  Counting convention (reading C-1): the DP is
+ * run with the over-count factor d = 1, so X counts colourful MAPS (injective
+ * edge-preserving maps V_T -> V whose image is colourful); copies are
+ * maps / |Aut(T)|.
+ *
+ * Conventions for every call:
+ *  - Every call returns a cc_status; on failure cc_last_error(ctx) gives a
+ *    message.  No C++ exception crosses the ABI.  Outputs are written only on
+ *    CC_OK.
+ *  - All pointer arguments are HOST memory.  The library copies inputs before
+ *    returning, so the caller keeps ownership and may free them on return.
+ *  - Device memory is owned by the context and released by cc_destroy.
+ *  - After CC_ERR_CUDA or CC_ERR_NCCL the context is poisoned: every later
+ *    call except cc_destroy / cc_last_error returns CC_ERR_STATE.
+ *  - A context is bound to one CUDA device and is not thread-safe.
+ *  - Multi-GPU (world > 1): one context per rank (one process per GPU).
+ *    cc_load_graph, cc_set_template, cc_color, cc_set_colors,
+ *    cc_count_colorful and cc_estimate are COLLECTIVE: all ranks call them in
+ *    the same order with the same arguments (the same global CSR) and all
+ *    ranks receive the same result.
+ */
+#ifndef CC_H
+#define CC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cc_ctx cc_ctx; /* opaque, one per rank */
+
+typedef enum {
+  CC_OK = 0,
+  CC_ERR_ARG = 1,       /* bad argument (null pointer, out-of-range option) */
+  CC_ERR_GRAPH = 2,     /* CSR rejected by validation (see cc_load_graph) */
+  CC_ERR_TEMPLATE = 3,  /* parent array is not a tree on 1..16 vertices */
+  CC_ERR_STATE = 4,     /* call order violated, or context poisoned */
+  CC_ERR_OOM = 5,       /* device or host allocation failed */
+  CC_ERR_CUDA = 6,      /* CUDA runtime error (context poisoned) */
+  CC_ERR_NCCL = 7,      /* NCCL error (context poisoned) */
+  CC_ERR_NONFINITE = 8  /* fp32 tables overflowed: the result is not finite */
+} cc_status;
+
+/* Table precision (reading C-6; the paper states none). */
+enum {
+  CC_FP64 = 0, /* fp64 tables and accumulation: exact for integers < 2^53 */
+  CC_FP32 = 1  /* fp32 table storage; fp64 neighbour-sum accumulation,
+                  fp64 root products and fp64 final reduction */
+};
+
+typedef struct {
+  int32_t precision;     /* CC_FP64 or CC_FP32 */
+  int32_t device;        /* CUDA device ordinal for this rank */
+  int32_t world;         /* number of ranks of the 1D vertex partition (>= 1) */
+  int32_t rank;          /* this rank, 0 <= rank < world */
+  const void *nccl_id;   /* 128-byte ncclUniqueId when world > 1 (from rank 0's
+                            cc_nccl_unique_id, broadcast by the caller); ignored
+                            when world == 1 */
+  int64_t chunk_cols;    /* column-chunk width of the aggregation (count-table
+                            columns per pass; PAPER.md lines 72, 391-396
+                            "intermediate data partitioning"); 0 = auto */
+  int32_t segment_len;   /* neighbour-list task size s: neighbour lists longer
+                            than this are split into segments of at most s
+                            neighbours (Alg. 4); 0 = auto */
+  int32_t use_graphs;    /* 1 = capture the per-colouring launch sequence in a
+                            CUDA graph and replay it; 0 = plain launches */
+  uint64_t relabel_seed; /* seed of the internal vertex permutation used to
+                            balance the partition ("randomly
+                            partitioned"); never changes results */
+} cc_options;
+
+/* Fill *opt with defaults: CC_FP64, device 0, world 1, rank 0, auto sizes,
+ * CUDA graphs on, relabel_seed 0x5eed. */
+cc_status cc_default_options(cc_options *opt);
+
+/* Rank 0 only: write a fresh 128-byte ncclUniqueId to out128 (host).
+ * CC_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+cc_status cc_nccl_unique_id(void *out128);
+
+/* Create a context on opt->device.  For world > 1 this joins the NCCL
+ * communicator (collective over all ranks).  *out receives the handle. */
+cc_status cc_create(const cc_options *opt, cc_ctx **out);
+
+/* Release all device memory, streams and the communicator.  NULL is a no-op. */
+void cc_destroy(cc_ctx *ctx);
+
+/* Message of the last failure on ctx ("" if none).  Valid until the next call. */
+const char *cc_last_error(const cc_ctx *ctx);
+
+/* Load the graph G (neighbour lists N(v)).
+ *  n       : number of vertices, 0 <= n < 2^31
+ *  row_ptr : n+1 int64 offsets, row_ptr[0] == 0, nondecreasing
+ *  col     : row_ptr[n] int32 neighbour ids in [0, n)
+ * The CSR must describe a simple undirected graph: no self-loops, no
+ * duplicate neighbours within a row, and symmetric (u in N(v) <=> v in N(u)).
+ * Rows need not be sorted.  Violations are REJECTED with CC_ERR_GRAPH (the
+ * library never cleans input).  Internally: isolated vertices are dropped
+ * from the tables (their rows are zero for templates of >= 2 vertices),
+ * vertices are relabelled (hubs first per rank; seeded shuffle across ranks)
+ * and, for world > 1, cut into balanced contiguous ranges with halo lists.
+ * Invalidates the colouring. */
+cc_status cc_load_graph(cc_ctx *ctx, int64_t n, const int64_t *row_ptr, const int32_t *col);
+
+/* Set the tree template T as a parent array of k
+ * entries, 1 <= k <= 16, exactly one -1 (the root rho(T));
+ * every other entry is the index of the vertex's parent and the pointers must
+ * form one tree.  Builds the sub-template partition (PAPER.md lines 110-113,
+ * 122, 159: cut an edge at the root; the active part keeps the root, the
+ * passive part is rooted at the cut neighbour), merges isomorphic
+ * sub-templates, and uploads the colour-set split tables.  k colours are used
+ * (PAPER.md line 154).  Invalidates the colouring.  CC_ERR_TEMPLATE on a bad
+ * parent array. */
+cc_status cc_set_template(cc_ctx *ctx, int32_t k, const int32_t *parent);
+
+/* Colour every vertex uniformly at random with k colours (PAPER.md lines
+ * 156-158), on the device, from the shared seed and the ORIGINAL vertex id:
+ *   col(v) = ((mix(mix(seed) ^ v) >> 32) * k) >> 32,
+ *   mix = SplitMix64 finaliser (reading C-2).
+ * Requires a template (k).  */
+cc_status cc_color(cc_ctx *ctx, uint64_t seed);
+
+/* Run the per-colouring DP (Alg. 1 lines 8-10, Eq. 2) and return
+ * X = sum_v C(v, T(rho), [k]) -- the number of colourful maps for the current
+ * colouring (Eq. 3 WITHOUT the k^k/k! scale).  In CC_FP64 mode X is exact
+ * while below 2^53.  Requires graph, template and colouring
+ * (CC_ERR_STATE otherwise).  CC_ERR_NONFINITE if fp32 tables overflowed. */
+cc_status cc_count_colorful(cc_ctx *ctx, double *colorful_maps);
+
+/* The estimator (Alg. 1 lines 4-13 and Eq. 3; DESIGN.md readings
+ * C-1, C-10): for j = 0..iterations-1, colour with seed0 + j, count X_j, and
+ * return *estimate = mean_j(X_j) * k^k / k! / |Aut(T)|, an estimate of the
+ * number of non-induced copies of T.  per_iter (nullable) receives the
+ * `iterations` values X_j.  iterations >= 1. */
+cc_status cc_estimate(cc_ctx *ctx, int32_t iterations, uint64_t seed0, double *estimate,
+                      double *per_iter);
+
+/* ---- test and bench hooks (off the hot path) ---------------------------- */
+
+/* Use a caller-supplied colouring: colors[v] in [0, k) for every ORIGINAL
+ * vertex id v < n (host array of n bytes; copied to the device). */
+cc_status cc_set_colors(cc_ctx *ctx, const uint8_t *colors);
+
+/* Copy the current colouring back, indexed by original vertex id (n bytes). */
+cc_status cc_get_colors(cc_ctx *ctx, uint8_t *colors);
+
+/* |Aut(T)|, |Aut_rho(T)| (automorphisms fixing the root) and the number of
+ * DP steps of the plan. */
+cc_status cc_template_info(cc_ctx *ctx, int64_t *aut, int64_t *aut_root, int32_t *n_steps);
+
+/* Re-run the DP for the current colouring keeping every table, and copy the
+ * full-subtree table of template vertex x, D_x(v, S), to out: n rows (ORIGINAL
+ * vertex order) x C(k, s_x) columns (colex order of S), as double, where s_x is
+ * the size of x's subtree.  For x = root this is the per-vertex C(v, T, [k]).
+ * World must be 1. */
+cc_status cc_get_subtree_counts(cc_ctx *ctx, int32_t x, double *out);
+
+/* Timing of the last cc_count_colorful, in ms, per phase (device events):
+ * out[0] = total, then per DP step.  *n receives the number written. */
+cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
+
+/* Stats of the last cc_count_colorful: out[0] = U = sum over aggregations of
+ * adjacency entries x columns ("edge x colour-set updates"),
+ * out[1] = algorithmic bytes moved (model bytes), out[2] = algorithmic bytes
+ * of the aggregation kernels alone, out[3] = number of kernel launches,
+ * out[4] = peak table bytes.  cap >= 5. */
+cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
+
+/* ---- host-only introspection (no GPU needed; used by CPU tests) --------- */
+
+/* Colex rank of the colour set `mask` (bit c = colour c) among sets of the
+ * same size: rank(S) = sum_i C(s_i, i+1), s_0 < s_1 < ... (combinatorial
+ * number system).  Returns -1 on a bad argument. */
+int64_t cc_colex_rank(uint32_t mask);
+
+/* Inverse: the size-s set of rank r (k-independent); 0xFFFFFFFF if invalid. */
+uint32_t cc_colex_unrank(int32_t s, int64_t r);
+
+/* Split table of a step (t; a, p) with k colours: for every S of size t
+ * (colex rank r < C(k,t)) and every q < C(t,a), the q-th subset S1 of S of
+ * size a (colex over positions in S) and S2 = S \ S1, packed as
+ * rank(S1) | rank(S2) << 16, stored at out[q * C(k,t) + r].  cap = entries
+ * available in out.  CC_ERR_ARG if too small. */
+cc_status cc_split_table(int32_t k, int32_t t, int32_t a, uint32_t *out, int64_t cap);
+
+/* Plan a template without a context.  steps_out receives, per step, 6 int32:
+ * t, a, p, active table id (-1 = single vertex), passive table id (-1 = single
+ * vertex), output table id (-1 = root).  Also |Aut(T)|, |Aut_rho(T)|, and
+ * Table-3 memory = sum C(k,t), computation = sum C(k,t) C(t,a) over the
+ * non-root steps. */
+cc_status cc_plan_template(int32_t k, const int32_t *parent, int32_t *steps_out, int32_t cap_steps,
+                           int32_t *n_steps, int64_t *aut, int64_t *aut_root, double *memory,
+                           double *computation);
+
+/* Partition plan of the 1D vertex partition (Alg. 2 line 2 and lines
+ * 374-382) for rank `rank` of `world`, computed on the host exactly as
+ * cc_load_graph does.  sizes_out[0..3] = n_own, n_halo, local CSR entries,
+ * total send rows.  When the array pointers are non-NULL they receive:
+ *   own_orig[n_own]   original ids of owned vertices, in internal order
+ *   halo_orig[n_halo] original ids of halo vertices, in internal order
+ *   recv_off[world+1] halo rows received from each peer (offsets into halo)
+ *   send_off[world+1] offsets into send_idx per peer
+ *   send_idx[...]     owned local indices sent to each peer, in the peer's
+ *                     receive order
+ *   rp[n_own+1], col[...] the local CSR; col < n_own is an owned row,
+ *                     col >= n_own is halo row col - n_own.
+ * Call once with NULL arrays to get sizes. */
+cc_status cc_partition_plan(int64_t n, const int64_t *row_ptr, const int32_t *col, int32_t world,
+                            int32_t rank, uint64_t relabel_seed, int64_t *sizes_out,
+                            int32_t *own_orig, int32_t *halo_orig, int64_t *recv_off,
+                            int64_t *send_off, int32_t *send_idx, int64_t *rp, int32_t *lcol);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CC_H */

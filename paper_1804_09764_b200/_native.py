@@ -1,0 +1,63 @@
+"""ctypes binding of libcc.so (include/cc.h).  Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels.  There is no
+fallback: if libcc.so is missing or fails to load, importing this module
+raises ImportError."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcc.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1804_09764_b200.build` "
+                      "(or __graft_entry__.build())")
+
+lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+
+c_i32, c_i64, c_u32, c_u64, c_dbl, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                         ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p)
+
+
+class cc_options(ctypes.Structure):
+    _fields_ = [("precision", c_i32), ("device", c_i32), ("world", c_i32), ("rank", c_i32),
+                ("nccl_id", vp), ("chunk_cols", c_i64), ("segment_len", c_i32),
+                ("use_graphs", c_i32), ("relabel_seed", c_u64)]
+
+
+CC_OK, CC_ERR_ARG, CC_ERR_GRAPH, CC_ERR_TEMPLATE, CC_ERR_STATE, CC_ERR_OOM, CC_ERR_CUDA, \
+    CC_ERR_NCCL, CC_ERR_NONFINITE = range(9)
+CC_FP64, CC_FP32 = 0, 1
+STATUS_NAMES = ["CC_OK", "CC_ERR_ARG", "CC_ERR_GRAPH", "CC_ERR_TEMPLATE", "CC_ERR_STATE", "CC_ERR_OOM",
+                "CC_ERR_CUDA", "CC_ERR_NCCL", "CC_ERR_NONFINITE"]
+
+# every symbol declared in include/cc.h, with its signature
+SIGNATURES = {
+    "cc_default_options": (c_i32, [vp]),
+    "cc_nccl_unique_id": (c_i32, [vp]),
+    "cc_create": (c_i32, [vp, vp]),
+    "cc_destroy": (None, [vp]),
+    "cc_last_error": (ctypes.c_char_p, [vp]),
+    "cc_load_graph": (c_i32, [vp, c_i64, vp, vp]),
+    "cc_set_template": (c_i32, [vp, c_i32, vp]),
+    "cc_color": (c_i32, [vp, c_u64]),
+    "cc_count_colorful": (c_i32, [vp, vp]),
+    "cc_estimate": (c_i32, [vp, c_i32, c_u64, vp, vp]),
+    "cc_set_colors": (c_i32, [vp, vp]),
+    "cc_get_colors": (c_i32, [vp, vp]),
+    "cc_template_info": (c_i32, [vp, vp, vp, vp]),
+    "cc_get_subtree_counts": (c_i32, [vp, c_i32, vp]),
+    "cc_last_profile": (c_i32, [vp, vp, c_i32, vp]),
+    "cc_last_stats": (c_i32, [vp, vp, c_i32]),
+    "cc_colex_rank": (c_i64, [c_u32]),
+    "cc_colex_unrank": (c_u32, [c_i32, c_i64]),
+    "cc_split_table": (c_i32, [c_i32, c_i32, c_i32, vp, c_i64]),
+    "cc_plan_template": (c_i32, [c_i32, vp, vp, c_i32, vp, vp, vp, vp, vp]),
+    "cc_partition_plan": (c_i32, [c_i64, vp, vp, c_i32, c_i32, c_u64, vp, vp, vp, vp, vp, vp, vp, vp]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args

@@ -1,0 +1,85 @@
+// colex.cpp -- colour-set indexing with the combinatorial number system and
+// the split / lift / complement tables of the DP steps.
+//
+// PAPER.md Alg. 1 line 8 (lines 159-160): "for v in V, T_i in T and subset
+// S_i subset of S with |S_i| = |T_i|" -- every table row holds C(k, |T_i|)
+// entries, one per colour set; Eq. 1/2 (lines 118, 167) sum over the splits
+// S = S1 u S2 with |S1| = |T_i'|, |S2| = |T_i''|.
+#include <cstring>
+
+#include "common.h"
+
+namespace cc {
+
+int64_t binom(int n, int r) {
+  if (r < 0 || n < 0 || r > n) return 0;
+  int64_t c = 1;
+  for (int i = 1; i <= r; ++i) c = c * (n - r + i) / i;
+  return c;
+}
+
+// rank(S) = sum_i C(s_i, i + 1) over the elements s_0 < s_1 < ... of S.
+int64_t colex_rank(uint32_t mask) {
+  int64_t r = 0;
+  int i = 0;
+  for (int c = 0; c < 32; ++c)
+    if (mask >> c & 1u) r += binom(c, ++i);
+  return r;
+}
+
+uint32_t colex_unrank(int s, int64_t r) {
+  if (s < 0 || s > kMaxK || r < 0) return 0xFFFFFFFFu;
+  uint32_t mask = 0;
+  int hi = 31;
+  for (int i = s; i >= 1; --i) {
+    // largest c with C(c, i) <= r
+    int c = i - 1;
+    while (c + 1 <= hi && binom(c + 1, i) <= r) ++c;
+    r -= binom(c, i);
+    mask |= 1u << c;
+    hi = c - 1;
+  }
+  return r == 0 ? mask : 0xFFFFFFFFu;
+}
+
+std::vector<uint32_t> split_table(int k, int t, int a) {
+  const int64_t nS = binom(k, t), nq = binom(t, a);
+  std::vector<uint32_t> out((size_t)(nS * nq));
+  int elem[kMaxK];
+  for (int64_t r = 0; r < nS; ++r) {
+    uint32_t S = colex_unrank(t, r);
+    int m = 0;
+    for (int c = 0; c < k; ++c)
+      if (S >> c & 1u) elem[m++] = c;
+    for (int64_t q = 0; q < nq; ++q) {
+      uint32_t pos = colex_unrank(a, q);  // positions within S
+      uint32_t S1 = 0;
+      for (int i = 0; i < t; ++i)
+        if (pos >> i & 1u) S1 |= 1u << elem[i];
+      uint32_t S2 = S & ~S1;
+      out[(size_t)(q * nS + r)] = (uint32_t)colex_rank(S1) | ((uint32_t)colex_rank(S2) << 16);
+    }
+  }
+  return out;
+}
+
+std::vector<uint16_t> drop_table(int k, int t) {
+  const int64_t nS = binom(k, t);
+  std::vector<uint16_t> out((size_t)(nS * 16), 0xFFFF);
+  for (int64_t r = 0; r < nS; ++r) {
+    uint32_t S = colex_unrank(t, r);
+    for (int c = 0; c < k; ++c)
+      if (S >> c & 1u) out[(size_t)(r * 16 + c)] = (uint16_t)colex_rank(S & ~(1u << c));
+  }
+  return out;
+}
+
+std::vector<uint16_t> complement_table(int k, int a) {
+  const int64_t nX = binom(k, a);
+  const uint32_t full = (k == 32) ? 0xFFFFFFFFu : ((1u << k) - 1u);
+  std::vector<uint16_t> out((size_t)nX);
+  for (int64_t r = 0; r < nX; ++r) out[(size_t)r] = (uint16_t)colex_rank(full & ~colex_unrank(a, r));
+  return out;
+}
+
+}  // namespace cc

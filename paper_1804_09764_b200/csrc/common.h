@@ -1,0 +1,101 @@
+// common.h -- internal host-side types of libcc (not part of the C ABI).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cc.h"
+
+namespace cc {
+
+// Thrown inside the library, converted to a cc_status at the ABI boundary.
+struct Error : std::runtime_error {
+  cc_status status;
+  Error(cc_status s, const std::string &m) : std::runtime_error(m), status(s) {}
+};
+
+constexpr int kMaxK = 16;
+
+// ---------------------------------------------------------------- colex.cpp
+// Binomial coefficients C(n, r) for n, r <= 16 (exact in int64).
+int64_t binom(int n, int r);
+// Combinatorial number system (colex) rank / unrank of colour sets.
+int64_t colex_rank(uint32_t mask);
+uint32_t colex_unrank(int s, int64_t r);
+// Split table of (t; a, t-a) over k colours: out[q * C(k,t) + r] =
+// rank(S1) | rank(S2) << 16 for the q-th size-a subset S1 of S = unrank(t, r).
+std::vector<uint32_t> split_table(int k, int t, int a);
+// Lift (drop) table for a = 1: out[r * 16 + c] = rank(S \ {c}) for S = unrank(t, r)
+// if c in S, else 0xFFFF.
+std::vector<uint16_t> drop_table(int k, int t);
+// Complement table at the root: out[r] = rank([k] \ X) for X = unrank(a, r).
+std::vector<uint16_t> complement_table(int k, int a);
+
+// ---------------------------------------------------------------- plan.cpp
+// One DP step (t; a, p): T_out(v, S) = sum_{S1 u S2 = S} A(v, S1) N_P(v, S2),
+// N_P(v, S2) = sum_{u in N(v)} P(u, S2).  Table ids index Plan::tables;
+// id -1 = the single-vertex table C(v, {x}, {c}) = [c == col v] (implicit).
+struct Step {
+  int t, a, p;
+  int active;   // table id or -1
+  int passive;  // table id or -1
+  int out;      // table id, or -1 for the root step (t == k)
+};
+
+struct TableInfo {
+  int size;       // number of template vertices = colour-set size
+  int template_x; // a template vertex whose full subtree (or partial) this is
+  int j;          // number of children of template_x included
+  std::string code;
+};
+
+struct Plan {
+  int k = 0;
+  int root = -1;
+  std::vector<int> parent;
+  std::vector<Step> steps;
+  std::vector<TableInfo> tables;
+  int64_t aut = 1, aut_root = 1;
+  double memory = 0, computation = 0;  // Table 3 quantities
+  // Per template vertex x: table id of its full subtree (-1 for leaves = single vertex;
+  // -2 for the root, whose table is the root step).
+  std::vector<int> full_table;
+  // Liveness: last step index that reads table id as active / as passive source.
+  std::vector<int> table_last_use;
+  // For each table id used as passive with p >= 2: first step (aggregation point)
+  // and last step that consumes its aggregated N.
+  std::vector<int> n_first_use, n_last_use;
+};
+
+Plan make_plan(int k, const int32_t *parent);  // throws Error(CC_ERR_TEMPLATE)
+
+// ---------------------------------------------------------------- graph.cpp
+// Validated CSR (copy) of the global graph.
+struct HostGraph {
+  int64_t n = 0;
+  std::vector<int64_t> rp;
+  std::vector<int32_t> col;
+};
+// Validate (throws Error(CC_ERR_GRAPH)) and copy with rows sorted.
+HostGraph validate_graph(int64_t n, const int64_t *row_ptr, const int32_t *col);
+
+// The 1D vertex partition of one rank (Alg. 2 line 2; lines 374-382).
+struct RankPart {
+  int world = 1, rank = 0;
+  int64_t n_own = 0, n_halo = 0;
+  std::vector<int32_t> own_orig;   // internal owned index -> original id
+  std::vector<int32_t> halo_orig;  // halo index -> original id
+  std::vector<int64_t> rp;         // local CSR over owned rows (n_own + 1)
+  std::vector<int32_t> col;        // < n_own: owned row; >= n_own: halo row
+  std::vector<int64_t> mid;        // first halo neighbour position per owned row
+  std::vector<int64_t> recv_off;   // world + 1, offsets into halo rows
+  std::vector<int64_t> send_off;   // world + 1, offsets into send_idx
+  std::vector<int32_t> send_idx;   // owned local indices, per peer in receive order
+  int64_t n_global = 0;            // n of the input graph (incl. isolated)
+  std::vector<int32_t> iso_orig;   // isolated vertices (coloured, never in tables)
+};
+RankPart partition_graph(const HostGraph &g, int world, int rank, uint64_t relabel_seed);
+
+}  // namespace cc

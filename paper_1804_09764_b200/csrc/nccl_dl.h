@@ -1,0 +1,29 @@
+// nccl_dl.h -- NCCL loaded at run time (dlopen), so libcc.so has no link-time
+// dependency on a particular libnccl; the process's already-loaded copy
+// (torch's bundled NCCL 2.28) is reused when present.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+namespace cc {
+
+struct NcclApi {
+  bool ok = false;
+  const char *why = "not loaded";
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi &nccl();
+
+}  // namespace cc
