@@ -120,6 +120,8 @@ struct cc_ctx {
   size_t ev_used = 0;
   bool profile = true;
   size_t cur_bytes = 0, peak_bytes = 0;
+  cudaEvent_t ev_color[2] = {nullptr, nullptr};
+  double color_ms = 0;
 
   int elem() const { return opt.precision == CC_FP64 ? 8 : 4; }
   int64_t ld_of(int W) const { return round_up(std::max(W, 1), 32 / elem()); }
@@ -383,8 +385,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump_o
         hist = c->amalloc(hist_bytes, c->s_main);
         cudaEvent_t b;
         c->begin(PH_HIST, c->s_main, &b);
-        c->stats[3] += launch_hist(elem, c->d_rp, c->d_col, c->d_colors, n, k, hist, c->ld_of(k), c->num_sms,
-                                   c->s_main);
+        c->stats[3] += launch_hist(elem, c->d_rp, c->d_rp + 1, c->d_col, c->d_colors, c->w_full.view(), n, k, hist,
+                                   c->ld_of(k), c->num_sms, c->s_main);
         c->check_launch();
         c->end(PH_HIST, c->s_main, b);
         const double nnz = (double)c->part.col.size();
@@ -592,6 +594,8 @@ void cc_destroy(cc_ctx *c) {
   if (c->comm) cc::nccl().CommDestroy(c->comm);
   for (void *p : c->persistent) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto e : c->ev_color)
+    if (e) cudaEventDestroy(e);
   if (c->s_main) cudaStreamDestroy(c->s_main);
   if (c->s_comm) cudaStreamDestroy(c->s_comm);
   delete c;
@@ -628,14 +632,12 @@ cc_status cc_load_graph(cc_ctx *c, int64_t n, const int64_t *row_ptr, const int3
   c->d_orig = c->pupload(orig);
   c->d_colors = c->pmalloc<uint8_t>((size_t)std::max<int64_t>(c->n_crow, 1));
   std::vector<int64_t> beg(R.rp.begin(), R.rp.end() - (R.rp.empty() ? 0 : 1)), end(R.rp.begin() + (R.rp.empty() ? 0 : 1), R.rp.end());
-  if (c->opt.world == 1) {
-    build_work(c, beg, end, false, c->w_full);
-  } else {
+  build_work(c, beg, end, false, c->w_full);  // world 1: the one pass; any world: the colour histogram
+  if (c->opt.world > 1) {
     c->d_mid = c->pupload(R.mid);
     c->d_send_idx = c->pupload(R.send_idx);
     build_work(c, beg, R.mid, false, c->w_local);
     build_work(c, R.mid, end, true, c->w_remote);
-    c->w_full.nnz = c->w_local.nnz + c->w_remote.nnz;
   }
   c->has_graph = true;
   if (had_template) {
@@ -658,11 +660,18 @@ cc_status cc_set_template(cc_ctx *c, int32_t k, const int32_t *parent) {
 cc_status cc_color(cc_ctx *c, uint64_t seed) {
   API_BEGIN(c)
   if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_color needs a graph and a template");
-  cudaEvent_t b;
-  c->begin(PH_COLOR, c->s_main, &b);
+  if (!c->ev_color[0]) {
+    CUDA_OK(cudaEventCreate(&c->ev_color[0]));
+    CUDA_OK(cudaEventCreate(&c->ev_color[1]));
+  }
+  CUDA_OK(cudaEventRecord(c->ev_color[0], c->s_main));
   cc::dev::launch_color(c->d_orig, c->n_crow, seed, c->plan.k, c->d_colors, c->s_main);
   c->check_launch();
+  CUDA_OK(cudaEventRecord(c->ev_color[1], c->s_main));
   CUDA_OK(cudaStreamSynchronize(c->s_main));
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, c->ev_color[0], c->ev_color[1]));
+  c->color_ms = ms;
   c->has_colors = true;
   API_END(c)
 }
@@ -772,6 +781,7 @@ cc_status cc_last_profile(cc_ctx *c, double *ms, int32_t cap, int32_t *n) {
   if (!c || !ms) return CC_ERR_ARG;
   const int m = std::min<int>(cap, PH_N + 1);
   for (int i = 0; i < m; ++i) ms[i] = c->prof[i];
+  if (m > 1 + PH_COLOR) ms[1 + PH_COLOR] = c->color_ms;
   if (n) *n = m;
   return CC_OK;
 }

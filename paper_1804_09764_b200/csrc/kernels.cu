@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -92,22 +93,45 @@ __global__ void k_color(const int32_t *__restrict__ orig, int64_t n, uint64_t se
 }
 
 // ------------------------------------------------------------------ hist
+// Work items as in k_agg (light vertices, segments of heavy neighbour lists).
+// Segment partial counts are added with atomics into a zeroed row: the values
+// are small integers, exact in fp32/fp64, so the result is order-independent.
 template <typename T, int G>
-__global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                                              const uint8_t *__restrict__ colors, int64_t n, int k,
-                                              T *__restrict__ out, int64_t ld) {
+__global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+                                              const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
+                                              AggWork work, int k, T *__restrict__ out, int64_t ld) {
+  constexpr int U = 4;
   const int lane = threadIdx.x & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; v < n; v += ngroups) {
+  const int64_t n_items = work.n_seg + work.n_light;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
+    const bool heavy = it < work.n_seg;
+    int64_t b, e;
+    int32_t v;
+    if (heavy) {
+      v = work.seg_v[it];
+      b = work.seg_b[it];
+      e = work.seg_e[it];
+    } else {
+      v = work.light[it - work.n_seg];
+      b = beg[v];
+      e = end[v];
+    }
     int cnt[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) cnt[j] = 0;
-    const int64_t e1 = rp[v + 1];
-    for (int64_t e = rp[v] + lane; e < e1; e += G) {
-      const int c = colors[__ldg(col + e)];
+    for (int64_t e0 = b + lane; e0 < e; e0 += G * U) {
+      int32_t u[U];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) cnt[j] += (c == j);
+      for (int q = 0; q < U; ++q) u[q] = e0 + q * G < e ? __ldg(col + e0 + q * G) : -1;
+      int c[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) c[q] = u[q] >= 0 ? (int)colors[u[q]] : 16;
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cnt[j] += (c[q] == j);
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -115,13 +139,16 @@ __global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ rp, co
       for (int o = G / 2; o > 0; o >>= 1) cnt[j] += __shfl_xor_sync(gmask, cnt[j], o, G);
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (j % G == lane && j < k) out[v * ld + j] = (T)cnt[j];
+      if (j % G == lane && j < k) {
+        if (heavy) atomicAdd(out + (int64_t)v * ld + j, (T)cnt[j]);
+        else out[(int64_t)v * ld + j] = (T)cnt[j];
+      }
   }
 }
 
 // ------------------------------------------------------------------ aggregation
-template <typename T, int G, int NV, int U>
-__global__ void __launch_bounds__(256) k_agg(AggArgs a, int nchunks, int CW) {
+template <typename T, int G, int NV, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_agg(AggArgs a, int nchunks, int CW) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   const int lane = threadIdx.x & (G - 1);
@@ -150,7 +177,7 @@ __global__ void __launch_bounds__(256) k_agg(AggArgs a, int nchunks, int CW) {
     const int c0 = chunk * CW + lane * VW;
     bool valid[NV];
 #pragma unroll
-    for (int j = 0; j < NV; ++j) valid[j] = c0 + j * G * VW < a.W;
+    for (int j = 0; j < NV; ++j) valid[j] = (lane * VW + j * G * VW < CW) && (c0 + j * G * VW < a.W);
     double acc[NV][VW];
 #pragma unroll
     for (int j = 0; j < NV; ++j)
@@ -361,13 +388,18 @@ int persistent_grid(K kernel, int threads, size_t smem, int num_sms) {
   return per_sm * num_sms;
 }
 
-template <typename T, int G, int NV>
+template <typename T, int G, int NV, int U = (G * NV >= 32) ? 8 : 4, int MINB = 1>
 void agg_go(const AggArgs &a, int nchunks, int CW, int num_sms, cudaStream_t s) {
-  constexpr int U = (G * NV >= 32) ? 8 : 4;
-  auto kern = k_agg<T, G, NV, U>;
+  auto kern = k_agg<T, G, NV, U, MINB>;
   static int grid = 0;
   if (!grid) grid = persistent_grid(kern, 256, 0, num_sms);
   kern<<<grid, 256, 0, s>>>(a, nchunks, CW);
+}
+
+// Tuning variants of the wide-row kernel (G = 32), selected by CC_AGG_VARIANT.
+int agg_variant() {
+  const char *e = getenv("CC_AGG_VARIANT");
+  return e ? atoi(e) : 0;
 }
 
 void agg_shape(int VW, int W, int64_t chunk_cols, int *G, int *NV) {
@@ -380,21 +412,39 @@ void agg_shape(int VW, int W, int64_t chunk_cols, int *G, int *NV) {
   if (chunk_cols > 0 && *G == 32) *NV = chunk_cols > 32 * VW ? 2 : 1;  // explicit chunk width
 }
 
+// Balanced column chunks: as few passes as the group's capacity allows, with
+// equal widths (a multiple of the vector width), so no pass runs nearly empty.
+void agg_chunking(int VW, int W, int cap, int *CW, int *nchunks) {
+  *nchunks = (W + cap - 1) / cap;
+  if (*nchunks < 1) *nchunks = 1;
+  const int per = (W + *nchunks - 1) / *nchunks;
+  *CW = (per + VW - 1) / VW * VW;
+}
+
 template <typename T>
 int agg_typed(const AggArgs &a, int64_t chunk_cols, int num_sms, int *nchunks_out, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
-  int G, NV;
+  int G, NV, CW, nchunks;
   agg_shape(VW, a.W, chunk_cols, &G, &NV);
-  const int CW = G * NV * VW;
-  const int nchunks = (a.W + CW - 1) / CW;
+  agg_chunking(VW, a.W, G * NV * VW, &CW, &nchunks);
   if (nchunks_out) *nchunks_out = nchunks;
   if (a.work.n_seg + a.work.n_light == 0) return 0;
   switch (G * 10 + NV) {
     case 41: agg_go<T, 4, 1>(a, nchunks, CW, num_sms, s); break;
     case 81: agg_go<T, 8, 1>(a, nchunks, CW, num_sms, s); break;
     case 161: agg_go<T, 16, 1>(a, nchunks, CW, num_sms, s); break;
-    case 321: agg_go<T, 32, 1>(a, nchunks, CW, num_sms, s); break;
-    default: agg_go<T, 32, 2>(a, nchunks, CW, num_sms, s); break;
+    case 321:
+      if (agg_variant() == 3) agg_go<T, 32, 1, 16>(a, nchunks, CW, num_sms, s);
+      else agg_go<T, 32, 1>(a, nchunks, CW, num_sms, s);
+      break;
+    default:
+      switch (agg_variant()) {
+        case 1: agg_go<T, 32, 2, 4>(a, nchunks, CW, num_sms, s); break;
+        case 2: agg_go<T, 32, 2, 4, 2>(a, nchunks, CW, num_sms, s); break;
+        case 5: agg_go<T, 32, 2>(a, nchunks, CW, num_sms, s); break;
+        default: agg_go<T, 32, 2, 8, 2>(a, nchunks, CW, num_sms, s); break;  // measured best (config 3)
+      }
+      break;
   }
   return 1;
 }
@@ -432,10 +482,10 @@ int agg_partials_blocks(int num_sms) { return num_sms * 8; }
 
 int agg_nchunks(int elem, int W, int64_t chunk_cols) {
   const int VW = elem == 8 ? 2 : 4;
-  int G, NV;
+  int G, NV, CW, nchunks;
   agg_shape(VW, W, chunk_cols, &G, &NV);
-  const int CW = G * NV * VW;
-  return (W + CW - 1) / CW;
+  agg_chunking(VW, W, G * NV * VW, &CW, &nchunks);
+  return nchunks;
 }
 
 int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *out, cudaStream_t s) {
@@ -445,19 +495,24 @@ int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *
   return 1;
 }
 
-int launch_hist(int elem, const int64_t *rp, const int32_t *col, const uint8_t *colors, int64_t n, int k, void *out,
-                int64_t ld, int num_sms, cudaStream_t s) {
-  if (n == 0) return 0;
+int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
+                const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s) {
+  if (work.n_seg + work.n_light == 0) return 0;
+  int launches = 1;
+  if (work.n_seg) {  // heavy rows accumulate segment counts atomically
+    cudaMemsetAsync(out, 0, (size_t)n * ld * elem, s);
+    ++launches;
+  }
   if (elem == 8) {
     static int grid = 0;
     if (!grid) grid = persistent_grid(k_hist<double, 8>, 256, 0, num_sms);
-    k_hist<double, 8><<<grid, 256, 0, s>>>(rp, col, colors, n, k, static_cast<double *>(out), ld);
+    k_hist<double, 8><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, static_cast<double *>(out), ld);
   } else {
     static int grid = 0;
     if (!grid) grid = persistent_grid(k_hist<float, 8>, 256, 0, num_sms);
-    k_hist<float, 8><<<grid, 256, 0, s>>>(rp, col, colors, n, k, static_cast<float *>(out), ld);
+    k_hist<float, 8><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, static_cast<float *>(out), ld);
   }
-  return 1;
+  return launches;
 }
 
 int launch_agg(int elem, const AggArgs &a, int64_t chunk_cols, int num_sms, int *nchunks_out, cudaStream_t s) {

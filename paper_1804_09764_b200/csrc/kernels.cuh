@@ -43,8 +43,8 @@ struct AggArgs {
 
 // Launchers.  `elem` = sizeof(T) (8 or 4).  Return the number of launches.
 int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *out, cudaStream_t s);
-int launch_hist(int elem, const int64_t *rp, const int32_t *col, const uint8_t *colors, int64_t n, int k,
-                void *out, int64_t ld, int num_sms, cudaStream_t s);
+int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
+                const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s);
 // Aggregation: chooses group width / chunking from W and chunk_cols.
 int launch_agg(int elem, const AggArgs &a, int64_t chunk_cols, int num_sms, int *nchunks_out,
                cudaStream_t s);

@@ -1,0 +1,289 @@
+"""-m gpu: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star):
+  * colouring: bit-exact (integer work);
+  * fp64 mode: every table entry within relative 1e-12, zero entries exactly
+    zero; bit-exact on configs[0] (integers < 2^53);
+  * fp32 mode: final colourful count within relative 1e-4.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import assert_close_entries, context, count, lib, rel_err, subtree_sizes, tables
+
+pytestmark = pytest.mark.gpu
+
+TOL_FP64 = 1e-12
+TOL_FP32 = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def oracle_tables(g, parent, col, numtype):
+    k = len(parent)
+    out = {}
+    sizes = subtree_sizes(parent)
+    for x in range(k):
+        if parent[x] == -1:
+            r = oracle.dp_count(g, parent, col, numtype, want_root=True)
+            out[x] = r.root.reshape(-1, 1)
+        else:
+            out[x] = oracle.dp_count(g, parent, col, numtype, keep_x=x).table
+        assert out[x].shape[1] == math.comb(k, sizes[x] if parent[x] != -1 else k)
+    return out
+
+
+# ------------------------------------------------------------------ colouring
+def test_colouring_bit_exact_vs_oracle():
+    cc = lib()
+    for n, k, seed in ((1000, 5, 2), (65_536, 7, 2), (1_000_003, 12, 123456789), (70_000, 16, 2 ** 63 + 5)):
+        g = synth.cycle(n)
+        with context(g, list(range(-1, k - 1))) as ctx:
+            cc.cc_color(ctx, seed)
+            got = cc.cc_get_colors(ctx, n)
+        assert np.array_equal(got, oracle.color(n, k, seed)), (n, k, seed)
+
+
+def test_colouring_includes_isolated_vertices():
+    cc = lib()
+    g = synth.from_edges(10, [(0, 1), (5, 6)])
+    with context(g, [-1, 0, 1]) as ctx:
+        cc.cc_color(ctx, 9)
+        assert np.array_equal(cc.cc_get_colors(ctx, 10), oracle.color(10, 3, 9))
+
+
+# ------------------------------------------------------------------ configs[0]: bit-exact
+def test_config0_bit_exact_count_and_every_table():
+    cfg = synth.CONFIGS[0]
+    g = cfg.graph()
+    col = oracle.color(g.n, cfg.k, cfg.color_seed)
+    want = oracle.dp_count(g, cfg.parent, col, oracle.NUM_EXACT).total
+    assert count(g, cfg.parent, seed=cfg.color_seed) == float(want)
+    got = tables(g, cfg.parent, col)
+    ref = oracle_tables(g, cfg.parent, col, oracle.NUM_EXACT)
+    for x in range(cfg.k):
+        assert np.array_equal(got[x], ref[x]), f"table of template vertex {x}"
+
+
+# ------------------------------------------------------------------ small-graph suite, exact
+def _small_suite():
+    rng = np.random.default_rng(1234)
+    cases = []
+    for trial in range(30):
+        k = int(rng.integers(2, 9))
+        n = int(rng.integers(k, 40))
+        g = synth.gnp(n, float(rng.choice([0.1, 0.3, 0.7])), int(rng.integers(1 << 30)))
+        parent = [-1] + [int(rng.integers(0, i)) for i in range(1, k)]
+        perm = rng.permutation(k)
+        relab = [-1] * k
+        for x in range(k):
+            relab[perm[x]] = -1 if parent[x] < 0 else int(perm[parent[x]])
+        col = rng.integers(0, k, n).astype(np.uint8)
+        cases.append((g, relab, col))
+    return cases
+
+
+def test_small_suite_every_table_exact():
+    for g, parent, col in _small_suite():
+        got = tables(g, parent, col)
+        ref = oracle_tables(g, parent, col, oracle.NUM_EXACT)
+        for x in range(len(parent)):
+            assert np.array_equal(got[x], ref[x]), (parent, x)
+
+
+def test_small_suite_heavy_segments_and_chunks_do_not_change_results():
+    for g, parent, col in _small_suite()[:10]:
+        want = float(oracle.dp_count(g, parent, col, oracle.NUM_EXACT).total)
+        for seg in (1, 2, 3):
+            assert count(g, parent, colors=col, segment_len=seg) == want
+        assert count(g, parent, colors=col, precision="fp32") == pytest.approx(want, rel=TOL_FP32)
+
+
+# ------------------------------------------------------------------ configs[1]: fp64 1e-12 per entry, fp32 1e-4
+def test_config1_fp64_every_entry_and_fp32_total():
+    cfg = synth.CONFIGS[1]
+    g = cfg.graph()
+    col = oracle.color(g.n, cfg.k, cfg.color_seed)
+    ref = oracle_tables(g, cfg.parent, col, oracle.NUM_EXACT)
+    got = tables(g, cfg.parent, col)
+    for x in range(cfg.k):
+        assert_close_entries(got[x], ref[x], TOL_FP64, f"config1 x={x}")
+    want = oracle.dp_count(g, cfg.parent, col, oracle.NUM_EXACT).total
+    assert rel_err(count(g, cfg.parent, seed=cfg.color_seed), want) <= TOL_FP64
+    assert rel_err(count(g, cfg.parent, seed=cfg.color_seed, precision="fp32"), want) <= TOL_FP32
+    # heavy split forced (max degree ~9.6K) and narrow chunks: same result
+    x1 = count(g, cfg.parent, seed=cfg.color_seed, segment_len=64)
+    assert rel_err(x1, want) <= TOL_FP64
+
+
+# ------------------------------------------------------------------ twins of configs 2-4 (oracle-sized)
+@pytest.mark.parametrize("ci,scale,ef", [(2, 14, 16), (3, 13, 32), (4, 11, 64)])
+def test_config_twins_fp64_every_entry(ci, scale, ef):
+    cfg = synth.scaled_twin(synth.CONFIGS[ci], scale, ef)
+    g = cfg.graph()
+    col = oracle.color(g.n, cfg.k, cfg.color_seed)
+    ref = oracle_tables(g, cfg.parent, col, oracle.NUM_LONGDOUBLE)
+    got = tables(g, cfg.parent, col, segment_len=256)
+    for x in range(cfg.k):
+        assert_close_entries(got[x], ref[x], TOL_FP64, f"{cfg.name} x={x}")
+
+
+@pytest.mark.parametrize("ci,scale,ef", [(2, 16, 16), (3, 14, 32), (4, 12, 64)])
+def test_config_twins_fp32_total(ci, scale, ef):
+    cfg = synth.scaled_twin(synth.CONFIGS[ci], scale, ef)
+    g = cfg.graph()
+    col = oracle.color(g.n, cfg.k, cfg.color_seed)
+    want = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE).total
+    assert rel_err(count(g, cfg.parent, seed=cfg.color_seed, precision="fp32"), want) <= TOL_FP32
+    assert rel_err(count(g, cfg.parent, seed=cfg.color_seed, precision="fp64"), want) <= TOL_FP64
+
+
+# ------------------------------------------------------------------ configs[2] at full size
+def test_config2_full_fp32_two_colourings():
+    cfg = synth.CONFIGS[2]
+    g = cfg.graph()
+    cc = lib()
+    with context(g, cfg.parent, "fp32") as ctx:
+        for seed in (cfg.color_seed, cfg.color_seed + 1):
+            cc.cc_color(ctx, seed)
+            x = cc.cc_count_colorful(ctx)
+            want = oracle.dp_count(g, cfg.parent, oracle.color(g.n, cfg.k, seed), oracle.NUM_DOUBLE).total
+            assert rel_err(x, want) <= TOL_FP32, seed
+
+
+# ------------------------------------------------------------------ closed forms at any size
+def test_star_closed_form_full_config3_graph():
+    """X(star with k-1 leaves) = (k-1)! sum_v prod_{j != c_v} cnt_j(v) (SURVEY 8(c) pins)."""
+    g = synth.CONFIGS[3].graph()
+    k = 5
+    col = oracle.color(g.n, k, 77)
+    src = np.repeat(np.arange(g.n), g.degrees())
+    lin = src.astype(np.int64) * k + col[g.col]
+    cnt = np.bincount(lin, minlength=g.n * k).reshape(g.n, k).astype(np.float64)
+    cnt[np.arange(g.n), col] = 1.0
+    want = math.factorial(k - 1) * float(np.sum(np.prod(cnt, axis=1) * (g.degrees() > 0)))
+    got = count(g, [-1] + [0] * (k - 1), seed=77, precision="fp64")
+    assert rel_err(got, want) <= 1e-12
+
+
+def test_clique_every_entry_closed_form():
+    n = 300
+    g = synth.clique(n)
+    cfg = synth.CONFIGS[2]
+    k = cfg.k
+    col = oracle.color(n, k, 5)
+    c = np.bincount(col, minlength=k).astype(np.float64)
+    x = count(g, cfg.parent, colors=col)
+    assert rel_err(x, math.factorial(k) * float(np.prod(c))) <= 1e-12
+    got = tables(g, cfg.parent, col)
+    sizes = subtree_sizes(cfg.parent)
+    import itertools
+    for xv in (1, 2):
+        s = sizes[xv]
+        subsets = sorted(itertools.combinations(range(k), s), key=lambda t: t[::-1])
+        for v in (0, 7, 299):
+            want = [math.factorial(s - 1) * math.prod(c[j] - (j == col[v]) for j in S if j != col[v])
+                    if col[v] in S else 0.0 for S in subsets]
+            assert_close_entries(got[xv][v], want, 1e-12, f"clique x={xv} v={v}")
+
+
+def test_path_on_long_cycle():
+    # P_k on C_n with col = v mod k, k | n: every window is rainbow, X = 2n (SURVEY 8(c) pins)
+    n, k = 200_004, 6
+    g = synth.cycle(n)
+    col = (np.arange(n) % k).astype(np.uint8)
+    assert count(g, [-1] + list(range(k - 1)), colors=col) == 2 * n
+    # random colouring: X = 2 * #rainbow windows
+    rng = np.random.default_rng(8)
+    col = rng.integers(0, k, n).astype(np.uint8)
+    win = np.ones(n, dtype=bool)
+    for a in range(k):
+        for b in range(a + 1, k):
+            win &= col[(np.arange(n) + a) % n] != col[(np.arange(n) + b) % n]
+    assert count(g, [-1] + list(range(k - 1)), colors=col, segment_len=1) == 2 * int(win.sum())
+
+
+# ------------------------------------------------------------------ degenerate cases
+def test_degenerate_cases():
+    cc = lib()
+    # k = 1: X = n (including isolated vertices)
+    g = synth.from_edges(7, [(0, 1)])
+    assert count(g, [-1], seed=1) == 7.0
+    # k = 2: X = 2 * #bichromatic edges
+    g = synth.rmat(10, 8, seed=4)
+    col = oracle.color(g.n, 2, 3)
+    eu, ev = g.edges()
+    assert count(g, [-1, 0], colors=col) == 2 * int(np.sum(col[eu] != col[ev]))
+    # n < k, edgeless, empty graph
+    assert count(synth.path(3), [-1, 0, 1, 2], seed=1) == 0.0
+    assert count(synth.from_edges(50, []), [-1, 0, 1], seed=1) == 0.0
+    assert count(synth.from_edges(0, []), [-1, 0], seed=1) == 0.0
+    # monochrome colouring
+    assert count(synth.clique(6), [-1, 0, 1], colors=np.zeros(6, np.uint8)) == 0.0
+    # G = T with a rainbow colouring: X = |Aut(T)|
+    for cfg in synth.CONFIGS:
+        gt = synth.tree_graph(cfg.parent)
+        assert count(gt, cfg.parent, colors=np.arange(cfg.k, dtype=np.uint8)) == oracle.aut(cfg.parent)
+    # k = 16 (maximum)
+    par16 = [-1] + [(i - 1) // 2 for i in range(1, 16)]
+    g16 = synth.tree_graph(par16)
+    assert count(g16, par16, colors=np.arange(16, dtype=np.uint8)) == oracle.aut(par16)
+    with context(synth.cycle(5), [-1, 0]) as ctx:
+        aut, aut_root, ns = cc.cc_template_info(ctx)
+        assert (aut, aut_root, ns) == (2, 1, 1)
+
+
+def test_determinism_bitwise():
+    cfg = synth.CONFIGS[1]
+    g = cfg.graph()
+    xs = {count(g, cfg.parent, seed=5, precision="fp32") for _ in range(3)}
+    assert len(xs) == 1
+
+
+def test_estimator_matches_oracle_formula():
+    cc = lib()
+    g = synth.gnp(40, 0.3, 3)
+    parent = [-1, 0, 1, 1]
+    with context(g, parent) as ctx:
+        est, xs = cc.cc_estimate(ctx, 50, 1000, per_iter=True)
+    want_x = [oracle.dp_count(g, parent, oracle.color(g.n, 4, 1000 + j), oracle.NUM_EXACT).total for j in range(50)]
+    assert list(xs) == [float(v) for v in want_x]
+    assert est == pytest.approx(oracle.estimate(want_x, 4, oracle.aut(parent)), rel=1e-14)
+
+
+# ------------------------------------------------------------------ errors
+def test_errors_are_reported():
+    cc = lib()
+    ctx = cc.cc_create(device=0)
+    try:
+        with pytest.raises(cc.CCError) as e:
+            cc.cc_count_colorful(ctx)
+        assert e.value.status == cc.CC_ERR_STATE
+        bad = synth.from_edges(3, [(0, 1)])
+        col = bad.col.copy()
+        col[0] = 2  # 0 -> 2 but 2 has no 0: asymmetric
+        with pytest.raises(cc.CCError) as e:
+            cc.cc_load_graph(ctx, 3, bad.row_ptr, col)
+        assert e.value.status == cc.CC_ERR_GRAPH
+        with pytest.raises(cc.CCError) as e:
+            cc.cc_load_graph(ctx, 2, np.array([0, 1, 2]), np.array([0, 1], np.int32))  # self-loops
+        assert e.value.status == cc.CC_ERR_GRAPH
+        with pytest.raises(cc.CCError) as e:
+            cc.cc_load_graph(ctx, 2, np.array([0, 2, 3]), np.array([1, 1, 0], np.int32))  # duplicate
+        assert e.value.status == cc.CC_ERR_GRAPH
+        for par in ([0, -1, 5], [-1, -1], [1, 0], list(range(-1, 16))):
+            with pytest.raises(cc.CCError) as e:
+                cc.cc_set_template(ctx, par)
+            assert e.value.status == cc.CC_ERR_TEMPLATE
+    finally:
+        cc.cc_destroy(ctx)

@@ -1,0 +1,141 @@
+"""-m "not gpu": host-side logic of the product library (no GPU needed):
+the C ABI loads and exports every symbol of include/cc.h; colex indexing,
+split tables, the template planner and the 1D partition are checked against
+definitions, the paper's Table 3, and the oracle's independent |Aut(T)|."""
+import itertools
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def cc():
+    import __graft_entry__
+    __graft_entry__._product_build()
+    import paper_1804_09764_b200 as cc
+    return cc
+
+
+def test_library_exports_every_header_symbol(cc):
+    hdr = open(os.path.join(ROOT, "include", "cc.h")).read()
+    declared = set(re.findall(r"\b(cc_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations found"
+    from paper_1804_09764_b200 import _native
+    assert declared == set(_native.SIGNATURES), declared ^ set(_native.SIGNATURES)
+    for name in declared:
+        assert hasattr(_native.lib, name), name
+
+
+def test_colex_rank_examples_and_bijection(cc):
+    # SPEC colex examples: k=3, s=2: {0,1}->0, {0,2}->1, {1,2}->2
+    assert [cc.cc_colex_rank(m) for m in (0b011, 0b101, 0b110)] == [0, 1, 2]
+    assert cc.cc_colex_rank(0b11111) == 0  # full set has rank 0
+    for k in (5, 9, 12):
+        for s in range(0, k + 1):
+            masks = sorted(m for m in range(1 << k) if bin(m).count("1") == s)  # colex = increasing mask
+            assert [cc.cc_colex_rank(m) for m in masks] == list(range(len(masks)))
+            assert [cc.cc_colex_unrank(s, r) for r in range(len(masks))] == masks
+    # complement reverses colex order when t = k/2 (SURVEY 8(f) F3 check)
+    k = 8
+    masks = sorted(m for m in range(1 << k) if bin(m).count("1") == 4)
+    full = (1 << k) - 1
+    assert [cc.cc_colex_rank(full ^ m) for m in masks] == list(range(len(masks)))[::-1]
+
+
+def test_split_tables_are_exactly_the_disjoint_splits(cc):
+    for k, t, a in ((5, 3, 1), (7, 5, 3), (12, 7, 4), (10, 10, 7), (15, 8, 1)):
+        tab = cc.cc_split_table(k, t, a)
+        assert tab.shape == (math.comb(t, a), math.comb(k, t))
+        sets = {s: sorted(m for m in range(1 << k) if bin(m).count("1") == s) for s in (t, a, t - a)}
+        for r in range(0, math.comb(k, t), max(1, math.comb(k, t) // 50)):
+            S = sets[t][r]
+            pairs = {(sets[a][p & 0xFFFF], sets[t - a][p >> 16]) for p in tab[:, r].tolist()}
+            want = {(X, S ^ X) for X in sets[a] if X & S == X}
+            assert pairs == want
+
+
+def test_plans_of_the_configs(cc):
+    want = [
+        [(2, 1, 1), (3, 1, 2), (4, 1, 3), (5, 1, 4)],
+        [(2, 1, 1), (3, 1, 2), (5, 3, 2), (7, 5, 2)],
+        [(2, 1, 1), (3, 1, 2), (4, 1, 3), (7, 4, 3), (10, 7, 3)],
+        [(2, 1, 1), (3, 2, 1), (4, 1, 3), (7, 4, 3), (8, 1, 7), (3, 1, 2), (4, 3, 1), (12, 8, 4)],
+        [(2, 1, 1), (3, 2, 1), (4, 1, 3), (7, 4, 3), (8, 1, 7), (15, 8, 7)],
+    ]
+    for cfg, w in zip(synth.CONFIGS, want):
+        p = cc.cc_plan_template(cfg.parent)
+        assert [(s["t"], s["a"], s["p"]) for s in p["steps"]] == w
+        assert p["aut"] == oracle.aut(cfg.parent)
+        # every step: t = a + p, the root step is last, tables used after being produced
+        made = set()
+        for i, s in enumerate(p["steps"]):
+            assert s["t"] == s["a"] + s["p"]
+            for tid in (s["active"], s["passive"]):
+                assert tid == -1 or tid in made
+            if s["out"] >= 0:
+                made.add(s["out"])
+            else:
+                assert i == len(p["steps"]) - 1 and s["t"] == cfg.k
+
+
+def test_table3_memory_and_computation(cc):
+    # PAPER.md Table 3 (lines 587-596): u3-1 3/6 (intensity 2), u5-2 25/70 (2.8)
+    for par, mem, comp in (([-1, 0, 1], 3, 6), ([-1, 0, 1, 2, 3], 25, 70)):
+        p = cc.cc_plan_template(par)
+        assert (p["memory"], p["computation"]) == (mem, comp)
+
+
+def test_aut_matches_oracle_on_all_small_trees(cc):
+    for k in range(1, 8):
+        for choice in itertools.islice(itertools.product(*[range(i) for i in range(1, k)]), 0, None, 3):
+            par = [-1] + list(choice)
+            p = cc.cc_plan_template(par)
+            assert p["aut"] == oracle.aut(par), par
+
+
+def test_template_validation(cc):
+    for bad in ([0, -1, 5], [-1, -1], [1, 0], [-1, 2, 1], list(range(-1, 16))):
+        with pytest.raises(cc.CCError) as e:
+            cc.cc_plan_template(bad)
+        assert e.value.status in (cc.CC_ERR_TEMPLATE, cc.CC_ERR_ARG)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_partition_invariants(cc, world):
+    g = synth.rmat(12, 16, seed=2)
+    deg = g.degrees()
+    nz = set(np.nonzero(deg)[0].tolist())
+    plans = [cc.cc_partition_plan(g.n, g.row_ptr, g.col, world, r) for r in range(world)]
+    owned = np.concatenate([p["own_orig"] for p in plans])
+    assert sorted(owned.tolist()) == sorted(nz)                     # disjoint cover of non-isolated
+    owner = {int(v): r for r, p in enumerate(plans) for v in p["own_orig"]}
+    adj_total = sum(int(deg[p["own_orig"]].sum()) for p in plans)
+    assert adj_total == g.nnz
+    loads = [int(deg[p["own_orig"]].sum()) + 16 * len(p["own_orig"]) for p in plans]
+    assert max(loads) <= 1.25 * (sum(loads) / world) + int(deg.max())   # balanced
+    for r, p in enumerate(plans):
+        n_own = len(p["own_orig"])
+        ids = np.concatenate([p["own_orig"], p["halo_orig"]])
+        # the local CSR is the global adjacency, relabelled
+        for i in range(0, n_own, max(1, n_own // 64)):
+            v = p["own_orig"][i]
+            loc = p["col"][p["rp"][i]:p["rp"][i + 1]]
+            assert sorted(ids[loc].tolist()) == sorted(g.neighbors(v).tolist())
+        # halo rows come from the peers, grouped; each peer's send list matches
+        for q in range(world):
+            recv = p["halo_orig"][p["recv_off"][q]:p["recv_off"][q + 1]]
+            assert all(owner[int(v)] == q for v in recv)
+            pq = plans[q]
+            sent = pq["own_orig"][pq["send_idx"][pq["send_off"][r]:pq["send_off"][r + 1]]]
+            assert np.array_equal(sent, recv)
+        # hubs first within the rank
+        d = deg[p["own_orig"]]
+        assert np.all(d[:-1] >= d[1:])
