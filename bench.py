@@ -219,7 +219,7 @@ def run_ours(args, cfg, rank, world, dist):
         x, prof = step(args.seed + j)
         xs.append(x)
         dev_ms.append(prof["total"] + prof["color"])
-        agg_ms.append(prof["aggregate"])
+        agg_ms.append(prof["gather"])
         stats = cc.cc_last_stats(ctx)
         last_prof = prof
     barrier()
@@ -272,7 +272,7 @@ def run_ours(args, cfg, rank, world, dist):
                            "l2": "tables of several GB per step >> 126 MB L2 (no flush needed)"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak if achieved else None, "traffic": None,
-                             "kernel": "k_agg (neighbour-sum SpMM gather)", "peak_source": peak_src,
+                             "kernel": "k_gather (neighbour-sum SpMM gather, colour-compressed rows)", "peak_source": peak_src,
                              "algorithmic_bytes_per_step": agg_bytes, "kernel_ms_per_step": agg_avg_ms},
                 "model_bytes_per_step": stats["model_bytes"],
                 "model_hbm_frac": stats["model_bytes"] / (ms_per_step * 1e-3) / 1e9 / peak,

@@ -1,0 +1,377 @@
+// api.cu -- the C ABI of include/cc.h: argument checks, state machine,
+// error conversion (no C++ exception crosses the boundary).
+#include <cstring>
+#include <memory>
+
+#include "ctx.h"
+
+using cc::Error;
+
+namespace {
+
+cc_status fail(cc_ctx *c, const Error &e) {
+  if (c) {
+    c->err = e.what();
+    if (e.status == CC_ERR_CUDA || e.status == CC_ERR_NCCL) c->poisoned = true;
+  }
+  return e.status;
+}
+
+#define API_BEGIN(c)                                             \
+  if (!(c)) return CC_ERR_ARG;                                   \
+  if ((c)->poisoned) {                                           \
+    (c)->err = "context poisoned by an earlier CUDA/NCCL error"; \
+    return CC_ERR_STATE;                                         \
+  }                                                              \
+  try {                                                          \
+    CUDA_OK(cudaSetDevice((c)->opt.device));
+#define API_END(c)                         \
+  }                                        \
+  catch (const Error &e) {                 \
+    return fail((c), e);                   \
+  }                                        \
+  catch (const std::bad_alloc &) {         \
+    (c)->err = "host allocation failed";   \
+    return CC_ERR_OOM;                     \
+  }                                        \
+  catch (const std::exception &e) {        \
+    (c)->err = e.what();                   \
+    return CC_ERR_ARG;                     \
+  }                                        \
+  (c)->err.clear();                        \
+  return CC_OK;
+
+void free_persistent(cc_ctx *c) {
+  for (void *p : c->persistent) cudaFree(p);
+  c->persistent.clear();
+  c->d_rp = c->d_mid = nullptr;
+  c->d_col = c->d_col_sorted = c->d_orig = c->d_send_idx = nullptr;
+  c->d_colors = nullptr;
+  c->p_full = c->p_local = c->p_remote = cc::Pass();
+  c->d_split.clear();
+  c->d_map.clear();
+  c->d_comp = nullptr;
+  c->d_partials = c->d_result = nullptr;
+  c->d_arrive = nullptr;
+  c->arrive_cap = 0;
+  c->max_hv = c->max_seg = 0;
+  c->has_graph = c->has_colors = c->sorted_valid = false;
+}
+
+void alloc_scratch(cc_ctx *c) {
+  c->n_partials = cc::dev::root_partials_blocks(c->num_sms);
+  c->d_partials = c->pmalloc<double>((size_t)c->n_partials);
+  c->d_result = c->pmalloc<double>(1);
+}
+
+// dense colex index (k-universe) -> compressed index of the row of colour c
+// (DESIGN.md "Data layout"); -1 if the set does not contain c
+int64_t compressed_index(uint32_t S, int c) {
+  if (!(S >> c & 1u)) return -1;
+  return cc::colex_rank(cc::squeeze(S & ~(1u << c), c));
+}
+
+}  // namespace
+
+extern "C" {
+
+cc_status cc_default_options(cc_options *opt) {
+  if (!opt) return CC_ERR_ARG;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->precision = CC_FP64;
+  opt->world = 1;
+  opt->use_graphs = 1;
+  opt->relabel_seed = 0x5eed;
+  return CC_OK;
+}
+
+cc_status cc_nccl_unique_id(void *out128) {
+  if (!out128) return CC_ERR_ARG;
+  auto &api = cc::nccl();
+  if (!api.ok) return CC_ERR_NCCL;
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return CC_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+  return CC_OK;
+}
+
+cc_status cc_create(const cc_options *opt, cc_ctx **out) {
+  if (!opt || !out) return CC_ERR_ARG;
+  if (opt->precision != CC_FP64 && opt->precision != CC_FP32) return CC_ERR_ARG;
+  if (opt->world < 1 || opt->world > 64 || opt->rank < 0 || opt->rank >= opt->world) return CC_ERR_ARG;
+  if (opt->world > 1 && !opt->nccl_id) return CC_ERR_ARG;
+  if (opt->chunk_cols < 0 || opt->segment_len < 0) return CC_ERR_ARG;
+  std::unique_ptr<cc_ctx> c(new cc_ctx());
+  c->opt = *opt;
+  c->opt.nccl_id = nullptr;
+  try {
+    CUDA_OK(cudaSetDevice(opt->device));
+    CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, opt->device));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, opt->device));
+    uint64_t thr = UINT64_MAX;
+    CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    alloc_scratch(c.get());
+    if (opt->world > 1) {
+      auto &api = cc::nccl();
+      if (!api.ok) throw Error(CC_ERR_NCCL, api.why);
+      ncclUniqueId id;
+      std::memcpy(&id, opt->nccl_id, sizeof(id));
+      NCCL_OK(api.CommInitRank(&c->comm, opt->world, id, opt->rank));
+    }
+  } catch (const Error &e) {
+    if (c->s_main) cudaStreamDestroy(c->s_main);
+    if (c->s_comm) cudaStreamDestroy(c->s_comm);
+    for (void *p : c->persistent) cudaFree(p);
+    return e.status;
+  }
+  *out = c.release();
+  return CC_OK;
+}
+
+void cc_destroy(cc_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->opt.device);
+  if (c->s_main) cudaStreamSynchronize(c->s_main);
+  if (c->s_comm) cudaStreamSynchronize(c->s_comm);
+  if (c->comm) cc::nccl().CommDestroy(c->comm);
+  for (void *p : c->persistent) cudaFree(p);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto e : c->ev_color)
+    if (e) cudaEventDestroy(e);
+  if (c->s_main) cudaStreamDestroy(c->s_main);
+  if (c->s_comm) cudaStreamDestroy(c->s_comm);
+  delete c;
+}
+
+const char *cc_last_error(const cc_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+cc_status cc_load_graph(cc_ctx *c, int64_t n, const int64_t *row_ptr, const int32_t *col) {
+  API_BEGIN(c)
+  cc::HostGraph g = cc::validate_graph(n, row_ptr, col);
+  CUDA_OK(cudaStreamSynchronize(c->s_main));
+  free_persistent(c);
+  alloc_scratch(c);
+  cc::load_graph(c, g);
+  if (c->has_template) cc::upload_template(c);
+  API_END(c)
+}
+
+cc_status cc_set_template(cc_ctx *c, int32_t k, const int32_t *parent) {
+  API_BEGIN(c)
+  cc::Plan p = cc::make_plan(k, parent);
+  c->plan = p;
+  c->has_template = true;
+  c->has_colors = false;
+  if (c->has_graph) cc::upload_template(c);
+  API_END(c)
+}
+
+cc_status cc_color(cc_ctx *c, uint64_t seed) {
+  API_BEGIN(c)
+  if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_color needs a graph and a template");
+  cc::launch_colouring(c, seed);
+  CUDA_OK(cudaStreamSynchronize(c->s_main));
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, c->ev_color[0], c->ev_color[1]));
+  c->color_ms = ms;
+  API_END(c)
+}
+
+cc_status cc_set_colors(cc_ctx *c, const uint8_t *colors) {
+  API_BEGIN(c)
+  if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_set_colors needs a graph and a template");
+  if (!colors && c->n_global) throw Error(CC_ERR_ARG, "colors is NULL");
+  const auto &R = c->part;
+  std::vector<uint8_t> h((size_t)c->n_crow);
+  for (int64_t i = 0; i < R.n_own; ++i) h[i] = colors[R.own_orig[i]];
+  for (int64_t i = 0; i < R.n_halo; ++i) h[R.n_own + i] = colors[R.halo_orig[i]];
+  for (size_t i = 0; i < R.iso_orig.size(); ++i) h[c->n_rows + i] = colors[R.iso_orig[i]];
+  for (auto x : h)
+    if (x >= c->plan.k) throw Error(CC_ERR_ARG, "colour out of [0, k)");
+  if (!h.empty()) CUDA_OK(cudaMemcpyAsync(c->d_colors, h.data(), h.size(), cudaMemcpyHostToDevice, c->s_main));
+  CUDA_OK(cudaStreamSynchronize(c->s_main));
+  c->has_colors = true;
+  c->sorted_valid = false;
+  API_END(c)
+}
+
+cc_status cc_get_colors(cc_ctx *c, uint8_t *colors) {
+  API_BEGIN(c)
+  if (!c->has_colors) throw Error(CC_ERR_STATE, "no colouring");
+  if (c->opt.world != 1) throw Error(CC_ERR_STATE, "cc_get_colors needs world == 1");
+  std::vector<uint8_t> h((size_t)c->n_crow);
+  if (!h.empty()) CUDA_OK(cudaMemcpy(h.data(), c->d_colors, h.size(), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < c->part.n_own; ++i) colors[c->part.own_orig[i]] = h[i];
+  for (size_t i = 0; i < c->part.iso_orig.size(); ++i) colors[c->part.iso_orig[i]] = h[c->n_rows + i];
+  API_END(c)
+}
+
+cc_status cc_count_colorful(cc_ctx *c, double *X) {
+  API_BEGIN(c)
+  if (!X) throw Error(CC_ERR_ARG, "output pointer is NULL");
+  if (!c->has_graph || !c->has_template || !c->has_colors)
+    throw Error(CC_ERR_STATE, "cc_count_colorful needs a graph, a template and a colouring");
+  cc::run_count(c, X, -1, nullptr, nullptr);
+  API_END(c)
+}
+
+cc_status cc_estimate(cc_ctx *c, int32_t iterations, uint64_t seed0, double *estimate, double *per_iter) {
+  API_BEGIN(c)
+  if (iterations < 1 || !estimate) throw Error(CC_ERR_ARG, "iterations >= 1 and estimate != NULL required");
+  if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_estimate needs a graph and a template");
+  long double mean = 0;
+  std::vector<double> xs((size_t)iterations);
+  for (int j = 0; j < iterations; ++j) {
+    cc::launch_colouring(c, seed0 + (uint64_t)j);
+    cc::run_count(c, &xs[j], -1, nullptr, nullptr);
+    mean += xs[j];
+  }
+  mean /= iterations;
+  long double scale = 1;  // k^k / k!
+  for (int i = 1; i <= c->plan.k; ++i) scale *= (long double)c->plan.k / i;
+  *estimate = (double)(mean * scale / (long double)c->plan.aut);
+  if (per_iter) std::copy(xs.begin(), xs.end(), per_iter);
+  API_END(c)
+}
+
+cc_status cc_template_info(cc_ctx *c, int64_t *aut, int64_t *aut_root, int32_t *n_steps) {
+  API_BEGIN(c)
+  if (!c->has_template) throw Error(CC_ERR_STATE, "no template");
+  if (aut) *aut = c->plan.aut;
+  if (aut_root) *aut_root = c->plan.aut_root;
+  if (n_steps) *n_steps = (int32_t)c->plan.steps.size();
+  API_END(c)
+}
+
+cc_status cc_get_subtree_counts(cc_ctx *c, int32_t x, double *out) {
+  API_BEGIN(c)
+  if (!c->has_graph || !c->has_template || !c->has_colors) throw Error(CC_ERR_STATE, "needs graph, template, colouring");
+  if (c->opt.world != 1) throw Error(CC_ERR_STATE, "cc_get_subtree_counts needs world == 1");
+  const auto &pl = c->plan;
+  if (x < 0 || x >= pl.k || !out) throw Error(CC_ERR_ARG, "bad template vertex or NULL output");
+  const auto &R = c->part;
+  const int k = pl.k;
+  const int tid = pl.full_table[x];
+  std::vector<uint8_t> col((size_t)c->n_crow);
+  if (!col.empty()) CUDA_OK(cudaMemcpy(col.data(), c->d_colors, col.size(), cudaMemcpyDeviceToHost));
+  double X = 0;
+  if (tid == -2) {  // root: per-vertex C(v, T, [k])
+    std::memset(out, 0, (size_t)c->n_global * sizeof(double));
+    if (k == 1) {
+      for (int64_t v = 0; v < c->n_global; ++v) out[v] = 1.0;
+    } else {
+      std::vector<double> root;
+      cc::run_count(c, &X, -1, nullptr, &root);
+      for (int64_t i = 0; i < R.n_own; ++i) out[R.own_orig[i]] = root[i];
+    }
+  } else if (tid == -1) {  // a leaf: the single-vertex table [S == {col v}]
+    std::memset(out, 0, (size_t)c->n_global * k * sizeof(double));
+    for (int64_t i = 0; i < R.n_own; ++i) out[(size_t)R.own_orig[i] * k + col[i]] = 1.0;
+    for (size_t i = 0; i < R.iso_orig.size(); ++i) out[(size_t)R.iso_orig[i] * k + col[c->n_rows + i]] = 1.0;
+  } else {  // decompress the table rows into the dense colex layout
+    std::vector<double> tab;
+    cc::run_count(c, &X, tid, &tab, nullptr);
+    const int s = pl.tables[tid].size;
+    const int64_t Wd = cc::binom(k, s), Wc = cc::binom(k - 1, s - 1);
+    std::memset(out, 0, (size_t)c->n_global * Wd * sizeof(double));
+    std::vector<uint32_t> sets((size_t)Wd);
+    for (int64_t r = 0; r < Wd; ++r) sets[r] = cc::colex_unrank(s, r);
+    for (int64_t i = 0; i < R.n_own; ++i) {
+      double *row = out + (size_t)R.own_orig[i] * Wd;
+      for (int64_t r = 0; r < Wd; ++r) {
+        const int64_t ci = compressed_index(sets[r], col[i]);
+        if (ci >= 0) row[r] = tab[(size_t)i * Wc + ci];
+      }
+    }
+  }
+  API_END(c)
+}
+
+cc_status cc_last_profile(cc_ctx *c, double *ms, int32_t cap, int32_t *n) {
+  if (!c || !ms) return CC_ERR_ARG;
+  const int m = std::min<int>(cap, cc::PH_N + 1);
+  for (int i = 0; i < m; ++i) ms[i] = c->prof[i];
+  if (m > 1 + cc::PH_COLOR) ms[1 + cc::PH_COLOR] = c->color_ms;
+  if (n) *n = m;
+  return CC_OK;
+}
+
+cc_status cc_last_stats(cc_ctx *c, double *out, int32_t cap) {
+  if (!c || !out || cap < 5) return CC_ERR_ARG;
+  for (int i = 0; i < 5; ++i) out[i] = c->stats[i];
+  return CC_OK;
+}
+
+// ---------------------------------------------------------------- host-only
+int64_t cc_colex_rank(uint32_t mask) { return mask >> cc::kMaxK ? -1 : cc::colex_rank(mask); }
+
+uint32_t cc_colex_unrank(int32_t s, int64_t r) {
+  if (s < 0 || s > cc::kMaxK || r < 0 || r >= cc::binom(cc::kMaxK, s)) return 0xFFFFFFFFu;
+  return cc::colex_unrank(s, r);
+}
+
+cc_status cc_split_table(int32_t k, int32_t t, int32_t a, uint32_t *out, int64_t cap) {
+  if (k < 1 || k > cc::kMaxK || t < 2 || t > k || a < 1 || a >= t || !out) return CC_ERR_ARG;
+  auto tab = cc::split_table(k, t, a);
+  if ((int64_t)tab.size() > cap) return CC_ERR_ARG;
+  std::copy(tab.begin(), tab.end(), out);
+  return CC_OK;
+}
+
+cc_status cc_plan_template(int32_t k, const int32_t *parent, int32_t *steps_out, int32_t cap_steps, int32_t *n_steps,
+                           int64_t *aut, int64_t *aut_root, double *memory, double *computation) {
+  try {
+    cc::Plan p = cc::make_plan(k, parent);
+    if (n_steps) *n_steps = (int32_t)p.steps.size();
+    if (steps_out) {
+      if (cap_steps < (int32_t)p.steps.size()) return CC_ERR_ARG;
+      for (size_t s = 0; s < p.steps.size(); ++s) {
+        const auto &st = p.steps[s];
+        int32_t *o = steps_out + 6 * s;
+        o[0] = st.t;
+        o[1] = st.a;
+        o[2] = st.p;
+        o[3] = st.active;
+        o[4] = st.passive;
+        o[5] = st.out;
+      }
+    }
+    if (aut) *aut = p.aut;
+    if (aut_root) *aut_root = p.aut_root;
+    if (memory) *memory = p.memory;
+    if (computation) *computation = p.computation;
+  } catch (const Error &e) {
+    return e.status;
+  }
+  return CC_OK;
+}
+
+cc_status cc_partition_plan(int64_t n, const int64_t *row_ptr, const int32_t *col, int32_t world, int32_t rank,
+                            uint64_t relabel_seed, int64_t *sizes_out, int32_t *own_orig, int32_t *halo_orig,
+                            int64_t *recv_off, int64_t *send_off, int32_t *send_idx, int64_t *rp, int32_t *lcol) {
+  try {
+    if (!sizes_out) return CC_ERR_ARG;
+    cc::HostGraph g = cc::validate_graph(n, row_ptr, col);
+    cc::RankPart R = cc::partition_graph(g, world, rank, relabel_seed);
+    sizes_out[0] = R.n_own;
+    sizes_out[1] = R.n_halo;
+    sizes_out[2] = (int64_t)R.col.size();
+    sizes_out[3] = R.send_off.back();
+    if (own_orig) std::copy(R.own_orig.begin(), R.own_orig.end(), own_orig);
+    if (halo_orig) std::copy(R.halo_orig.begin(), R.halo_orig.end(), halo_orig);
+    if (recv_off) std::copy(R.recv_off.begin(), R.recv_off.end(), recv_off);
+    if (send_off) std::copy(R.send_off.begin(), R.send_off.end(), send_off);
+    if (send_idx) std::copy(R.send_idx.begin(), R.send_idx.end(), send_idx);
+    if (rp) std::copy(R.rp.begin(), R.rp.end(), rp);
+    if (lcol) std::copy(R.col.begin(), R.col.end(), lcol);
+  } catch (const Error &e) {
+    return e.status;
+  }
+  return CC_OK;
+}
+
+}  // extern "C"

@@ -74,6 +74,26 @@ std::vector<uint16_t> drop_table(int k, int t) {
   return out;
 }
 
+// sq_c: drop colour c from the universe (colours above c shift down by one);
+// us_c: its inverse (re-insert a gap at c).
+uint32_t squeeze(uint32_t mask, int c) { return (mask & ((1u << c) - 1u)) | ((mask >> (c + 1)) << c); }
+uint32_t unsqueeze(uint32_t mask, int c) { return (mask & ((1u << c) - 1u)) | ((mask >> c) << (c + 1)); }
+
+std::vector<uint16_t> gather_map(int k, int p) {
+  const int64_t w_in = binom(k - 1, p - 1);
+  std::vector<uint16_t> out((size_t)(k * k * w_in), 0xFFFF);
+  for (int cu = 0; cu < k; ++cu)
+    for (int cv = 0; cv < k; ++cv) {
+      if (cu == cv) continue;
+      for (int64_t r = 0; r < w_in; ++r) {
+        const uint32_t Y = unsqueeze(colex_unrank(p - 1, r), cu) | (1u << cu);  // u's colour set
+        if (Y >> cv & 1u) continue;                                             // meets v's colour
+        out[(size_t)((cu * k + cv) * w_in + r)] = (uint16_t)colex_rank(squeeze(Y, cv));
+      }
+    }
+  return out;
+}
+
 std::vector<uint16_t> complement_table(int k, int a) {
   const int64_t nX = binom(k, a);
   const uint32_t full = (k == 32) ? 0xFFFFFFFFu : ((1u << k) - 1u);

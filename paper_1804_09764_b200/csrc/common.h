@@ -32,6 +32,15 @@ std::vector<uint32_t> split_table(int k, int t, int a);
 std::vector<uint16_t> drop_table(int k, int t);
 // Complement table at the root: out[r] = rank([k] \ X) for X = unrank(a, r).
 std::vector<uint16_t> complement_table(int k, int a);
+// Colour-compressed layout: sq_c removes colour c
+// from the universe (higher colours shift down), us_c re-inserts it.
+uint32_t squeeze(uint32_t mask, int c);
+uint32_t unsqueeze(uint32_t mask, int c);
+// Gather map of a passive part of size p: for neighbour colour cu, vertex
+// colour cv and compressed index r of u's row (Y' = unrank(p-1, r) in the
+// (k-1)-universe of cu), out[(cu*k + cv) * C(k-1,p-1) + r] = rank of
+// sq_cv({cu} u us_cu(Y')) in C(k-1, p), or 0xFFFF if that set contains cv.
+std::vector<uint16_t> gather_map(int k, int p);
 
 // ---------------------------------------------------------------- plan.cpp
 // One DP step (t; a, p): T_out(v, S) = sum_{S1 u S2 = S} A(v, S1) N_P(v, S2),

@@ -1,0 +1,184 @@
+// ctx.h -- the library context (one per rank) and the executor interface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+#include "nccl_dl.h"
+
+#define CUDA_OK(expr)                                                                                  \
+  do {                                                                                                 \
+    cudaError_t e_ = (expr);                                                                           \
+    if (e_ != cudaSuccess)                                                                             \
+      throw cc::Error(e_ == cudaErrorMemoryAllocation ? CC_ERR_OOM : CC_ERR_CUDA,                      \
+                      std::string(#expr) + ": " + cudaGetErrorString(e_));                             \
+  } while (0)
+
+#define NCCL_OK(expr)                                                                                  \
+  do {                                                                                                 \
+    ncclResult_t r_ = (expr);                                                                          \
+    if (r_ != ncclSuccess)                                                                             \
+      throw cc::Error(CC_ERR_NCCL, std::string(#expr) + ": " + cc::nccl().GetErrorString(r_));        \
+  } while (0)
+
+namespace cc {
+
+// Phases reported by cc_last_profile after "total": PROFILE order.
+enum Phase { PH_COLOR = 0, PH_CSORT, PH_HIST, PH_GATHER, PH_COMBINE, PH_ROOT, PH_EXCHANGE, PH_N };
+
+// One aggregation pass over a range [beg[v], end[v]) of every owned row.
+struct Pass {
+  int32_t *light = nullptr;
+  int32_t *seg_v = nullptr, *seg_hv = nullptr, *hv_first = nullptr, *hv_nseg = nullptr;
+  int64_t *seg_b = nullptr, *seg_e = nullptr;
+  int64_t n_light = 0, n_seg = 0, n_hv = 0;
+  int64_t nnz = 0;             // adjacency entries covered
+  const int64_t *beg = nullptr, *end = nullptr;  // device
+  uint16_t *goff = nullptr;    // n_items x 16 colour-group ends (per colouring)
+  int64_t items() const { return n_seg + n_light; }
+  dev::AggWork view() const {
+    dev::AggWork w;
+    w.light = light;
+    w.n_light = n_light;
+    w.seg_v = seg_v;
+    w.seg_b = seg_b;
+    w.seg_e = seg_e;
+    w.seg_hv = seg_hv;
+    w.hv_first = hv_first;
+    w.hv_nseg = hv_nseg;
+    w.n_seg = n_seg;
+    w.n_hv = n_hv;
+    return w;
+  }
+};
+
+// A stream-ordered device buffer shared by several table handles (a lift
+// step's table is the very buffer of its neighbour sum).
+struct Buf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  int refs = 0;
+};
+
+}  // namespace cc
+
+struct cc_ctx {
+  cc_options opt{};
+  std::string err;
+  bool poisoned = false;
+  int num_sms = 148;
+  cudaStream_t s_main = nullptr, s_comm = nullptr;
+  ncclComm_t comm = nullptr;
+  std::vector<void *> persistent;  // cudaMalloc'd: graph, plan tables (freed on reload / destroy)
+
+  // graph
+  bool has_graph = false;
+  cc::RankPart part;
+  int64_t n_global = 0, n_own = 0, n_halo = 0, n_rows = 0;
+  int64_t n_crow = 0;  // coloured rows: owned | halo | isolated
+  int64_t *d_rp = nullptr, *d_mid = nullptr;
+  int32_t *d_col = nullptr, *d_col_sorted = nullptr, *d_orig = nullptr, *d_send_idx = nullptr;
+  uint8_t *d_colors = nullptr;
+  cc::Pass p_full, p_local, p_remote;  // world 1: p_full; world > 1: p_local + p_remote (+ p_full for hist)
+  int64_t max_seg = 0, max_hv = 0;
+
+  // template
+  bool has_template = false;
+  cc::Plan plan;
+  std::vector<uint32_t *> d_split;    // per step: split table (combine steps)
+  std::vector<uint16_t *> d_map;      // per passive size p: gather map (p >= 2)
+  uint16_t *d_comp = nullptr;         // root step complement table
+  bool has_colors = false;
+  bool sorted_valid = false;          // colour-sorted adjacency matches the colouring
+
+  // scratch
+  double *d_partials = nullptr, *d_result = nullptr;
+  int n_partials = 0;
+  unsigned int *d_arrive = nullptr;
+  int64_t arrive_cap = 0;
+
+  // profile / stats of the last count
+  double prof[cc::PH_N + 1] = {0};
+  double stats[5] = {0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t ev_color[2] = {nullptr, nullptr};
+  double color_ms = 0;
+  size_t cur_bytes = 0, peak_bytes = 0;
+
+  int elem() const { return opt.precision == CC_FP64 ? 8 : 4; }
+  int64_t ld_of(int64_t W) const {
+    const int64_t m = 32 / elem();
+    return (std::max<int64_t>(W, 1) + m - 1) / m * m;
+  }
+
+  template <typename T>
+  T *pmalloc(size_t count) {
+    T *d = nullptr;
+    if (!count) return nullptr;
+    CUDA_OK(cudaMalloc(&d, count * sizeof(T)));
+    persistent.push_back(d);
+    return d;
+  }
+  template <typename T>
+  T *pupload(const std::vector<T> &h) {
+    T *d = pmalloc<T>(h.size());
+    if (d) CUDA_OK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  void pfree(void *p) {
+    if (!p) return;
+    auto it = std::find(persistent.begin(), persistent.end(), p);
+    if (it != persistent.end()) persistent.erase(it);
+    cudaFree(p);
+  }
+  void *amalloc(size_t bytes, cudaStream_t s) {
+    void *p = nullptr;
+    CUDA_OK(cudaMallocAsync(&p, std::max<size_t>(bytes, 256), s));
+    cur_bytes += bytes;
+    peak_bytes = std::max(peak_bytes, cur_bytes);
+    return p;
+  }
+  void afree(void *&p, size_t bytes, cudaStream_t s) {
+    if (!p) return;
+    CUDA_OK(cudaFreeAsync(p, s));
+    cur_bytes -= bytes;
+    p = nullptr;
+  }
+  cudaEvent_t ev() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  cudaEvent_t begin(cudaStream_t s) {
+    cudaEvent_t b = ev();
+    CUDA_OK(cudaEventRecord(b, s));
+    return b;
+  }
+  void end(int ph, cudaStream_t s, cudaEvent_t b) {
+    cudaEvent_t e = ev();
+    CUDA_OK(cudaEventRecord(e, s));
+    ev_log.push_back({ph, {b, e}});
+  }
+  void check_launch() { CUDA_OK(cudaGetLastError()); }
+};
+
+namespace cc {
+// exec.cu
+void load_graph(cc_ctx *c, const HostGraph &g);
+void upload_template(cc_ctx *c);
+void launch_colouring(cc_ctx *c, uint64_t seed);
+// One colouring's DP.  dump_table >= 0 keeps every table and returns table
+// `dump_table` (compressed rows, owned order) in *dump; root_out receives the
+// per-vertex root values.
+void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out);
+}  // namespace cc

@@ -1,0 +1,401 @@
+// exec.cu -- graph upload, plan upload and the per-colouring step executor.
+//
+// One cc_count_colorful = PAPER.md Alg. 1 lines 8-10 (Eq. 2) for one
+// colouring, distributed as Alg. 2 (lines 199-243) when world > 1:
+//   colour-sort the neighbour ranges (once per colouring);
+//   for each step (t; a, p) of the plan (sub-templates in reverse partition
+//   order):
+//     N'' <- neighbour sum of the passive table (once per distinct passive);
+//            world > 1: the passive table's boundary rows are exchanged with
+//            grouped NCCL send/recv on a comm stream while the local part of
+//            the neighbour sum runs (pipelining);
+//     T'  <- split-sum combine of the active table with N'' (a >= 2), or
+//            T' = N'' itself (a = 1: no work in the compressed layout);
+//   X = sum_v of the root step (fp64), all-reduced over ranks (line 237).
+#include <cmath>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace cc {
+
+namespace {
+
+void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<int64_t> &end, bool skip_empty,
+                Pass &w) {
+  // segment length s of Alg. 4; colour-group offsets are stored as uint16
+  const int64_t L = std::min<int64_t>(c->opt.segment_len > 0 ? c->opt.segment_len : 4096, 65535);
+  std::vector<int32_t> light, seg_v, seg_hv, hv_first, hv_nseg;
+  std::vector<int64_t> seg_b, seg_e;
+  int64_t nnz = 0;
+  for (int64_t v = 0; v < (int64_t)beg.size(); ++v) {
+    const int64_t d = end[v] - beg[v];
+    nnz += d;
+    if (d == 0 && skip_empty) continue;
+    if (d > L) {
+      const int64_t ns = (d + L - 1) / L;
+      hv_first.push_back((int32_t)seg_v.size());
+      hv_nseg.push_back((int32_t)ns);
+      for (int64_t s = 0; s < ns; ++s) {
+        seg_v.push_back((int32_t)v);
+        seg_hv.push_back((int32_t)(hv_first.size() - 1));
+        seg_b.push_back(beg[v] + s * L);
+        seg_e.push_back(std::min(end[v], beg[v] + (s + 1) * L));
+      }
+    } else {
+      light.push_back((int32_t)v);
+    }
+  }
+  w.nnz = nnz;
+  w.n_light = (int64_t)light.size();
+  w.n_seg = (int64_t)seg_v.size();
+  w.n_hv = (int64_t)hv_first.size();
+  w.light = c->pupload(light);
+  w.seg_v = c->pupload(seg_v);
+  w.seg_hv = c->pupload(seg_hv);
+  w.hv_first = c->pupload(hv_first);
+  w.hv_nseg = c->pupload(hv_nseg);
+  w.seg_b = c->pupload(seg_b);
+  w.seg_e = c->pupload(seg_e);
+  w.goff = c->pmalloc<uint16_t>((size_t)std::max<int64_t>(w.items(), 1) * 16);
+  c->max_hv = std::max(c->max_hv, w.n_hv);
+  c->max_seg = std::max(c->max_seg, w.n_seg);
+}
+
+// Stream-ordered buffers with shared ownership (see Buf).
+struct Bufs {
+  cc_ctx *c;
+  std::vector<Buf> pool;
+  explicit Bufs(cc_ctx *cx) : c(cx) { pool.reserve(256); }
+  int make(size_t bytes) {
+    pool.push_back({c->amalloc(bytes, c->s_main), bytes, 1});
+    return (int)pool.size() - 1;
+  }
+  void ref(int b) { pool[b].refs++; }
+  void unref(int b) {
+    if (b < 0) return;
+    if (--pool[b].refs == 0) c->afree(pool[b].p, pool[b].bytes, c->s_main);
+  }
+  void *ptr(int b) const { return b < 0 ? nullptr : pool[b].p; }
+};
+
+}  // namespace
+
+void load_graph(cc_ctx *c, const HostGraph &g) {
+  c->part = partition_graph(g, c->opt.world, c->opt.rank, c->opt.relabel_seed);
+  const auto &R = c->part;
+  c->n_global = g.n;
+  c->n_own = R.n_own;
+  c->n_halo = R.n_halo;
+  c->n_rows = R.n_own + R.n_halo;
+  c->d_rp = c->pupload(R.rp);
+  c->d_col = c->pupload(R.col);
+  c->d_col_sorted = c->pmalloc<int32_t>(std::max<size_t>(R.col.size(), 1));
+  std::vector<int32_t> orig(R.own_orig);
+  orig.insert(orig.end(), R.halo_orig.begin(), R.halo_orig.end());
+  orig.insert(orig.end(), R.iso_orig.begin(), R.iso_orig.end());
+  c->n_crow = (int64_t)orig.size();
+  c->d_orig = c->pupload(orig);
+  c->d_colors = c->pmalloc<uint8_t>((size_t)std::max<int64_t>(c->n_crow, 1));
+  std::vector<int64_t> beg(R.rp.begin(), R.rp.end() - 1), end(R.rp.begin() + 1, R.rp.end());
+  build_pass(c, beg, end, false, c->p_full);
+  c->p_full.beg = c->d_rp;
+  c->p_full.end = c->d_rp + 1;
+  if (c->opt.world > 1) {
+    c->d_mid = c->pupload(R.mid);
+    c->d_send_idx = c->pupload(R.send_idx);
+    build_pass(c, beg, R.mid, false, c->p_local);
+    build_pass(c, R.mid, end, true, c->p_remote);
+    c->p_local.beg = c->d_rp;
+    c->p_local.end = c->d_mid;
+    c->p_remote.beg = c->d_mid;
+    c->p_remote.end = c->d_rp + 1;
+  }
+  c->d_arrive = c->pmalloc<unsigned int>((size_t)std::max<int64_t>(c->max_hv, 1));
+  c->arrive_cap = std::max<int64_t>(c->max_hv, 1);
+  c->has_graph = true;
+  c->sorted_valid = false;
+}
+
+void upload_template(cc_ctx *c) {
+  for (auto *p : c->d_split) c->pfree(p);
+  for (auto *p : c->d_map) c->pfree(p);
+  c->pfree(c->d_comp);
+  c->d_split.assign(c->plan.steps.size(), nullptr);
+  c->d_map.assign(kMaxK + 1, nullptr);
+  c->d_comp = nullptr;
+  const int k = c->plan.k;
+  for (size_t s = 0; s < c->plan.steps.size(); ++s) {
+    const Step &st = c->plan.steps[s];
+    // compressed universe: k-1 colours, sets of size t-1 split into (a-1, p)
+    if (st.out < 0) {
+      if (st.a > 1) c->d_comp = c->pupload(complement_table(k - 1, st.a - 1));
+    } else if (st.a > 1) {
+      c->d_split[s] = c->pupload(split_table(k - 1, st.t - 1, st.a - 1));
+    }
+    if (st.p > 1 && !c->d_map[st.p]) c->d_map[st.p] = c->pupload(gather_map(k, st.p));
+  }
+}
+
+void launch_colouring(cc_ctx *c, uint64_t seed) {
+  if (!c->ev_color[0]) {
+    CUDA_OK(cudaEventCreate(&c->ev_color[0]));
+    CUDA_OK(cudaEventCreate(&c->ev_color[1]));
+  }
+  CUDA_OK(cudaEventRecord(c->ev_color[0], c->s_main));
+  dev::launch_color(c->d_orig, c->n_crow, seed, c->plan.k, c->d_colors, c->s_main);
+  c->check_launch();
+  CUDA_OK(cudaEventRecord(c->ev_color[1], c->s_main));
+  c->has_colors = true;
+  c->sorted_valid = false;
+}
+
+namespace {
+
+void csort(cc_ctx *c, Pass &p) {
+  c->stats[3] += dev::launch_csort(p.beg, p.end, c->d_col, c->d_colors, p.view(), c->d_col_sorted, p.goff,
+                                   c->num_sms, c->s_main);
+  c->check_launch();
+  c->stats[1] += (double)p.nnz * 14.0 + (double)p.items() * 32.0;
+}
+
+// N'' = neighbour sum of the passive table P' (size p >= 2) over one pass.
+void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate) {
+  const int k = c->plan.k, elem = c->elem();
+  const int W_in = (int)binom(k - 1, p - 1), W_out = (int)binom(k - 1, p);
+  dev::GatherArgs a;
+  a.beg = w.beg;
+  a.end = w.end;
+  a.col = c->d_col_sorted;
+  a.goff = w.goff;
+  a.colors = c->d_colors;
+  a.src = P;
+  a.ld_src = c->ld_of(W_in);
+  a.W_in = W_in;
+  a.map = c->d_map[p];
+  a.dst = N;
+  a.ld_dst = c->ld_of(W_out);
+  a.W_out = W_out;
+  a.k = k;
+  a.accumulate = accumulate;
+  a.work = w.view();
+  a.ld_scratch = W_out;
+  void *scratch = nullptr;
+  const size_t sbytes = (size_t)w.n_seg * W_out * sizeof(double);
+  if (w.n_seg) {
+    scratch = c->amalloc(sbytes, c->s_main);
+    CUDA_OK(cudaMemsetAsync(c->d_arrive, 0, (size_t)w.n_hv * sizeof(unsigned int), c->s_main));
+  }
+  a.scratch = static_cast<double *>(scratch);
+  a.arrive = c->d_arrive;
+  cudaEvent_t b = c->begin(c->s_main);
+  c->stats[3] += dev::launch_gather(elem, a, c->num_sms, c->s_main);
+  c->check_launch();
+  c->end(PH_GATHER, c->s_main, b);
+  if (scratch) c->afree(scratch, sbytes, c->s_main);
+  // algorithmic bytes: index stream + compressed rows of the neighbours whose
+  // colour differs from the row vertex's (expected fraction (k-1)/k) + N'' rows
+  // written (+ read when accumulating)
+  const double rows = (double)w.nnz * (double)(k - 1) / k * W_in * elem;
+  const double bytes = (double)w.nnz * 4.0 + rows + (double)(w.n_light + w.n_hv) * W_out * elem * (1 + accumulate);
+  c->stats[0] += (double)w.nnz * (double)binom(k, p);  // U: dense edge x colour-set updates
+  c->stats[1] += bytes;
+  c->stats[2] += bytes;
+}
+
+void aggregate(cc_ctx *c, void *P, int p, void *N) {
+  if (c->opt.world == 1) {
+    gather_pass(c, c->p_full, P, p, N, 0);
+    return;
+  }
+  // world > 1: exchange the boundary rows of P' on the comm stream while the
+  // local part runs; then add the remote part.
+  auto &api = nccl();
+  const int k = c->plan.k, elem = c->elem();
+  const int64_t ld = c->ld_of(binom(k - 1, p - 1));
+  cudaEvent_t ready = c->ev(), recvd = c->ev();
+  CUDA_OK(cudaEventRecord(ready, c->s_main));
+  CUDA_OK(cudaStreamWaitEvent(c->s_comm, ready, 0));
+  const auto &R = c->part;
+  const int64_t send_rows = R.send_off[c->opt.world];
+  const size_t sbytes = (size_t)send_rows * ld * elem;
+  void *sendbuf = send_rows ? c->amalloc(sbytes, c->s_comm) : nullptr;
+  cudaEvent_t xb = c->begin(c->s_comm);
+  c->stats[3] += dev::launch_pack(elem, P, ld, c->d_send_idx, send_rows, sendbuf, c->s_comm);
+  c->check_launch();
+  const ncclDataType_t dt = elem == 8 ? ncclFloat64 : ncclFloat32;
+  NCCL_OK(api.GroupStart());
+  for (int q = 0; q < c->opt.world; ++q) {
+    if (q == c->opt.rank) continue;
+    const int64_t ns = R.send_off[q + 1] - R.send_off[q];
+    const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
+    if (ns)
+      NCCL_OK(api.Send(static_cast<char *>(sendbuf) + (size_t)R.send_off[q] * ld * elem, (size_t)(ns * ld), dt, q,
+                       c->comm, c->s_comm));
+    if (nr)
+      NCCL_OK(api.Recv(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[q]) * ld * elem, (size_t)(nr * ld), dt,
+                       q, c->comm, c->s_comm));
+  }
+  NCCL_OK(api.GroupEnd());
+  c->end(PH_EXCHANGE, c->s_comm, xb);
+  if (sendbuf) c->afree(sendbuf, sbytes, c->s_comm);
+  CUDA_OK(cudaEventRecord(recvd, c->s_comm));
+  gather_pass(c, c->p_local, P, p, N, 0);
+  CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
+  gather_pass(c, c->p_remote, P, p, N, 1);
+  c->stats[1] += (double)send_rows * ld * elem * 2;
+}
+
+}  // namespace
+
+void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out) {
+  const Plan &pl = c->plan;
+  const int k = pl.k, elem = c->elem();
+  std::fill(c->stats, c->stats + 5, 0.0);
+  c->ev_used = 0;
+  c->ev_log.clear();
+  c->cur_bytes = c->peak_bytes = 0;
+  std::fill(c->prof, c->prof + PH_N + 1, 0.0);
+  if (k == 1) {  // the single-vertex template maps onto every vertex
+    *X = (double)c->n_global;
+    return;
+  }
+  const int64_t n = c->n_own, rows = c->n_rows;
+  cudaEvent_t t0 = c->ev(), t1 = c->ev();
+  CUDA_OK(cudaEventRecord(t0, c->s_main));
+
+  // colour-sort the neighbour ranges of every pass (once per colouring)
+  if (!c->sorted_valid) {
+    cudaEvent_t b = c->begin(c->s_main);
+    if (c->opt.world == 1) {
+      csort(c, c->p_full);
+    } else {
+      csort(c, c->p_local);
+      csort(c, c->p_remote);
+    }
+    c->end(PH_CSORT, c->s_main, b);
+    c->sorted_valid = true;
+  }
+
+  Bufs bufs(c);
+  const int nt = (int)pl.tables.size();
+  std::vector<int> T(nt, -1), Nb(nt, -1);
+  int hist = -1;
+  int last_hist_use = -1;
+  for (int s = 0; s < (int)pl.steps.size(); ++s)
+    if (pl.steps[s].p == 1) last_hist_use = s;
+  double *per_vertex = nullptr;
+  if (root_out) per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
+
+  for (int s = 0; s < (int)pl.steps.size(); ++s) {
+    const Step &st = pl.steps[s];
+    const int Wa = (int)binom(k - 1, st.a - 1), Wp = (int)binom(k - 1, st.p), Wt = (int)binom(k - 1, st.t - 1);
+    int nbuf;  // buffer of N''
+    if (st.p == 1) {
+      if (hist < 0) {
+        hist = bufs.make((size_t)rows * c->ld_of(k - 1) * elem);
+        cudaEvent_t b = c->begin(c->s_main);
+        c->stats[3] += dev::launch_hist(elem, c->d_rp, c->d_rp + 1, c->d_col, c->d_colors, c->p_full.view(), n, k,
+                                        bufs.ptr(hist), c->ld_of(k - 1), c->num_sms, c->s_main);
+        c->check_launch();
+        c->end(PH_HIST, c->s_main, b);
+        const double nnz = (double)c->part.col.size();
+        c->stats[0] += nnz * k;  // U counts C(k,1) = k colour sets per adjacency entry
+        c->stats[1] += nnz * 5.0 + (double)n * (k - 1) * elem;
+      }
+      nbuf = hist;
+    } else {
+      const int P = st.passive;
+      if (Nb[P] < 0) {
+        Nb[P] = bufs.make((size_t)rows * c->ld_of(Wp) * elem);
+        aggregate(c, bufs.ptr(T[P]), st.p, bufs.ptr(Nb[P]));
+      }
+      nbuf = Nb[P];
+    }
+    const int64_t ldN = c->ld_of(Wp);
+    if (st.out < 0) {  // root step fused with the sum over v (Eq. 3)
+      cudaEvent_t b = c->begin(c->s_main);
+      const void *A = st.a > 1 ? bufs.ptr(T[st.active]) : nullptr;
+      c->stats[3] += dev::launch_root(elem, A, c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, c->d_comp, n, c->d_partials,
+                                      c->n_partials, per_vertex, c->d_result, c->s_main);
+      c->check_launch();
+      c->end(PH_ROOT, c->s_main, b);
+      c->stats[1] += (double)n * (st.a > 1 ? 2.0 * Wa : 1.0) * elem;
+    } else if (st.a == 1) {  // T'(v, .) = N''(v, .): alias, no kernel
+      T[st.out] = nbuf;
+      bufs.ref(nbuf);
+    } else {
+      T[st.out] = bufs.make((size_t)rows * c->ld_of(Wt) * elem);
+      cudaEvent_t b = c->begin(c->s_main);
+      c->stats[3] += dev::launch_combine(elem, bufs.ptr(T[st.active]), c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, Wp,
+                                         c->d_split[s], (int)binom(st.t - 1, st.a - 1), n, bufs.ptr(T[st.out]),
+                                         c->ld_of(Wt), Wt, c->num_sms, c->s_main);
+      c->check_launch();
+      c->end(PH_COMBINE, c->s_main, b);
+      c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;
+    }
+    if (dump_table < 0) {  // release dead tables / neighbour sums
+      for (int id = 0; id < nt; ++id) {
+        if (T[id] >= 0 && pl.table_last_use[id] == s) {
+          bufs.unref(T[id]);
+          T[id] = -1;
+        }
+        if (Nb[id] >= 0 && pl.n_last_use[id] == s) {
+          bufs.unref(Nb[id]);
+          Nb[id] = -1;
+        }
+      }
+      if (hist >= 0 && s == last_hist_use) {
+        bufs.unref(hist);
+        hist = -2;  // computed and released
+      }
+    }
+  }
+  if (c->opt.world > 1) {
+    cudaEvent_t b = c->begin(c->s_main);
+    NCCL_OK(nccl().AllReduce(c->d_result, c->d_result, 1, ncclFloat64, ncclSum, c->comm, c->s_main));
+    c->end(PH_EXCHANGE, c->s_main, b);
+  }
+  CUDA_OK(cudaEventRecord(t1, c->s_main));
+  double host_x = 0;
+  CUDA_OK(cudaMemcpyAsync(&host_x, c->d_result, sizeof(double), cudaMemcpyDeviceToHost, c->s_main));
+  if (dump && dump_table >= 0 && T[dump_table] >= 0) {
+    const int W = (int)binom(k - 1, pl.tables[dump_table].size - 1);
+    std::vector<char> raw((size_t)n * c->ld_of(W) * elem);
+    if (!raw.empty())
+      CUDA_OK(cudaMemcpyAsync(raw.data(), bufs.ptr(T[dump_table]), raw.size(), cudaMemcpyDeviceToHost, c->s_main));
+    CUDA_OK(cudaStreamSynchronize(c->s_main));
+    dump->assign((size_t)n * W, 0.0);
+    for (int64_t v = 0; v < n; ++v)
+      for (int j = 0; j < W; ++j) {
+        const size_t off = (size_t)v * c->ld_of(W) + j;
+        (*dump)[(size_t)v * W + j] =
+            elem == 8 ? reinterpret_cast<double *>(raw.data())[off] : reinterpret_cast<float *>(raw.data())[off];
+      }
+  }
+  if (root_out) {
+    root_out->resize((size_t)n);
+    if (n) CUDA_OK(cudaMemcpyAsync(root_out->data(), per_vertex, (size_t)n * 8, cudaMemcpyDeviceToHost, c->s_main));
+  }
+  for (auto &b : bufs.pool)
+    if (b.p) c->afree(b.p, b.bytes, c->s_main);
+  if (per_vertex) {
+    void *pv = per_vertex;
+    c->afree(pv, (size_t)std::max<int64_t>(n, 1) * 8, c->s_main);
+  }
+  CUDA_OK(cudaStreamSynchronize(c->s_main));
+  if (c->opt.world > 1) CUDA_OK(cudaStreamSynchronize(c->s_comm));
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, t0, t1));
+  c->prof[0] = ms;
+  for (auto &e : c->ev_log) {
+    float m = 0;
+    CUDA_OK(cudaEventElapsedTime(&m, e.second.first, e.second.second));
+    c->prof[1 + e.first] += m;
+  }
+  c->stats[4] = (double)c->peak_bytes;
+  if (!std::isfinite(host_x)) throw Error(CC_ERR_NONFINITE, "colourful count is not finite (fp32 table overflow?)");
+  *X = host_x;
+}
+
+}  // namespace cc

@@ -6,20 +6,25 @@
 // occupancy calculator) and walk their work with a static interleaved stride,
 // so every reduction order -- and therefore every result -- is deterministic.
 //
+// Tables are colour-compressed (kernels.cuh).  The kernels:
 //   k_color   colouring, PAPER.md lines 156-158 (reading C-2)
-//   k_hist    N(v, {c}) = #{u in N(v): col u = c}: the neighbour sum of the
-//             single-vertex table (passive part of size 1)
-//   k_agg     N(v, Y) = sum_{u in N(v)} P(u, Y): the inner sum over u of
-//             Eq. 1, SpMM-shaped, column-chunked,
-//             heavy neighbour lists split into segments (Alg. 4, lines
-//             494-523) and reduced deterministically by the last arriver
-//   k_lift    T(v, S) = [c_v in S] N(v, S \ {c_v}): a step whose active part
-//             is the single root vertex (split sum has one term)
-//   k_combine T(v, S) = sum_{S1 u S2 = S} A(v, S1) N(v, S2): the split sum of
-//             Eq. 1 over the split table of the step
-//   k_root    X = sum_v sum_{S1} A(v, S1) N(v, [k] \ S1): the last step fused
-//             with Eq. 3's sum over v, fp64
+//   k_csort   per colouring: stable sort of every neighbour range by colour
+//             (groups neighbours whose compressed rows share an index space)
+//   k_hist    N''(v, {y}): neighbour counts per colour -- the neighbour sum of
+//             the single-vertex table (passive part of size 1)
+//   k_gather  N''(v, Y'') = sum_{u in N(v)} P(u, Y): the inner sum over u of
+//             Eq. 1, SpMM-shaped; per colour group the
+//             compressed rows are summed in registers (fp64), then expanded
+//             once into the vertex's N'' row in shared memory; heavy
+//             neighbour lists are split into segments (Alg. 4)
+//             whose partial rows the last arriver sums in segment order
+//   k_combine T'(v, S') = sum_{X' u Y'' = S'} A'(v, X') N''(v, Y''): the split
+//             sum of Eq. 1, colour-independent in the compressed universe
+//   k_root    X = sum_v sum_{X'} A'(v, X') N''(v, [k-1] \ X'): the last step
+//             fused with Eq. 3's sum over v, fp64
 //   k_pack    halo rows for the 1D partition exchange (Alg. 2 line 15)
+// A step whose active part is the single root vertex (a = 1) needs no kernel:
+// in the compressed layout its table IS the neighbour sum N''.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -60,26 +65,32 @@ __device__ __forceinline__ void add_vec(double *acc, const double2 &v) {
   acc[0] += v.x;
   acc[1] += v.y;
 }
-__device__ __forceinline__ void store_vec(float *p, const double *acc) {
-  *reinterpret_cast<float4 *>(p) = make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
-}
-__device__ __forceinline__ void store_vec(double *p, const double *acc) {
-  *reinterpret_cast<double2 *>(p) = make_double2(acc[0], acc[1]);
-}
-__device__ __forceinline__ void load_add(const float *p, double *acc) {
-  float4 v = *reinterpret_cast<const float4 *>(p);
-  add_vec(acc, v);
-}
-__device__ __forceinline__ void load_add(const double *p, double *acc) {
-  double2 v = *reinterpret_cast<const double2 *>(p);
-  add_vec(acc, v);
-}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // SplitMix64 finaliser (reading C-2)
   uint64_t z = x + 0x9E3779B97F4A7C15ULL;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
+}
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  return (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+}
+
+// item -> (vertex, neighbour range)
+__device__ __forceinline__ bool item_range(const AggWork &w, const int64_t *beg, const int64_t *end, int64_t it,
+                                           int32_t &v, int64_t &b, int64_t &e) {
+  if (it < w.n_seg) {
+    v = w.seg_v[it];
+    b = w.seg_b[it];
+    e = w.seg_e[it];
+    return true;
+  }
+  v = w.light[it - w.n_seg];
+  b = beg[v];
+  e = end[v];
+  return false;
 }
 
 // ------------------------------------------------------------------ colour
@@ -92,9 +103,56 @@ __global__ void k_color(const int32_t *__restrict__ orig, int64_t n, uint64_t se
   }
 }
 
-// ------------------------------------------------------------------ hist
-// Work items as in k_agg (light vertices, segments of heavy neighbour lists).
-// Segment partial counts are added with atomics into a zeroed row: the values
+// ------------------------------------------------------------------ colour sort
+// One warp per item.  Pass 1 counts colours; pass 2 places each neighbour at
+// base[colour] + (rank among equal colours in this 32-wide window), so the
+// sort is stable and deterministic.
+__global__ void __launch_bounds__(256) k_csort(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+                                               const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
+                                               AggWork work, int32_t *__restrict__ col_out,
+                                               uint16_t *__restrict__ goff) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const int64_t n_items = work.n_seg + work.n_light;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; it < n_items; it += nwarps) {
+    int32_t v;
+    int64_t b, e;
+    item_range(work, beg, end, it, v, b, e);
+    int cnt[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cnt[j] = 0;
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int c = colors[__ldg(col + p)];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cnt[j] += (c == j);
+    }
+    int base[16];
+    int run = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
+      base[j] = run;
+      run += cnt[j];
+      if (lane == j) goff[it * 16 + j] = (uint16_t)run;
+    }
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+      const bool ok = p0 + lane < e;
+      const int32_t u = ok ? __ldg(col + p0 + lane) : 0;
+      const int c = ok ? (int)colors[u] : 16;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const unsigned m = __ballot_sync(0xffffffffu, c == j);
+        if (c == j) col_out[b + base[j] + __popc(m & lt)] = u;
+        base[j] += __popc(m);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ hist (p = 1)
+// Heavy segments add their counts atomically into a zeroed row: the values
 // are small integers, exact in fp32/fp64, so the result is order-independent.
 template <typename T, int G>
 __global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
@@ -102,22 +160,13 @@ __global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ beg, c
                                               AggWork work, int k, T *__restrict__ out, int64_t ld) {
   constexpr int U = 4;
   const int lane = threadIdx.x & (G - 1);
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const unsigned gmask = group_mask<G>();
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
   const int64_t n_items = work.n_seg + work.n_light;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
-    const bool heavy = it < work.n_seg;
-    int64_t b, e;
     int32_t v;
-    if (heavy) {
-      v = work.seg_v[it];
-      b = work.seg_b[it];
-      e = work.seg_e[it];
-    } else {
-      v = work.light[it - work.n_seg];
-      b = beg[v];
-      e = end[v];
-    }
+    int64_t b, e;
+    const bool heavy = item_range(work, beg, end, it, v, b, e);
     int cnt[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) cnt[j] = 0;
@@ -137,149 +186,127 @@ __global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ beg, c
     for (int j = 0; j < 16; ++j)
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) cnt[j] += __shfl_xor_sync(gmask, cnt[j], o, G);
+    const int cv = colors[v];
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (j % G == lane && j < k) {
-        if (heavy) atomicAdd(out + (int64_t)v * ld + j, (T)cnt[j]);
-        else out[(int64_t)v * ld + j] = (T)cnt[j];
+      if (j % G == lane && j < k && j != cv) {
+        T *p = out + (int64_t)v * ld + (j < cv ? j : j - 1);  // squeeze: sq_{c_v}(j)
+        if (heavy) atomicAdd(p, (T)cnt[j]);
+        else *p = (T)cnt[j];
       }
   }
 }
 
-// ------------------------------------------------------------------ aggregation
+// ------------------------------------------------------------------ gather (p >= 2)
 template <typename T, int G, int NV, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_agg(AggArgs a, int nchunks, int CW) {
+__global__ void __launch_bounds__(256, MINB) k_gather(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
+  constexpr int CAP = G * NV * VW;  // input columns per pass
+  extern __shared__ double sacc_all[];
   const int lane = threadIdx.x & (G - 1);
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const unsigned gmask = group_mask<G>();
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
   const int64_t n_items = a.work.n_seg + a.work.n_light;
-  const int64_t total = n_items * nchunks;
+  double *sacc = sacc_all + (threadIdx.x / G) * (int64_t)a.W_out;
   const T *__restrict__ src = static_cast<const T *>(a.src);
   T *__restrict__ dst = static_cast<T *>(a.dst);
 
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; w < total; w += ngroups) {
-    const int chunk = (int)(w / n_items);
-    const int64_t it = w - (int64_t)chunk * n_items;
-    const bool heavy = it < a.work.n_seg;
-    int64_t b, e;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
     int32_t v;
-    if (heavy) {
-      v = a.work.seg_v[it];
-      b = a.work.seg_b[it];
-      e = a.work.seg_e[it];
-    } else {
-      v = a.work.light[it - a.work.n_seg];
-      b = a.beg[v];
-      e = a.end[v];
-    }
-    const int c0 = chunk * CW + lane * VW;
-    bool valid[NV];
+    int64_t b, e;
+    const bool heavy = item_range(a.work, a.beg, a.end, it, v, b, e);
+    const int cv = a.colors[v];
+    for (int j = lane; j < a.W_out; j += G) sacc[j] = 0.0;
+    __syncwarp(gmask);
+    const uint16_t *go = a.goff + it * 16;
+    int gstart = 0;
+    for (int cu = 0; cu < a.k; ++cu) {
+      const int gend = go[cu];
+      if (cu != cv && gend > gstart) {
+        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.W_in;
+        for (int ch = 0; ch < nch; ++ch) {
+          const int c0 = ch * CAP + lane * VW;
+          bool valid[NV];
 #pragma unroll
-    for (int j = 0; j < NV; ++j) valid[j] = (lane * VW + j * G * VW < CW) && (c0 + j * G * VW < a.W);
-    double acc[NV][VW];
+          for (int j = 0; j < NV; ++j) valid[j] = c0 + j * G * VW < a.W_in;
+          double acc[NV][VW];
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
+          for (int j = 0; j < NV; ++j)
 #pragma unroll
-      for (int q = 0; q < VW; ++q) acc[j][q] = 0.0;
-
-    for (int64_t e0 = b; e0 < e; e0 += G) {
-      const int cnt = (int)min((int64_t)G, e - e0);
-      const int32_t my_u = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
-      for (int j0 = 0; j0 < cnt; j0 += U) {
-        V vals[U][NV];
+            for (int q = 0; q < VW; ++q) acc[j][q] = 0.0;
+          for (int64_t e0 = b + gstart; e0 < b + gend; e0 += G) {
+            const int cnt = (int)min((int64_t)G, b + gend - e0);
+            const int32_t my_u = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
+            for (int j0 = 0; j0 < cnt; j0 += U) {
+              V vals[U][NV];
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-          const int32_t u = __shfl_sync(gmask, my_u, (j0 + uu) & (G - 1), G);
-          const T *row = src + (int64_t)u * a.ld_src + c0;
+              for (int uu = 0; uu < U; ++uu) {
+                const int32_t u = __shfl_sync(gmask, my_u, (j0 + uu) & (G - 1), G);
+                const T *row = src + (int64_t)u * a.ld_src + c0;
 #pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            if (j0 + uu < cnt && valid[j]) vals[uu][j] = ldg_vec(row + j * G * VW);
-            else zero_vec(vals[uu][j]);
+                for (int j = 0; j < NV; ++j) {
+                  if (j0 + uu < cnt && valid[j]) vals[uu][j] = ldg_vec(row + j * G * VW);
+                  else zero_vec(vals[uu][j]);
+                }
+              }
+#pragma unroll
+              for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+                for (int j = 0; j < NV; ++j) add_vec(acc[j], vals[uu][j]);
+            }
           }
+          // expand the colour group's sum into the vertex's N'' row (the map is
+          // injective for a fixed colour pair, so lanes never collide)
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int q = 0; q < VW; ++q) {
+              const int y = c0 + j * G * VW + q;
+              if (y < a.W_in) {
+                const uint16_t m = __ldg(mrow + y);
+                if (m != 0xFFFF) sacc[m] += acc[j][q];
+              }
+            }
         }
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu)
-#pragma unroll
-          for (int j = 0; j < NV; ++j) add_vec(acc[j], vals[uu][j]);
+        __syncwarp(gmask);
       }
+      gstart = gend;
     }
 
     if (!heavy) {
-#pragma unroll
-      for (int j = 0; j < NV; ++j)
-        if (valid[j]) {
-          T *p = dst + (int64_t)v * a.ld_dst + c0 + j * G * VW;
-          if (a.accumulate) load_add(p, acc[j]);
-          store_vec(p, acc[j]);
-        }
+      T *drow = dst + (int64_t)v * a.ld_dst;
+      for (int j = lane; j < a.W_out; j += G) {
+        double x = sacc[j];
+        if (a.accumulate) x += (double)drow[j];
+        drow[j] = (T)x;
+      }
     } else {
-      double *sp = a.scratch + it * a.ld_scratch + c0;
-#pragma unroll
-      for (int j = 0; j < NV; ++j)
-        if (valid[j]) {
-#pragma unroll
-          for (int q = 0; q < VW; q += 2)
-            *reinterpret_cast<double2 *>(sp + j * G * VW + q) = make_double2(acc[j][q], acc[j][q + 1]);
-        }
+      double *sp = a.scratch + it * a.ld_scratch;
+      for (int j = lane; j < a.W_out; j += G) sp[j] = sacc[j];
       __threadfence();
       __syncwarp(gmask);
       const int32_t hv = a.work.seg_hv[it];
       unsigned prev = 0;
-      if (lane == 0) prev = atomicAdd(&a.arrive[(int64_t)hv * nchunks + chunk], 1u);
+      if (lane == 0) prev = atomicAdd(&a.arrive[hv], 1u);
       prev = __shfl_sync(gmask, prev, 0, G);
       if (prev == (unsigned)(a.work.hv_nseg[hv] - 1)) {  // last arriver reduces in segment order
         __threadfence();
         const int32_t s0 = a.work.hv_first[hv], ns = a.work.hv_nseg[hv];
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-#pragma unroll
-          for (int q = 0; q < VW; ++q) acc[j][q] = 0.0;
-        for (int s = 0; s < ns; ++s) {
-          const double *p = a.scratch + (int64_t)(s0 + s) * a.ld_scratch + c0;
-#pragma unroll
-          for (int j = 0; j < NV; ++j)
-            if (valid[j]) {
-#pragma unroll
-              for (int q = 0; q < VW; q += 2) {
-                double2 x = __ldcg(reinterpret_cast<const double2 *>(p + j * G * VW + q));
-                acc[j][q] += x.x;
-                acc[j][q + 1] += x.y;
-              }
-            }
+        T *drow = dst + (int64_t)v * a.ld_dst;
+        for (int j = lane; j < a.W_out; j += G) {
+          double x = 0.0;
+          for (int s = 0; s < ns; ++s) x += __ldcg(a.scratch + (int64_t)(s0 + s) * a.ld_scratch + j);
+          if (a.accumulate) x += (double)drow[j];
+          drow[j] = (T)x;
         }
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-          if (valid[j]) {
-            T *p = dst + (int64_t)v * a.ld_dst + c0 + j * G * VW;
-            if (a.accumulate) load_add(p, acc[j]);
-            store_vec(p, acc[j]);
-          }
       }
     }
+    __syncwarp(gmask);
   }
 }
 
-// ------------------------------------------------------------------ lift (a = 1)
-template <typename T>
-__global__ void __launch_bounds__(256) k_lift(const T *__restrict__ N, int64_t ldN, const uint8_t *__restrict__ colors,
-                                              const uint16_t *__restrict__ drop, int64_t n, int Wt,
-                                              T *__restrict__ out, int64_t ldO) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; v < n; v += nwarps) {
-    const int c = colors[v];
-    const T *nr = N + v * ldN;
-    T *orow = out + v * ldO;
-    for (int r = lane; r < Wt; r += 32) {
-      const uint16_t d = __ldg(drop + r * 16 + c);
-      orow[r] = d == 0xFFFF ? (T)0 : nr[d];
-    }
-  }
-}
-
-// ------------------------------------------------------------------ combine
+// ------------------------------------------------------------------ combine (a >= 2)
 template <typename T, int V>
 __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_t ldA, int WA,
                                                  const T *__restrict__ N, int64_t ldN, int WN,
@@ -322,8 +349,7 @@ __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_
 // ------------------------------------------------------------------ root
 template <typename T>
 __global__ void __launch_bounds__(256) k_root(const T *__restrict__ A, int64_t ldA, int WA, const T *__restrict__ N,
-                                              int64_t ldN, const uint16_t *__restrict__ comp,
-                                              const uint8_t *__restrict__ colors, int64_t n,
+                                              int64_t ldN, const uint16_t *__restrict__ comp, int64_t n,
                                               double *__restrict__ partials, double *__restrict__ per_vertex) {
   __shared__ double wsum_s[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -336,7 +362,7 @@ __global__ void __launch_bounds__(256) k_root(const T *__restrict__ A, int64_t l
       const T *nr = N + v * ldN;
       for (int x = lane; x < WA; x += 32) s += (double)ar[x] * (double)nr[__ldg(comp + x)];
     } else if (lane == 0) {
-      s = (double)N[v * ldN + __ldg(comp + colors[v])];
+      s = (double)N[v * ldN];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
@@ -388,63 +414,42 @@ int persistent_grid(K kernel, int threads, size_t smem, int num_sms) {
   return per_sm * num_sms;
 }
 
-template <typename T, int G, int NV, int U = (G * NV >= 32) ? 8 : 4, int MINB = 1>
-void agg_go(const AggArgs &a, int nchunks, int CW, int num_sms, cudaStream_t s) {
-  auto kern = k_agg<T, G, NV, U, MINB>;
-  static int grid = 0;
-  if (!grid) grid = persistent_grid(kern, 256, 0, num_sms);
-  kern<<<grid, 256, 0, s>>>(a, nchunks, CW);
-}
-
-// Tuning variants of the wide-row kernel (G = 32), selected by CC_AGG_VARIANT.
-int agg_variant() {
-  const char *e = getenv("CC_AGG_VARIANT");
-  return e ? atoi(e) : 0;
-}
-
-void agg_shape(int VW, int W, int64_t chunk_cols, int *G, int *NV) {
-  const int wvec = (W + VW - 1) / VW;  // vectors per row
-  if (wvec <= 4) { *G = 4; *NV = 1; }
-  else if (wvec <= 8) { *G = 8; *NV = 1; }
-  else if (wvec <= 16) { *G = 16; *NV = 1; }
-  else if (wvec <= 32) { *G = 32; *NV = 1; }
-  else { *G = 32; *NV = 2; }
-  if (chunk_cols > 0 && *G == 32) *NV = chunk_cols > 32 * VW ? 2 : 1;  // explicit chunk width
-}
-
-// Balanced column chunks: as few passes as the group's capacity allows, with
-// equal widths (a multiple of the vector width), so no pass runs nearly empty.
-void agg_chunking(int VW, int W, int cap, int *CW, int *nchunks) {
-  *nchunks = (W + cap - 1) / cap;
-  if (*nchunks < 1) *nchunks = 1;
-  const int per = (W + *nchunks - 1) / *nchunks;
-  *CW = (per + VW - 1) / VW * VW;
+template <typename T, int G, int NV, int U, int MINB = 1>
+void gather_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = G * NV * VW;
+  auto kern = k_gather<T, G, NV, U, MINB>;
+  // shared memory: one fp64 N'' row per group; shrink the block if rows are wide
+  const size_t row = (size_t)a.W_out * sizeof(double);
+  int groups = 256 / G;
+  while (groups > 1 && row * groups > 96 * 1024) groups /= 2;
+  const int threads = groups * G;
+  const size_t smem = row * groups;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, threads, smem, num_sms);
+  const int nch = (a.W_in + CAP - 1) / CAP;
+  kern<<<grid, threads, smem, s>>>(a, nch);
 }
 
 template <typename T>
-int agg_typed(const AggArgs &a, int64_t chunk_cols, int num_sms, int *nchunks_out, cudaStream_t s) {
+int gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
-  int G, NV, CW, nchunks;
-  agg_shape(VW, a.W, chunk_cols, &G, &NV);
-  agg_chunking(VW, a.W, G * NV * VW, &CW, &nchunks);
-  if (nchunks_out) *nchunks_out = nchunks;
   if (a.work.n_seg + a.work.n_light == 0) return 0;
-  switch (G * 10 + NV) {
-    case 41: agg_go<T, 4, 1>(a, nchunks, CW, num_sms, s); break;
-    case 81: agg_go<T, 8, 1>(a, nchunks, CW, num_sms, s); break;
-    case 161: agg_go<T, 16, 1>(a, nchunks, CW, num_sms, s); break;
-    case 321:
-      if (agg_variant() == 3) agg_go<T, 32, 1, 16>(a, nchunks, CW, num_sms, s);
-      else agg_go<T, 32, 1>(a, nchunks, CW, num_sms, s);
-      break;
-    default:
-      switch (agg_variant()) {
-        case 1: agg_go<T, 32, 2, 4>(a, nchunks, CW, num_sms, s); break;
-        case 2: agg_go<T, 32, 2, 4, 2>(a, nchunks, CW, num_sms, s); break;
-        case 5: agg_go<T, 32, 2>(a, nchunks, CW, num_sms, s); break;
-        default: agg_go<T, 32, 2, 8, 2>(a, nchunks, CW, num_sms, s); break;  // measured best (config 3)
-      }
-      break;
+  const int wvec = (a.W_in + VW - 1) / VW;
+  // one vector per lane per pass (wide rows take several column passes per
+  // colour group): few registers, many resident warps, U rows in flight each
+  if (wvec <= 4) gather_go<T, 4, 1, 4, 3>(a, num_sms, s);
+  else if (wvec <= 8) gather_go<T, 8, 1, 4, 3>(a, num_sms, s);
+  else if (wvec <= 16) gather_go<T, 16, 1, 8, 3>(a, num_sms, s);
+  else {
+    const char *var = getenv("CC_GATHER_VARIANT");  // tuning knob (scripts/agg_sweep.py)
+    switch (var ? atoi(var) : 0) {
+      case 1: gather_go<T, 32, 1, 8, 3>(a, num_sms, s); break;
+      case 2: gather_go<T, 32, 1, 8, 2>(a, num_sms, s); break;
+      case 3: gather_go<T, 32, 1, 2, 6>(a, num_sms, s); break;
+      case 4: gather_go<T, 32, 1, 4, 5>(a, num_sms, s); break;
+      default: gather_go<T, 32, 1, 4, 4>(a, num_sms, s); break;  // measured best (config 3)
+    }
   }
   return 1;
 }
@@ -454,11 +459,7 @@ void combine_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, 
                 int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
   auto kern = k_combine<T, V>;
   const size_t smem = (size_t)V * (WA + WN) * sizeof(T);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = persistent_grid(kern, 256, smem, num_sms);
   kern<<<grid, 256, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq, n,
                                static_cast<T *>(out), ldO, WO);
@@ -478,20 +479,21 @@ void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ld
 
 }  // namespace
 
-int agg_partials_blocks(int num_sms) { return num_sms * 8; }
-
-int agg_nchunks(int elem, int W, int64_t chunk_cols) {
-  const int VW = elem == 8 ? 2 : 4;
-  int G, NV, CW, nchunks;
-  agg_shape(VW, W, chunk_cols, &G, &NV);
-  agg_chunking(VW, W, G * NV * VW, &CW, &nchunks);
-  return nchunks;
-}
+int root_partials_blocks(int num_sms) { return num_sms * 8; }
 
 int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *out, cudaStream_t s) {
   if (n == 0) return 0;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   k_color<<<grid, 256, 0, s>>>(orig, n, seed, k, out);
+  return 1;
+}
+
+int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
+                 const AggWork &work, int32_t *col_out, uint16_t *goff, int num_sms, cudaStream_t s) {
+  if (work.n_seg + work.n_light == 0) return 0;
+  static int grid = 0;
+  if (!grid) grid = persistent_grid(k_csort, 256, 0, num_sms);
+  k_csort<<<grid, 256, 0, s>>>(beg, end, col, colors, work, col_out, goff);
   return 1;
 }
 
@@ -515,26 +517,8 @@ int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t 
   return launches;
 }
 
-int launch_agg(int elem, const AggArgs &a, int64_t chunk_cols, int num_sms, int *nchunks_out, cudaStream_t s) {
-  return elem == 8 ? agg_typed<double>(a, chunk_cols, num_sms, nchunks_out, s)
-                   : agg_typed<float>(a, chunk_cols, num_sms, nchunks_out, s);
-}
-
-int launch_lift(int elem, const void *N, int64_t ldN, const uint8_t *colors, const uint16_t *drop, int64_t n, int Wt,
-                void *out, int64_t ldO, int num_sms, cudaStream_t s) {
-  if (n == 0) return 0;
-  if (elem == 8) {
-    static int grid = 0;
-    if (!grid) grid = persistent_grid(k_lift<double>, 256, 0, num_sms);
-    k_lift<double><<<grid, 256, 0, s>>>(static_cast<const double *>(N), ldN, colors, drop, n, Wt,
-                                         static_cast<double *>(out), ldO);
-  } else {
-    static int grid = 0;
-    if (!grid) grid = persistent_grid(k_lift<float>, 256, 0, num_sms);
-    k_lift<float><<<grid, 256, 0, s>>>(static_cast<const float *>(N), ldN, colors, drop, n, Wt,
-                                        static_cast<float *>(out), ldO);
-  }
-  return 1;
+int launch_gather(int elem, const GatherArgs &a, int num_sms, cudaStream_t s) {
+  return elem == 8 ? gather_typed<double>(a, num_sms, s) : gather_typed<float>(a, num_sms, s);
 }
 
 int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
@@ -547,14 +531,13 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
 }
 
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, const uint16_t *comp,
-                const uint8_t *colors, int64_t n, double *partials, int n_partials, double *per_vertex,
-                double *result, cudaStream_t s) {
+                int64_t n, double *partials, int n_partials, double *per_vertex, double *result, cudaStream_t s) {
   if (elem == 8)
     k_root<double><<<n_partials, 256, 0, s>>>(static_cast<const double *>(A), ldA, WA, static_cast<const double *>(N),
-                                               ldN, comp, colors, n, partials, per_vertex);
+                                               ldN, comp, n, partials, per_vertex);
   else
     k_root<float><<<n_partials, 256, 0, s>>>(static_cast<const float *>(A), ldA, WA, static_cast<const float *>(N),
-                                              ldN, comp, colors, n, partials, per_vertex);
+                                              ldN, comp, n, partials, per_vertex);
   k_reduce<<<1, 32, 0, s>>>(partials, n_partials, result);
   return 2;
 }

@@ -1,7 +1,13 @@
 // kernels.cuh -- device kernels of the colour-coding DP (sm_100a) and their
-// host launchers.  All kernels are templated on the table storage type T
-// (double for CC_FP64, float for CC_FP32); neighbour sums and root products
-// accumulate in double.
+// host launchers.  Tables use the COLOUR-COMPRESSED row layout (DESIGN.md
+// "Data layout"): the row of vertex v (colour c) of a sub-template of size t
+// holds only the colour sets S that contain c -- the only ones that can be
+// non-zero -- indexed by the colex rank of S' = sq_c(S \ {c}) in the
+// (k-1)-colour universe (sq_c shifts colours above c down by one), i.e.
+// C(k-1, t-1) entries.  Neighbour sums N''(v, Y'') are indexed by
+// Y'' = sq_c(Y), |Y| = p, Y not containing c: C(k-1, p) entries.
+// Storage type T = double (CC_FP64) or float (CC_FP32); neighbour sums and
+// root products accumulate in double.
 #pragma once
 
 #include <cstdint>
@@ -15,6 +21,7 @@ namespace dev {
 //   light[i]       vertices whose [beg, end) range has <= s neighbours
 //   seg_*          segments of heavy vertices, grouped per heavy vertex
 //   hv_first/nseg  first segment and segment count of heavy vertex h
+// Items are numbered segments first, then light vertices.
 struct AggWork {
   const int32_t *light = nullptr;
   int64_t n_light = 0;
@@ -25,45 +32,50 @@ struct AggWork {
   int64_t n_seg = 0, n_hv = 0;
 };
 
-struct AggArgs {
-  const int64_t *beg;    // per vertex: first neighbour position
-  const int64_t *end;    // per vertex: one past the last
-  const int32_t *col;    // neighbour row ids into src
-  const void *src;       // passive table P (rows x ld_src)
+struct GatherArgs {
+  const int64_t *beg;     // per vertex: first neighbour position of this pass
+  const int64_t *end;     // per vertex: one past the last
+  const int32_t *col;     // neighbour ids, colour-sorted within each item
+  const uint16_t *goff;   // per item: 16 cumulative colour-group end offsets (relative to item begin)
+  const uint8_t *colors;  // colour of every row (owned | halo)
+  const void *src;        // passive table P' (rows x ld_src), W_in = C(k-1, p-1) valid columns
   int64_t ld_src;
-  void *dst;             // N (rows x ld_dst)
+  int W_in;
+  const uint16_t *map;    // [c_u][c_v][W_in] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
+  void *dst;              // N'' (rows x ld_dst), W_out = C(k-1, p)
   int64_t ld_dst;
-  int W;                 // valid columns
-  int accumulate;        // 0: dst = sum; 1: dst += sum
-  double *scratch;       // n_seg x W_pad doubles (heavy partials)
+  int W_out;
+  int k;
+  int accumulate;         // 0: dst = sum; 1: dst += sum
+  double *scratch;        // n_seg x ld_scratch doubles (heavy partial rows)
   int64_t ld_scratch;
-  unsigned int *arrive;  // n_hv x nchunks counters (zeroed before launch)
+  unsigned int *arrive;   // n_hv counters (zeroed before launch)
   AggWork work;
 };
 
-// Launchers.  `elem` = sizeof(T) (8 or 4).  Return the number of launches.
 int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *out, cudaStream_t s);
+// Colour-sort every item's neighbour range (stable) into col_out and record
+// the 16 cumulative colour-group offsets of the item.
+int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
+                 const AggWork &work, int32_t *col_out, uint16_t *goff, int num_sms, cudaStream_t s);
+// N''(v, {y}) = #{u in N(v) : sq_{c_v}(col u) = y}, k-1 columns.
 int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                 const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s);
-// Aggregation: chooses group width / chunking from W and chunk_cols.
-int launch_agg(int elem, const AggArgs &a, int64_t chunk_cols, int num_sms, int *nchunks_out,
-               cudaStream_t s);
-int launch_lift(int elem, const void *N, int64_t ldN, const uint8_t *colors, const uint16_t *drop,
-                int64_t n, int Wt, void *out, int64_t ldO, int num_sms, cudaStream_t s);
+// The neighbour sum of a passive table of size p >= 2 (compressed).
+int launch_gather(int elem, const GatherArgs &a, int num_sms, cudaStream_t s);
 int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms,
                    cudaStream_t s);
 // Root step + deterministic reduction into result[0] (double).  A == nullptr
-// means the single-vertex active part (a = 1): sum_v N(v, comp1[col v]).
+// means a single-vertex active part: sum_v N''(v, [k-1]) (one column).
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN,
-                const uint16_t *comp, const uint8_t *colors, int64_t n, double *partials,
-                int n_partials, double *per_vertex, double *result, cudaStream_t s);
+                const uint16_t *comp, int64_t n, double *partials, int n_partials, double *per_vertex,
+                double *result, cudaStream_t s);
 // Halo pack: out[i, :] = src[idx[i], :] for i < rows (whole padded rows).
 int launch_pack(int elem, const void *src, int64_t ld, const int32_t *idx, int64_t rows, void *out,
                 cudaStream_t s);
 
-int agg_partials_blocks(int num_sms);  // grid size used by launch_root partials
-int agg_nchunks(int elem, int W, int64_t chunk_cols);  // column chunks launch_agg will use
+int root_partials_blocks(int num_sms);  // grid size used by launch_root partials
 
 }  // namespace dev
 }  // namespace cc

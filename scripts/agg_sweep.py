@@ -34,7 +34,7 @@ for seg in map(int, args.segs.split(",")):
         cc.cc_set_template(ctx, cfg.parent)
         load_s = time.time() - t
         for var in args.variants.split(","):
-            os.environ["CC_AGG_VARIANT"] = var
+            os.environ["CC_GATHER_VARIANT"] = var
             cc.cc_color(ctx, 2)
             cc.cc_count_colorful(ctx)  # warm
             best = None
@@ -46,6 +46,6 @@ for seg in map(int, args.segs.split(",")):
                     best = p
             st = cc.cc_last_stats(ctx)
             print(json.dumps({"variant": var, "seg": seg, "chunk": chunk, "load_s": round(load_s, 1),
-                              "agg_GBs": round(st["agg_bytes"] / best["aggregate"] / 1e6, 1),
+                              "agg_GBs": round(st["agg_bytes"] / best["gather"] / 1e6, 1),
                               **{k: round(v, 3) for k, v in best.items()}}), flush=True)
         cc.cc_destroy(ctx)
