@@ -1,0 +1,96 @@
+"""-m "not gpu": the N > 1 host path on CPU with world-size-2 gloo.
+
+Each rank takes its 1D-partition plan from the product library
+(`cc_partition_plan`, the same host code `cc_load_graph` runs), exchanges the
+boundary rows of a passive table with its peer exactly as the plan says (send
+lists in the peer's receive order), aggregates over its local CSR, and checks
+the result against the single-process neighbour sum.  This is the exchange
+protocol of Alg. 2 that the NCCL path implements.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synth
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, scale, W, errq):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import torch
+
+        import paper_1804_09764_b200 as cc
+        g = synth.rmat(scale, 8, seed=5)
+        P = np.random.default_rng(1).random((g.n, W))  # a passive table, rows by original id
+        plan = cc.cc_partition_plan(g.n, g.row_ptr, g.col, world, rank)
+        n_own = len(plan["own_orig"])
+        n_halo = len(plan["halo_orig"])
+        local = np.zeros((n_own + n_halo, W))
+        local[:n_own] = P[plan["own_orig"]]
+        # grouped send/recv with every peer (the NCCL step)
+        reqs = []
+        for q in range(world):
+            if q == rank:
+                continue
+            s0, s1 = plan["send_off"][q], plan["send_off"][q + 1]
+            send = torch.from_numpy(np.ascontiguousarray(local[plan["send_idx"][s0:s1]]))
+            reqs.append(dist.isend(send, q))
+        for q in range(world):
+            if q == rank:
+                continue
+            r0, r1 = plan["recv_off"][q], plan["recv_off"][q + 1]
+            buf = torch.zeros((r1 - r0, W), dtype=torch.float64)
+            dist.recv(buf, q)
+            local[n_own + r0:n_own + r1] = buf.numpy()
+        for r in reqs:
+            r.wait()
+        # the halo rows are the rows of the global table
+        assert np.array_equal(local[n_own:], P[plan["halo_orig"]])
+        # local aggregation == global aggregation on owned rows
+        rp, col = plan["rp"], plan["col"]
+        N_local = np.add.reduceat(local[col], rp[:-1], axis=0) if len(col) else np.zeros((n_own, W))
+        N_local[np.diff(rp) == 0] = 0
+        src = np.repeat(np.arange(g.n), g.degrees())
+        N_global = np.zeros((g.n, W))
+        np.add.at(N_global, src, P[g.col])
+        assert np.allclose(N_local, N_global[plan["own_orig"]], rtol=1e-12, atol=0)
+        # every rank derived the same partition: owned sets are disjoint and cover
+        owned = [None] * world
+        dist.all_gather_object(owned, plan["own_orig"].tolist())
+        allv = sorted(v for o in owned for v in o)
+        assert allv == sorted(np.nonzero(g.degrees())[0].tolist())
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+@pytest.mark.parametrize("world", [2])
+def test_halo_exchange_gloo_world2(world):
+    import __graft_entry__
+    __graft_entry__._product_build()
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 11, 6, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
