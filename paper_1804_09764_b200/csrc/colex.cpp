@@ -79,16 +79,18 @@ std::vector<uint16_t> drop_table(int k, int t) {
 uint32_t squeeze(uint32_t mask, int c) { return (mask & ((1u << c) - 1u)) | ((mask >> (c + 1)) << c); }
 uint32_t unsqueeze(uint32_t mask, int c) { return (mask & ((1u << c) - 1u)) | ((mask >> c) << (c + 1)); }
 
+int64_t gather_map_ld(int k, int p) { return (binom(k - 1, p - 1) + 7) / 8 * 8; }
+
 std::vector<uint16_t> gather_map(int k, int p) {
-  const int64_t w_in = binom(k - 1, p - 1);
-  std::vector<uint16_t> out((size_t)(k * k * w_in), 0xFFFF);
+  const int64_t w_in = binom(k - 1, p - 1), ld = gather_map_ld(k, p);
+  std::vector<uint16_t> out((size_t)(k * k * ld), 0xFFFF);
   for (int cu = 0; cu < k; ++cu)
     for (int cv = 0; cv < k; ++cv) {
       if (cu == cv) continue;
       for (int64_t r = 0; r < w_in; ++r) {
         const uint32_t Y = unsqueeze(colex_unrank(p - 1, r), cu) | (1u << cu);  // u's colour set
         if (Y >> cv & 1u) continue;                                             // meets v's colour
-        out[(size_t)((cu * k + cv) * w_in + r)] = (uint16_t)colex_rank(squeeze(Y, cv));
+        out[(size_t)((cu * k + cv) * ld + r)] = (uint16_t)colex_rank(squeeze(Y, cv));
       }
     }
   return out;

@@ -41,6 +41,7 @@ uint32_t unsqueeze(uint32_t mask, int c);
 // (k-1)-universe of cu), out[(cu*k + cv) * C(k-1,p-1) + r] = rank of
 // sq_cv({cu} u us_cu(Y')) in C(k-1, p), or 0xFFFF if that set contains cv.
 std::vector<uint16_t> gather_map(int k, int p);
+int64_t gather_map_ld(int k, int p);  // map row stride: C(k-1,p-1) rounded up to 8 (padding 0xFFFF)
 
 // ---------------------------------------------------------------- plan.cpp
 // One DP step (t; a, p): T_out(v, S) = sum_{S1 u S2 = S} A(v, S1) N_P(v, S2),

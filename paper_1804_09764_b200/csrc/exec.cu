@@ -173,6 +173,7 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate) {
   a.ld_src = c->ld_of(W_in);
   a.W_in = W_in;
   a.map = c->d_map[p];
+  a.map_ld = gather_map_ld(k, p);
   a.dst = N;
   a.ld_dst = c->ld_of(W_out);
   a.W_out = W_out;

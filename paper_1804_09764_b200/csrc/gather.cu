@@ -1,0 +1,501 @@
+// gather.cu -- the neighbour-sum kernels of the DP (sm_100a).
+//
+//   k_csort        per colouring: stable sort of every work item's neighbour
+//                  range by neighbour colour, recording the 16 colour-group
+//                  ends (neighbours whose compressed rows share an index space
+//                  become contiguous)
+//   k_hist         N''(v, {y}): neighbour counts per colour -- the neighbour
+//                  sum of the single-vertex table (passive part of size 1)
+//   k_gather_ring  N''(v, Y'') = sum_{u in N(v)} P(u, Y): the inner sum over
+//                  u of Eq. 1, SpMM-shaped.  Rows of the
+//                  compressed passive table are fetched with cp.async into a
+//                  per-group shared-memory ring; per colour group they are
+//                  summed in registers and expanded once into the vertex's
+//                  N'' row in shared memory through the colour-pair map.
+//                  Heavy neighbour lists are split into segments (Alg. 4,
+//                  PAPER.md lines 494-523) whose partial rows the last
+//                  arriving segment sums in segment order (deterministic).
+//   k_gather       the same computation with plain register loads (kept as
+//                  the comparison variant, CC_GATHER_IMPL=reg).
+#include <algorithm>
+#include <cstdlib>
+
+#include "dev_common.cuh"
+
+namespace cc {
+namespace dev {
+
+namespace {
+
+// ------------------------------------------------------------------ colour sort
+// One warp per item.  Pass 1 counts colours; pass 2 places each neighbour at
+// base[colour] + (rank among equal colours in this 32-wide window): stable.
+__global__ void __launch_bounds__(256) k_csort(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+                                               const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
+                                               AggWork work, int32_t *__restrict__ col_out,
+                                               uint16_t *__restrict__ goff) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const int64_t n_items = work.n_seg + work.n_light;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; it < n_items; it += nwarps) {
+    int32_t v;
+    int64_t b, e;
+    item_range(work, beg, end, it, v, b, e);
+    int cnt[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cnt[j] = 0;
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int c = colors[__ldg(col + p)];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cnt[j] += (c == j);
+    }
+    int base[16];
+    int run = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
+      base[j] = run;
+      run += cnt[j];
+      if (lane == j) goff[it * 16 + j] = (uint16_t)run;
+    }
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+      const bool ok = p0 + lane < e;
+      const int32_t u = ok ? __ldg(col + p0 + lane) : 0;
+      const int c = ok ? (int)colors[u] : 16;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const unsigned m = __ballot_sync(0xffffffffu, c == j);
+        if (c == j) col_out[b + base[j] + __popc(m & lt)] = u;
+        base[j] += __popc(m);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ hist (p = 1)
+// Heavy segments add their counts atomically into a zeroed row: the values
+// are small integers, exact in fp32/fp64, so the result is order-independent.
+template <typename T, int G>
+__global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+                                              const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
+                                              AggWork work, int k, T *__restrict__ out, int64_t ld) {
+  constexpr int U = 4;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned gmask = group_mask<G>();
+  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
+  const int64_t n_items = work.n_seg + work.n_light;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
+    int32_t v;
+    int64_t b, e;
+    const bool heavy = item_range(work, beg, end, it, v, b, e);
+    int cnt[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cnt[j] = 0;
+    for (int64_t e0 = b + lane; e0 < e; e0 += G * U) {
+      int32_t u[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) u[q] = e0 + q * G < e ? __ldg(col + e0 + q * G) : -1;
+      int c[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) c[q] = u[q] >= 0 ? (int)colors[u[q]] : 16;
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cnt[j] += (c[q] == j);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) cnt[j] += __shfl_xor_sync(gmask, cnt[j], o, G);
+    const int cv = colors[v];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j % G == lane && j < k && j != cv) {
+        T *p = out + (int64_t)v * ld + (j < cv ? j : j - 1);  // squeeze: sq_{c_v}(j)
+        if (heavy) atomicAdd(p, (T)cnt[j]);
+        else *p = (T)cnt[j];
+      }
+  }
+}
+
+// ------------------------------------------------------------------ shared epilogue
+// Write the item's N'' row (light vertex) or its partial (heavy segment; the
+// last arriving segment of the vertex sums all partials in segment order).
+template <typename T, int G>
+__device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const double *sacc, int64_t it, int32_t v,
+                                                bool heavy, int lane, unsigned gmask) {
+  T *drow = static_cast<T *>(a.dst) + (int64_t)v * a.ld_dst;
+  if (!heavy) {
+    for (int j = lane; j < a.W_out; j += G) {
+      double x = sacc[j];
+      if (a.accumulate) x += (double)drow[j];
+      drow[j] = (T)x;
+    }
+    return;
+  }
+  double *sp = a.scratch + it * a.ld_scratch;
+  for (int j = lane; j < a.W_out; j += G) sp[j] = sacc[j];
+  __threadfence();
+  __syncwarp(gmask);
+  const int32_t hv = a.work.seg_hv[it];
+  unsigned prev = 0;
+  if (lane == 0) prev = atomicAdd(&a.arrive[hv], 1u);
+  prev = __shfl_sync(gmask, prev, 0, G);
+  if (prev == (unsigned)(a.work.hv_nseg[hv] - 1)) {
+    __threadfence();
+    const int32_t s0 = a.work.hv_first[hv], ns = a.work.hv_nseg[hv];
+    for (int j = lane; j < a.W_out; j += G) {
+      double x = 0.0;
+      for (int s = 0; s < ns; ++s) x += __ldcg(a.scratch + (int64_t)(s0 + s) * a.ld_scratch + j);
+      if (a.accumulate) x += (double)drow[j];
+      drow[j] = (T)x;
+    }
+  }
+}
+
+// expand one colour group's column sums into N'' (map injective per colour pair)
+template <int NV, int VW, int G>
+__device__ __forceinline__ void expand(const GatherArgs &a, int cu, int cv, int c0, double (&acc)[NV][VW],
+                                       double *sacc) {
+  const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int y0 = c0 + j * G * VW;
+    uint16_t m[VW];
+    if (y0 < a.W_in) {
+      if (VW == 4) {
+        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + y0));
+        m[0] = w.x & 0xFFFF;
+        m[1] = w.x >> 16;
+        m[2 % VW] = w.y & 0xFFFF;
+        m[3 % VW] = w.y >> 16;
+      } else {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + y0));
+        m[0] = w & 0xFFFF;
+        m[1 % VW] = w >> 16;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < VW; ++q) m[q] = 0xFFFF;
+    }
+#pragma unroll
+    for (int q = 0; q < VW; ++q) {
+      if (m[q] != 0xFFFF) sacc[m[q]] += acc[j][q];
+      acc[j][q] = 0.0;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ gather, cp.async ring
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// fp32 rows are summed in blocks of up to 8 consecutive rows in fp32 and the
+// blocks in fp64 (relative error <= 7 u32 + O(n u64) per entry; DESIGN.md
+// reading C-6); fp64 rows are summed in fp64.
+template <typename T, int G, int NV, int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch) {
+  using V = typename Vec<T>::type;
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = G * NV * VW;  // input columns per pass
+  constexpr int BLK = 8;            // fp32 block length
+  extern __shared__ __align__(16) unsigned char smem_ring[];
+  const int lane = threadIdx.x & (G - 1);
+  const int grp = threadIdx.x / G;
+  const unsigned gmask = group_mask<G>();
+  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
+  const int64_t n_items = a.work.n_seg + a.work.n_light;
+  const int groups_per_block = blockDim.x / G;
+  V *ring = reinterpret_cast<V *>(smem_ring) + (int64_t)grp * D * NV * G;  // [D][NV][G]
+  double *sacc = reinterpret_cast<double *>(reinterpret_cast<V *>(smem_ring) + (int64_t)groups_per_block * D * NV * G) +
+                 (int64_t)grp * a.W_out;
+  const T *__restrict__ src = static_cast<const T *>(a.src);
+
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
+    int32_t v;
+    int64_t b, e;
+    const bool heavy = item_range(a.work, a.beg, a.end, it, v, b, e);
+    const int cv = a.colors[v];
+    for (int j = lane; j < a.W_out; j += G) sacc[j] = 0.0;
+    __syncwarp(gmask);
+    const uint16_t *go = a.goff + it * 16;
+    // the stream = the item's neighbours minus the group of v's own colour
+    const int cv_lo = cv == 0 ? 0 : go[cv - 1], cv_hi = go[cv];
+    const int skip = cv_hi - cv_lo;
+    const int n_s = (int)(e - b) - skip;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int c0 = ch * CAP + lane * VW;
+      int nbytes[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) nbytes[j] = c0 + j * G * VW < a.W_in ? 16 : 0;
+      // neighbour ids: a window of G stream positions per lane, one window ahead
+      auto load_idx = [&](int r) -> int32_t {
+        return r < n_s ? __ldg(a.col + b + (r < cv_lo ? r : r + skip)) : 0;
+      };
+      int win = 0;
+      int32_t idx_cur = load_idx(lane), idx_nxt = load_idx(G + lane);
+      auto issue = [&](int r) {
+        if (r >= win + G) {
+          win += G;
+          idx_cur = idx_nxt;
+          idx_nxt = load_idx(win + G + lane);
+        }
+        const int32_t u = __shfl_sync(gmask, idx_cur, r - win, G);
+        if (r < n_s) {
+          const T *row = src + (int64_t)u * a.ld_src + c0;
+          V *slot = ring + (r % D) * NV * G + lane;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) cp_async16(slot + j * G, nbytes[j] ? row + j * G * VW : row, nbytes[j]);
+        }
+        cp_async_commit();
+      };
+#pragma unroll
+      for (int r = 0; r < D - 1; ++r) issue(r);
+      // current colour group (stream coordinates)
+      int gc = 0, gend_s = 0;
+      auto next_group = [&]() {
+        while (gc < a.k) {
+          const int lo = gc == 0 ? 0 : go[gc - 1], hi = go[gc];
+          if (gc != cv && hi > lo) {
+            gend_s = hi - (gc > cv ? skip : 0);
+            return;
+          }
+          ++gc;
+        }
+      };
+      next_group();
+      double acc[NV][VW];
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int q = 0; q < VW; ++q) acc[j][q] = 0.0;
+      float4 blk[NV];
+      int nb = 0;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) blk[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < n_s; ++i) {
+        issue(i + D - 1);
+        cp_async_wait<D - 1>();
+        const V *slot = ring + (i % D) * NV * G + lane;
+        if constexpr (VW == 4) {  // fp32 storage: fp32 blocks of BLK rows
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            const float4 x = reinterpret_cast<const float4 *>(slot)[j * G];
+            blk[j].x += x.x;
+            blk[j].y += x.y;
+            blk[j].z += x.z;
+            blk[j].w += x.w;
+          }
+          const bool gend = i + 1 == gend_s;
+          if (++nb == BLK || gend) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              add_vec(acc[j], blk[j]);
+              blk[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            nb = 0;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < NV; ++j) add_vec(acc[j], slot[j * G]);
+        }
+        if (i + 1 == gend_s) {  // end of a colour group: expand into N''
+          expand<NV, VW, G>(a, gc, cv, c0, acc, sacc);
+          __syncwarp(gmask);
+          ++gc;
+          next_group();
+        }
+      }
+      cp_async_wait<0>();
+      __syncwarp(gmask);
+    }
+    gather_epilogue<T, G>(a, sacc, it, v, heavy, lane, gmask);
+    __syncwarp(gmask);
+  }
+}
+
+// ------------------------------------------------------------------ gather, register rounds
+template <typename T, int G, int NV, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_gather(GatherArgs a, int nch) {
+  using V = typename Vec<T>::type;
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = G * NV * VW;
+  extern __shared__ double sacc_all[];
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned gmask = group_mask<G>();
+  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
+  const int64_t n_items = a.work.n_seg + a.work.n_light;
+  double *sacc = sacc_all + (threadIdx.x / G) * (int64_t)a.W_out;
+  const T *__restrict__ src = static_cast<const T *>(a.src);
+
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
+    int32_t v;
+    int64_t b, e;
+    const bool heavy = item_range(a.work, a.beg, a.end, it, v, b, e);
+    const int cv = a.colors[v];
+    for (int j = lane; j < a.W_out; j += G) sacc[j] = 0.0;
+    __syncwarp(gmask);
+    const uint16_t *go = a.goff + it * 16;
+    int gstart = 0;
+    for (int cu = 0; cu < a.k; ++cu) {
+      const int gend = go[cu];
+      if (cu != cv && gend > gstart) {
+        for (int ch = 0; ch < nch; ++ch) {
+          const int c0 = ch * CAP + lane * VW;
+          bool valid[NV];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) valid[j] = c0 + j * G * VW < a.W_in;
+          double acc[NV][VW];
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int q = 0; q < VW; ++q) acc[j][q] = 0.0;
+          for (int64_t e0 = b + gstart; e0 < b + gend; e0 += G) {
+            const int cnt = (int)min((int64_t)G, b + gend - e0);
+            const int32_t my_u = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
+            for (int j0 = 0; j0 < cnt; j0 += U) {
+              V vals[U][NV];
+#pragma unroll
+              for (int uu = 0; uu < U; ++uu) {
+                const int32_t u = __shfl_sync(gmask, my_u, (j0 + uu) & (G - 1), G);
+                const T *row = src + (int64_t)u * a.ld_src + c0;
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                  if (j0 + uu < cnt && valid[j]) vals[uu][j] = ldg_vec(row + j * G * VW);
+                  else zero_vec(vals[uu][j]);
+                }
+              }
+#pragma unroll
+              for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+                for (int j = 0; j < NV; ++j) add_vec(acc[j], vals[uu][j]);
+            }
+          }
+          expand<NV, VW, G>(a, cu, cv, c0, acc, sacc);
+        }
+        __syncwarp(gmask);
+      }
+      gstart = gend;
+    }
+    gather_epilogue<T, G>(a, sacc, it, v, heavy, lane, gmask);
+    __syncwarp(gmask);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+template <typename T, int G, int NV, int D, int MINB = 1>
+void ring_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = G * NV * VW;
+  auto kern = k_gather_ring<T, G, NV, D, MINB>;
+  const size_t per_group = (size_t)D * NV * G * 16 + (size_t)a.W_out * sizeof(double);
+  int groups = 256 / G;
+  while (groups > 1 && per_group * groups > 100 * 1024) groups /= 2;
+  const int threads = groups * G;
+  const size_t smem = per_group * groups;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, threads, smem, num_sms);
+  const int nch = (a.W_in + CAP - 1) / CAP;
+  kern<<<grid, threads, smem, s>>>(a, nch);
+}
+
+template <typename T, int G, int NV, int U, int MINB = 1>
+void reg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = G * NV * VW;
+  auto kern = k_gather<T, G, NV, U, MINB>;
+  const size_t row = (size_t)a.W_out * sizeof(double);
+  int groups = 256 / G;
+  while (groups > 1 && row * groups > 96 * 1024) groups /= 2;
+  const int threads = groups * G;
+  const size_t smem = row * groups;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, threads, smem, num_sms);
+  const int nch = (a.W_in + CAP - 1) / CAP;
+  kern<<<grid, threads, smem, s>>>(a, nch);
+}
+
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+template <typename T>
+void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  const int wvec = (a.W_in + VW - 1) / VW;
+  const char *impl = getenv("CC_GATHER_IMPL");  // "reg": register rounds; default: cp.async ring
+  if (impl && impl[0] == 'r' && impl[1] == 'e') {
+    if (wvec <= 4) reg_go<T, 4, 1, 4, 3>(a, num_sms, s);
+    else if (wvec <= 8) reg_go<T, 8, 1, 4, 3>(a, num_sms, s);
+    else if (wvec <= 16) reg_go<T, 16, 1, 8, 3>(a, num_sms, s);
+    else reg_go<T, 32, 1, 4, 4>(a, num_sms, s);
+    return;
+  }
+  const int vr = env_int("CC_RING_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
+  if (wvec <= 4) ring_go<T, 4, 1, 16, 2>(a, num_sms, s);
+  else if (wvec <= 8) ring_go<T, 8, 1, 16, 2>(a, num_sms, s);
+  else if (wvec <= 16) ring_go<T, 16, 1, 16, 2>(a, num_sms, s);
+  else if (wvec <= 32) ring_go<T, 32, 1, 16, 2>(a, num_sms, s);
+  else if (wvec <= 64) {
+    if (vr == 1) ring_go<T, 32, 2, 4, 2>(a, num_sms, s);
+    else ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
+  } else {
+    switch (vr) {
+      case 1: ring_go<T, 32, 4, 8, 2>(a, num_sms, s); break;
+      case 2: ring_go<T, 32, 4, 2, 3>(a, num_sms, s); break;
+      case 3: ring_go<T, 32, 4, 6, 2>(a, num_sms, s); break;
+      default: ring_go<T, 32, 4, 4, 2>(a, num_sms, s); break;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
+                 const AggWork &work, int32_t *col_out, uint16_t *goff, int num_sms, cudaStream_t s) {
+  if (work.n_seg + work.n_light == 0) return 0;
+  static int grid = 0;
+  if (!grid) grid = persistent_grid(k_csort, 256, 0, num_sms);
+  k_csort<<<grid, 256, 0, s>>>(beg, end, col, colors, work, col_out, goff);
+  return 1;
+}
+
+int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
+                const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s) {
+  if (work.n_seg + work.n_light == 0) return 0;
+  int launches = 1;
+  if (work.n_seg) {  // heavy rows accumulate segment counts atomically
+    cudaMemsetAsync(out, 0, (size_t)n * ld * elem, s);
+    ++launches;
+  }
+  if (elem == 8) {
+    static int grid = 0;
+    if (!grid) grid = persistent_grid(k_hist<double, 8>, 256, 0, num_sms);
+    k_hist<double, 8><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, static_cast<double *>(out), ld);
+  } else {
+    static int grid = 0;
+    if (!grid) grid = persistent_grid(k_hist<float, 8>, 256, 0, num_sms);
+    k_hist<float, 8><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, static_cast<float *>(out), ld);
+  }
+  return launches;
+}
+
+int launch_gather(int elem, const GatherArgs &a, int num_sms, cudaStream_t s) {
+  if (a.work.n_seg + a.work.n_light == 0) return 0;
+  if (elem == 8) gather_typed<double>(a, num_sms, s);
+  else gather_typed<float>(a, num_sms, s);
+  return 1;
+}
+
+}  // namespace dev
+}  // namespace cc

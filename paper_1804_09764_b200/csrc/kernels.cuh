@@ -41,7 +41,8 @@ struct GatherArgs {
   const void *src;        // passive table P' (rows x ld_src), W_in = C(k-1, p-1) valid columns
   int64_t ld_src;
   int W_in;
-  const uint16_t *map;    // [c_u][c_v][W_in] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
+  const uint16_t *map;    // [c_u][c_v][map_ld] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
+  int64_t map_ld;         // map row stride (multiple of 8 entries, padding = 0xFFFF)
   void *dst;              // N'' (rows x ld_dst), W_out = C(k-1, p)
   int64_t ld_dst;
   int W_out;

@@ -1,6 +1,10 @@
-"""Tuning sweep (GPU): per-phase device ms of one colouring for each
-aggregation-kernel variant / chunk width / segment length.  Not a bench."""
+"""Tuning sweep (GPU): per-phase device ms of one colouring for each kernel
+variant (environment knobs) / segment length.  Not a bench.
+
+  --envs "CC_GATHER_IMPL=reg;CC_RING_VARIANT=0,1,2"
+expands to the cartesian product of the listed values."""
 import argparse
+import itertools
 import json
 import os
 import sys
@@ -13,12 +17,18 @@ import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
-ap.add_argument("--variants", default="0,1,2,4")
+ap.add_argument("--envs", default="CC_RING_VARIANT=0")
 ap.add_argument("--segs", default="4096")
-ap.add_argument("--chunks", default="0")
 ap.add_argument("--precision", default=None)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--check", action="store_true", help="compare every variant's count with the first")
 args = ap.parse_args()
+
+knobs = []
+for part in args.envs.split(";"):
+    name, vals = part.split("=")
+    knobs.append([(name, v) for v in vals.split(",")])
+combos = list(itertools.product(*knobs))
 
 cfg = synth.CONFIGS[args.config]
 t = time.time()
@@ -26,26 +36,31 @@ g = cfg.graph()
 print(f"graph {cfg.name}: n={g.n} 2m={g.nnz} gen {time.time() - t:.1f}s", flush=True)
 prec = args.precision or cfg.precision
 for seg in map(int, args.segs.split(",")):
-    for chunk in map(int, args.chunks.split(",")):
-        ctx = cc.cc_create(device=0, precision=cc.CC_FP32 if prec == "fp32" else cc.CC_FP64, segment_len=seg,
-                           chunk_cols=chunk)
-        t = time.time()
-        cc.cc_load_graph(ctx, g.n, g.row_ptr, g.col)
-        cc.cc_set_template(ctx, cfg.parent)
-        load_s = time.time() - t
-        for var in args.variants.split(","):
-            os.environ["CC_GATHER_VARIANT"] = var
-            cc.cc_color(ctx, 2)
-            cc.cc_count_colorful(ctx)  # warm
-            best = None
-            for r in range(args.reps):
-                cc.cc_color(ctx, 2 + r)
-                x = cc.cc_count_colorful(ctx)
-                p = cc.cc_last_profile(ctx)
-                if best is None or p["total"] < best["total"]:
-                    best = p
-            st = cc.cc_last_stats(ctx)
-            print(json.dumps({"variant": var, "seg": seg, "chunk": chunk, "load_s": round(load_s, 1),
-                              "agg_GBs": round(st["agg_bytes"] / best["gather"] / 1e6, 1),
-                              **{k: round(v, 3) for k, v in best.items()}}), flush=True)
-        cc.cc_destroy(ctx)
+    ctx = cc.cc_create(device=0, precision=cc.CC_FP32 if prec == "fp32" else cc.CC_FP64, segment_len=seg)
+    t = time.time()
+    cc.cc_load_graph(ctx, g.n, g.row_ptr, g.col)
+    cc.cc_set_template(ctx, cfg.parent)
+    load_s = time.time() - t
+    ref = None
+    for combo in combos:
+        for name, val in combo:
+            os.environ[name] = val
+        cc.cc_color(ctx, 2)
+        cc.cc_count_colorful(ctx)  # warm
+        best = None
+        xs = []
+        for r in range(args.reps):
+            cc.cc_color(ctx, 2 + r)
+            xs.append(cc.cc_count_colorful(ctx))
+            p = cc.cc_last_profile(ctx)
+            if best is None or p["total"] < best["total"]:
+                best = p
+        st = cc.cc_last_stats(ctx)
+        if ref is None:
+            ref = xs
+        rec = {"env": dict(combo), "seg": seg, "load_s": round(load_s, 1),
+               "gather_GBs": round(st["agg_bytes"] / best["gather"] / 1e6, 1),
+               "same_as_first": xs == ref,
+               **{k: round(v, 3) for k, v in best.items()}}
+        print(json.dumps(rec), flush=True)
+    cc.cc_destroy(ctx)
