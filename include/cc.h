@@ -86,6 +86,10 @@ typedef struct {
   uint64_t relabel_seed; /* seed of the internal vertex permutation used to
                             balance the partition ("randomly
                             partitioned"); never changes results */
+  int32_t fixed_root;    /* 0 = the planner picks the DP root and child order
+                            minimising modelled bytes (the
+                            root "can be picked arbitrarily"); 1 = root at the
+                            parent -1 vertex, children in index order */
 } cc_options;
 
 /* Fill *opt with defaults: CC_FP64, device 0, world 1, rank 0, auto sizes,
@@ -209,6 +213,14 @@ cc_status cc_split_table(int32_t k, int32_t t, int32_t a, uint32_t *out, int64_t
 cc_status cc_plan_template(int32_t k, const int32_t *parent, int32_t *steps_out, int32_t cap_steps,
                            int32_t *n_steps, int64_t *aut, int64_t *aut_root, double *memory,
                            double *computation);
+
+/* The plan cc_set_template would choose with fixed_root = 0 for a graph of
+ * average degree avg_degree and elem-byte table entries (4 or 8): same
+ * outputs as cc_plan_template plus *root = the chosen DP root and *cost = its
+ * modelled bytes per stored vertex. */
+cc_status cc_plan_template_auto(int32_t k, const int32_t *parent, double avg_degree, int32_t elem,
+                                int32_t *steps_out, int32_t cap_steps, int32_t *n_steps, int32_t *root,
+                                double *cost);
 
 /* Partition plan of the 1D vertex partition (Alg. 2 line 2 and lines
  * 374-382) for rank `rank` of `world`, computed on the host exactly as

@@ -170,6 +170,16 @@ def cc_plan_template(parent) -> dict:
     return dict(steps=st, aut=aut.value, aut_root=aut_root.value, memory=mem.value, computation=comp.value)
 
 
+def cc_plan_template_auto(parent, avg_degree: float = 32.0, elem: int = 4) -> dict:
+    par = np.ascontiguousarray(parent, dtype=np.int32)
+    steps = np.zeros((64, 6), dtype=np.int32)
+    ns, root, cost = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+    _check(None, _lib.cc_plan_template_auto(len(par), _p(par), avg_degree, elem, _p(steps), 64, ctypes.byref(ns),
+                                            ctypes.byref(root), ctypes.byref(cost)))
+    st = [dict(zip(("t", "a", "p", "active", "passive", "out"), map(int, r))) for r in steps[:ns.value]]
+    return dict(steps=st, root=root.value, cost=cost.value)
+
+
 def cc_partition_plan(n: int, row_ptr, col, world: int, rank: int, relabel_seed: int = 0x5eed) -> dict:
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
     cl = np.ascontiguousarray(col, dtype=np.int32)

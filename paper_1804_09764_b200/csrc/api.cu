@@ -108,6 +108,9 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   try {
     CUDA_OK(cudaSetDevice(opt->device));
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, opt->device));
+    int l2 = 0;
+    CUDA_OK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, opt->device));
+    if (l2 > 0) c->l2_bytes = l2;
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
     cudaMemPool_t pool;
@@ -156,17 +159,18 @@ cc_status cc_load_graph(cc_ctx *c, int64_t n, const int64_t *row_ptr, const int3
   free_persistent(c);
   alloc_scratch(c);
   cc::load_graph(c, g);
-  if (c->has_template) cc::upload_template(c);
+  if (c->has_template) cc::replan(c, false);
   API_END(c)
 }
 
 cc_status cc_set_template(cc_ctx *c, int32_t k, const int32_t *parent) {
   API_BEGIN(c)
-  cc::Plan p = cc::make_plan(k, parent);
-  c->plan = p;
-  c->has_template = true;
+  cc::make_plan(k, parent);  // validates (throws CC_ERR_TEMPLATE)
+  c->user_parent.assign(parent, parent + k);
   c->has_colors = false;
-  if (c->has_graph) cc::upload_template(c);
+  c->sorted_valid = false;
+  cc::replan(c, false);
+  c->has_template = true;
   API_END(c)
 }
 
@@ -251,8 +255,20 @@ cc_status cc_get_subtree_counts(cc_ctx *c, int32_t x, double *out) {
   API_BEGIN(c)
   if (!c->has_graph || !c->has_template || !c->has_colors) throw Error(CC_ERR_STATE, "needs graph, template, colouring");
   if (c->opt.world != 1) throw Error(CC_ERR_STATE, "cc_get_subtree_counts needs world == 1");
+  if (x < 0 || x >= c->plan.k || !out) throw Error(CC_ERR_ARG, "bad template vertex or NULL output");
+  // tables are defined for the user's rooting: plan with the fixed root for
+  // this call, restore the cost-model plan afterwards
+  struct Restore {
+    cc_ctx *c;
+    ~Restore() {
+      try {
+        cc::replan(c, false);
+      } catch (...) {
+      }
+    }
+  } restore{c};
+  cc::replan(c, true);
   const auto &pl = c->plan;
-  if (x < 0 || x >= pl.k || !out) throw Error(CC_ERR_ARG, "bad template vertex or NULL output");
   const auto &R = c->part;
   const int k = pl.k;
   const int tid = pl.full_table[x];
@@ -344,6 +360,38 @@ cc_status cc_plan_template(int32_t k, const int32_t *parent, int32_t *steps_out,
     if (aut_root) *aut_root = p.aut_root;
     if (memory) *memory = p.memory;
     if (computation) *computation = p.computation;
+  } catch (const Error &e) {
+    return e.status;
+  }
+  return CC_OK;
+}
+
+cc_status cc_plan_template_auto(int32_t k, const int32_t *parent, double avg_degree, int32_t elem,
+                                int32_t *steps_out, int32_t cap_steps, int32_t *n_steps, int32_t *root,
+                                double *cost) {
+  try {
+    if (elem != 4 && elem != 8) return CC_ERR_ARG;
+    cc::PlanOpts o;
+    o.auto_root = true;
+    o.avg_degree = avg_degree;
+    o.elem = elem;
+    cc::Plan p = cc::make_plan(k, parent, &o);
+    if (n_steps) *n_steps = (int32_t)p.steps.size();
+    if (steps_out) {
+      if (cap_steps < (int32_t)p.steps.size()) return CC_ERR_ARG;
+      for (size_t s = 0; s < p.steps.size(); ++s) {
+        const auto &st = p.steps[s];
+        int32_t *out = steps_out + 6 * s;
+        out[0] = st.t;
+        out[1] = st.a;
+        out[2] = st.p;
+        out[3] = st.active;
+        out[4] = st.passive;
+        out[5] = st.out;
+      }
+    }
+    if (root) *root = p.root;
+    if (cost) *cost = cc::plan_cost(p, o);
   } catch (const Error &e) {
     return e.status;
   }

@@ -63,7 +63,8 @@ struct TableInfo {
 
 struct Plan {
   int k = 0;
-  int root = -1;
+  int root = -1;       // root of the plan (chosen by the planner)
+  int user_root = -1;  // the parent -1 vertex of the user's array
   std::vector<int> parent;
   std::vector<Step> steps;
   std::vector<TableInfo> tables;
@@ -79,7 +80,17 @@ struct Plan {
   std::vector<int> n_first_use, n_last_use;
 };
 
-Plan make_plan(int k, const int32_t *parent);  // throws Error(CC_ERR_TEMPLATE)
+// Planner options.  auto_root: choose the root and child order minimising
+// plan_cost (the count of colourful maps does not depend on them, reading
+// C-4); otherwise the root is the parent -1 vertex, children in index order.
+struct PlanOpts {
+  bool auto_root = true;
+  double avg_degree = 32.0;  // adjacency entries per stored vertex
+  int elem = 4;              // table entry bytes
+  double fma_bytes = 0.25;   // weight of one combine FMA in bytes
+};
+Plan make_plan(int k, const int32_t *parent, const PlanOpts *opts = nullptr);  // throws Error(CC_ERR_TEMPLATE)
+double plan_cost(const Plan &P, const PlanOpts &o);
 
 // ---------------------------------------------------------------- graph.cpp
 // Validated CSR (copy) of the global graph.

@@ -72,6 +72,7 @@ struct cc_ctx {
   std::string err;
   bool poisoned = false;
   int num_sms = 148;
+  int64_t l2_bytes = 126LL << 20;
   cudaStream_t s_main = nullptr, s_comm = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<void *> persistent;  // cudaMalloc'd: graph, plan tables (freed on reload / destroy)
@@ -89,6 +90,7 @@ struct cc_ctx {
 
   // template
   bool has_template = false;
+  std::vector<int32_t> user_parent;  // the template as given (re-planned when the graph changes)
   cc::Plan plan;
   std::vector<uint32_t *> d_split;    // per step: split table (combine steps)
   std::vector<uint16_t *> d_map;      // per passive size p: gather map (p >= 2)
@@ -176,6 +178,9 @@ namespace cc {
 // exec.cu
 void load_graph(cc_ctx *c, const HostGraph &g);
 void upload_template(cc_ctx *c);
+// (Re)plan c->user_parent: fixed root if `fixed` or opt.fixed_root, else the
+// cost-model root for the loaded graph's average degree and table precision.
+void replan(cc_ctx *c, bool fixed);
 void launch_colouring(cc_ctx *c, uint64_t seed);
 // One colouring's DP.  dump_table >= 0 keeps every table and returns table
 // `dump_table` (compressed rows, owned order) in *dump; root_out receives the

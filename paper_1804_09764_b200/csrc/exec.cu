@@ -117,6 +117,15 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
   c->sorted_valid = false;
 }
 
+void replan(cc_ctx *c, bool fixed) {
+  PlanOpts o;
+  o.auto_root = !(fixed || c->opt.fixed_root);
+  o.elem = c->elem();
+  if (c->has_graph && c->n_own > 0) o.avg_degree = (double)c->part.col.size() / (double)c->n_own;
+  c->plan = make_plan((int)c->user_parent.size(), c->user_parent.data(), &o);
+  if (c->has_graph) upload_template(c);
+}
+
 void upload_template(cc_ctx *c) {
   for (auto *p : c->d_split) c->pfree(p);
   for (auto *p : c->d_map) c->pfree(p);
@@ -131,7 +140,13 @@ void upload_template(cc_ctx *c) {
     if (st.out < 0) {
       if (st.a > 1) c->d_comp = c->pupload(complement_table(k - 1, st.a - 1));
     } else if (st.a > 1) {
-      c->d_split[s] = c->pupload(split_table(k - 1, st.t - 1, st.a - 1));
+      // rows of the split table padded to a multiple of 8 outputs (16-byte
+      // aligned groups of split entries for the combine kernels)
+      const std::vector<uint32_t> tab = split_table(k - 1, st.t - 1, st.a - 1);
+      const int64_t WO = binom(k - 1, st.t - 1), WOp = (WO + 7) / 8 * 8, nq = binom(st.t - 1, st.a - 1);
+      std::vector<uint32_t> pad((size_t)(nq * WOp), 0);
+      for (int64_t q = 0; q < nq; ++q) std::copy(tab.begin() + q * WO, tab.begin() + (q + 1) * WO, pad.begin() + q * WOp);
+      c->d_split[s] = c->pupload(pad);
     }
     if (st.p > 1 && !c->d_map[st.p]) c->d_map[st.p] = c->pupload(gather_map(k, st.p));
   }
@@ -174,6 +189,11 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate) {
   a.W_in = W_in;
   a.map = c->d_map[p];
   a.map_ld = gather_map_ld(k, p);
+  {  // hub rows kept in L2: a fraction of the L2 (rows are degree-ordered, hubs first)
+    const char *f = getenv("CC_HUB_L2_FRAC");
+    const double frac = f ? atof(f) : 0.5;
+    a.hub_rows = (int64_t)(frac * (double)c->l2_bytes / (double)(a.ld_src * elem));
+  }
   a.dst = N;
   a.ld_dst = c->ld_of(W_out);
   a.W_out = W_out;

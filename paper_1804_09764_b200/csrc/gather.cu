@@ -189,9 +189,23 @@ __device__ __forceinline__ void expand(const GatherArgs &a, int cu, int cv, int 
 }
 
 // ------------------------------------------------------------------ gather, cp.async ring
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes, uint64_t policy) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes), "l"(policy)
+               : "memory");
+}
+// L2 policies: hub rows (the most re-gathered; internal ids are degree-ordered,
+// so they are the lowest row ids) are kept, all other rows stream through.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -219,6 +233,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
   double *sacc = reinterpret_cast<double *>(reinterpret_cast<V *>(smem_ring) + (int64_t)groups_per_block * D * NV * G) +
                  (int64_t)grp * a.W_out;
   const T *__restrict__ src = static_cast<const T *>(a.src);
+  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
 
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
     int32_t v;
@@ -253,8 +268,10 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
         if (r < n_s) {
           const T *row = src + (int64_t)u * a.ld_src + c0;
           V *slot = ring + (r % D) * NV * G + lane;
+          const uint64_t pol = u < a.hub_rows ? pol_keep : pol_stream;
 #pragma unroll
-          for (int j = 0; j < NV; ++j) cp_async16(slot + j * G, nbytes[j] ? row + j * G * VW : row, nbytes[j]);
+          for (int j = 0; j < NV; ++j)
+            cp_async16(slot + j * G, nbytes[j] ? row + j * G * VW : row, nbytes[j], pol);
         }
         cp_async_commit();
       };
@@ -451,8 +468,8 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
     else ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
   } else {
     switch (vr) {
-      case 1: ring_go<T, 32, 4, 8, 2>(a, num_sms, s); break;
-      case 2: ring_go<T, 32, 4, 2, 3>(a, num_sms, s); break;
+      case 1: ring_go<T, 32, 4, 5, 2>(a, num_sms, s); break;
+      case 2: ring_go<T, 32, 4, 3, 2>(a, num_sms, s); break;
       case 3: ring_go<T, 32, 4, 6, 2>(a, num_sms, s); break;
       default: ring_go<T, 32, 4, 4, 2>(a, num_sms, s); break;
     }

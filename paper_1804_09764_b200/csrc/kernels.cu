@@ -36,44 +36,115 @@ __global__ void k_color(const int32_t *__restrict__ orig, int64_t n, uint64_t se
 }
 
 // ------------------------------------------------------------------ combine (a >= 2)
-// V vertices per CTA: their A' and N'' rows are staged in shared memory; one
-// thread per output colour set walks the split table (coalesced, L1/L2
-// resident) and accumulates the V products in fp64.
+// V vertices per CTA: their A' and N'' rows are staged in shared memory
+// TRANSPOSED (column-major over the tile's vertices), so one 16-byte load
+// feeds VW vertices of the same split.  One thread per output colour set
+// walks the split table (coalesced, L1/L2 resident).  Accumulation is in the
+// storage type: fp64 tables -> DFMA; fp32 tables -> FFMA over at most
+// C(t-1, a-1) terms (relative error <= C(t-1,a-1) * 2^-24, C-6).
 template <typename T, int V>
 __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_t ldA, int WA,
                                                  const T *__restrict__ N, int64_t ldN, int WN,
                                                  const uint32_t *__restrict__ split, int nq, int64_t n,
                                                  T *__restrict__ out, int64_t ldO, int WO) {
+  using VT = typename Vec<T>::type;
+  constexpr int VW = Vec<T>::W;
+  static_assert(V % VW == 0, "tile must be a multiple of the vector width");
+  constexpr int SV = V == VW ? V : V + VW;  // padded row stride spreads rows over the banks
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *As = reinterpret_cast<T *>(smem_raw);
-  T *Ns = As + V * WA;
+  T *As = reinterpret_cast<T *>(smem_raw);  // [WA][SV]
+  T *Ns = As + SV * WA;                     // [WN][SV]
   const int64_t ntiles = (n + V - 1) / V;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t v0 = tile * V;
     const int nv = (int)min((int64_t)V, n - v0);
     for (int i = threadIdx.x; i < V * WA; i += blockDim.x) {
       const int r = i / WA, x = i - r * WA;
-      As[i] = r < nv ? A[(v0 + r) * ldA + x] : (T)0;
+      As[x * SV + r] = r < nv ? A[(v0 + r) * ldA + x] : (T)0;
     }
     for (int i = threadIdx.x; i < V * WN; i += blockDim.x) {
       const int r = i / WN, y = i - r * WN;
-      Ns[i] = r < nv ? N[(v0 + r) * ldN + y] : (T)0;
+      Ns[y * SV + r] = r < nv ? N[(v0 + r) * ldN + y] : (T)0;
     }
     __syncthreads();
     for (int s = threadIdx.x; s < WO; s += blockDim.x) {
-      double acc[V];
+      T acc[V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] = 0.0;
+      for (int i = 0; i < V; ++i) acc[i] = (T)0;
       for (int q = 0; q < nq; ++q) {
-        const uint32_t sp = __ldg(split + (int64_t)q * WO + s);
-        const int x = sp & 0xFFFF, y = sp >> 16;
+        const uint32_t sp = __ldg(split + (int64_t)q * ((WO + 7) & ~7) + s);
+        const VT *ax = reinterpret_cast<const VT *>(As + (sp & 0xFFFF) * SV);
+        const VT *ny = reinterpret_cast<const VT *>(Ns + (sp >> 16) * SV);
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] += (double)As[i * WA + x] * (double)Ns[i * WN + y];
+        for (int i = 0; i < V / VW; ++i) {
+          const VT av = ax[i], nv4 = ny[i];
+          if constexpr (VW == 4) {
+            acc[4 * i + 0] = fmaf(av.x, nv4.x, acc[4 * i + 0]);
+            acc[4 * i + 1] = fmaf(av.y, nv4.y, acc[4 * i + 1]);
+            acc[4 * i + 2] = fmaf(av.z, nv4.z, acc[4 * i + 2]);
+            acc[4 * i + 3] = fmaf(av.w, nv4.w, acc[4 * i + 3]);
+          } else {
+            acc[2 * i + 0] = fma(av.x, nv4.x, acc[2 * i + 0]);
+            acc[2 * i + 1] = fma(av.y, nv4.y, acc[2 * i + 1]);
+          }
+        }
       }
 #pragma unroll
       for (int i = 0; i < V; ++i)
-        if (i < nv) out[(v0 + i) * ldO + s] = (T)acc[i];
+        if (i < nv) out[(v0 + i) * ldO + s] = acc[i];
     }
+    __syncthreads();
+  }
+}
+
+// Lane-per-vertex combine: a CTA stages 32 vertices' A' / N'' rows in shared
+// memory as [column][33] (stride 33: conflict-free both for the transposing
+// stores and for the lane-indexed loads); each warp takes output columns s,
+// reads the split (x, y) warp-uniformly from L1 and every lane accumulates
+// its own vertex: 2 conflict-free LDS per FMA.  Outputs are staged in shared
+// memory and written back as whole rows.
+template <typename T>
+__global__ void __launch_bounds__(256) k_combine_lane(const T *__restrict__ A, int64_t ldA, int WA,
+                                                      const T *__restrict__ N, int64_t ldN, int WN,
+                                                      const uint32_t *__restrict__ split, int nq, int64_t n,
+                                                      T *__restrict__ out, int64_t ldO, int WO) {
+  constexpr int S = 33;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *As = reinterpret_cast<T *>(smem_raw);  // [WA][33]
+  T *Ns = As + S * WA;                      // [WN][33]
+  T *Os = Ns + S * WN;                      // [WO][33]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int64_t ntiles = (n + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t v0 = tile * 32;
+    const int nv = (int)min((int64_t)32, n - v0);
+    for (int r = warp; r < 32; r += nwarp) {  // a warp stages whole rows (coalesced reads)
+      const bool ok = r < nv;
+      for (int x = lane; x < WA; x += 32) As[x * S + r] = ok ? A[(v0 + r) * ldA + x] : (T)0;
+      for (int y = lane; y < WN; y += 32) Ns[y * S + r] = ok ? N[(v0 + r) * ldN + y] : (T)0;
+    }
+    __syncthreads();
+    // 8 outputs per warp pass: two warp-uniform 16-byte split loads per q feed
+    // 8 independent FMA chains (the split table rows are padded to 8 entries)
+    const int WOp = (WO + 7) & ~7;
+    for (int g = warp; g < WOp / 8; g += nwarp) {
+      T acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = (T)0;
+      const uint4 *sp = reinterpret_cast<const uint4 *>(split) + 2 * g;
+      for (int q = 0; q < nq; ++q) {
+        const uint4 e0 = __ldg(sp + (int64_t)q * (WOp / 4)), e1 = __ldg(sp + (int64_t)q * (WOp / 4) + 1);
+        const uint32_t xy[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fma(As[(xy[j] & 0xFFFF) * S + lane], Ns[(xy[j] >> 16) * S + lane], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (8 * g + j < WO) Os[(8 * g + j) * S + lane] = acc[j];
+    }
+    __syncthreads();
+    for (int r = warp; r < nv; r += nwarp)
+      for (int s = lane; s < WO; s += 32) out[(v0 + r) * ldO + s] = Os[s * S + r];
     __syncthreads();
   }
 }
@@ -141,23 +212,36 @@ template <typename T, int V>
 void combine_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
                 int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
   auto kern = k_combine<T, V>;
-  const size_t smem = (size_t)V * (WA + WN) * sizeof(T);
+  const size_t smem = (size_t)(V == Vec<T>::W ? V : V + Vec<T>::W) * (WA + WN) * sizeof(T);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, 256, smem, num_sms);
-  kern<<<grid, 256, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq, n,
-                               static_cast<T *>(out), ldO, WO);
+  const int threads = std::min(256, (WO + 31) / 32 * 32);  // one thread per output column
+  const int grid = persistent_grid(kern, threads, smem, num_sms);
+  kern<<<grid, threads, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq,
+                                   n, static_cast<T *>(out), ldO, WO);
 }
 
 template <typename T>
 void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
                    int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
+  const char *impl = getenv("CC_COMBINE_IMPL");  // "lane": lane-per-vertex kernel (default: V-tile, measured faster)
+  const size_t lane_smem = (size_t)(WA + WN + WO) * 33 * sizeof(T);
+  if (lane_smem <= 200 * 1024 && impl && impl[0] == 'l') {
+    auto kern = k_combine_lane<T>;
+    if (lane_smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lane_smem);
+    const int grid = persistent_grid(kern, 256, lane_smem, num_sms);
+    kern<<<grid, 256, lane_smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split,
+                                      nq, n, static_cast<T *>(out), ldO, WO);
+    return;
+  }
+  // wide rows: tile of V vertices (padded rows); k <= 16 bounds a row by
+  // 2 x C(15,7) entries, so the smallest tile always fits in 227 KB
   const size_t row = (size_t)(WA + WN) * sizeof(T);
   const size_t budget = 100 * 1024;
-  if (row * 16 <= budget) combine_go<T, 16>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  else if (row * 8 <= budget) combine_go<T, 8>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  else if (row * 4 <= budget) combine_go<T, 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  else if (row * 2 <= budget) combine_go<T, 2>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  else combine_go<T, 1>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  if (row * 20 <= budget) combine_go<T, 16>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  else if (row * 12 <= budget) combine_go<T, 8>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  else if (sizeof(T) == 4 || row * 6 <= 220 * 1024)
+    combine_go<T, 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  else combine_go<T, sizeof(T) == 8 ? 2 : 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
 }
 
 }  // namespace

@@ -43,6 +43,7 @@ struct GatherArgs {
   int W_in;
   const uint16_t *map;    // [c_u][c_v][map_ld] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
   int64_t map_ld;         // map row stride (multiple of 8 entries, padding = 0xFFFF)
+  int64_t hub_rows;       // rows [0, hub_rows) of src are gathered with an L2 evict-last policy
   void *dst;              // N'' (rows x ld_dst), W_out = C(k-1, p)
   int64_t ld_dst;
   int W_out;

@@ -82,11 +82,106 @@ int64_t factorial(int m) {
 
 }  // namespace
 
-Plan make_plan(int k, const int32_t *parent) {
-  Tree T = load_tree(k, parent);
+// The same tree rooted at w; children ordered by `order` (0 = vertex index,
+// 1 = subtree size ascending, 2 = subtree size descending; ties by index).
+Tree reroot(const Tree &T0, int w, int order) {
+  const int k = T0.k;
+  std::vector<std::vector<int>> adj(k);
+  for (int i = 0; i < k; ++i)
+    if (T0.parent[i] >= 0) {
+      adj[i].push_back(T0.parent[i]);
+      adj[T0.parent[i]].push_back(i);
+    }
+  Tree T;
+  T.k = k;
+  T.root = w;
+  T.parent.assign(k, -1);
+  T.child.assign(k, {});
+  std::vector<int> queue{w}, seen(k, 0);
+  seen[w] = 1;
+  for (size_t h = 0; h < queue.size(); ++h) {
+    const int x = queue[h];
+    std::vector<int> nb = adj[x];
+    std::sort(nb.begin(), nb.end());
+    for (int y : nb)
+      if (!seen[y]) {
+        seen[y] = 1;
+        T.parent[y] = x;
+        T.child[x].push_back(y);
+        queue.push_back(y);
+      }
+  }
+  T.size.assign(k, 1);
+  for (int h = (int)queue.size() - 1; h > 0; --h) T.size[T.parent[queue[h]]] += T.size[queue[h]];
+  if (order)
+    for (int x = 0; x < k; ++x)
+      std::stable_sort(T.child[x].begin(), T.child[x].end(), [&](int a, int b) {
+        return order == 1 ? T.size[a] < T.size[b] : T.size[a] > T.size[b];
+      });
+  return T;
+}
+
+Plan plan_rooted(const Tree &T);
+
+// Model cost of one colouring of a plan (bytes-equivalent, compressed layout):
+// each distinct passive of size p >= 2 gathers (k-1)/k x C(k-1, p-1) entries
+// per adjacency entry (+ 4 B index) and writes C(k-1, p) per vertex; the
+// colour histogram reads 5 B per adjacency entry; each combine reads and
+// writes its rows and performs C(k-1,t-1) C(t-1,a-1) FMAs (weighted as
+// `fma_bytes` bytes each).
+double plan_cost(const Plan &P, const PlanOpts &o) {
+  const int k = P.k;
+  const double e = o.elem, d = o.avg_degree;
+  double c = 0;
+  bool hist = false;
+  std::vector<char> seen(P.tables.size(), 0);
+  for (const Step &st : P.steps) {
+    if (st.p == 1) {
+      hist = true;
+    } else if (!seen[st.passive]) {
+      seen[st.passive] = 1;
+      c += d * (4.0 + (double)(k - 1) / k * binom(k - 1, st.p - 1) * e) + binom(k - 1, st.p) * e;
+    }
+    if (st.a > 1) {
+      const double rows = binom(k - 1, st.a - 1) + (st.out >= 0 ? binom(k - 1, st.p) + binom(k - 1, st.t - 1) : 1);
+      c += rows * e + (st.out >= 0 ? binom(k - 1, st.t - 1) * (double)binom(st.t - 1, st.a - 1) : binom(k - 1, st.a - 1)) *
+                           o.fma_bytes;
+    }
+  }
+  if (hist) c += d * 5.0;
+  return c;
+}
+
+Plan make_plan(int k, const int32_t *parent, const PlanOpts *opts) {
+  Tree T0 = load_tree(k, parent);
+  Plan base = plan_rooted(T0);
+  if (!opts || !opts->auto_root || k <= 2) return base;
+  Plan best = base;
+  double best_cost = plan_cost(base, *opts);
+  for (int w = 0; w < k; ++w)
+    for (int order = 0; order < 3; ++order) {
+      Plan p = plan_rooted(reroot(T0, w, order));
+      const double c = plan_cost(p, *opts);
+      if (c < best_cost * (1.0 - 1e-9)) {
+        best = std::move(p);
+        best_cost = c;
+      }
+    }
+  // |Aut|, |Aut_rho| and the Table-3 quantities refer to the user's rooting
+  best.aut = base.aut;
+  best.aut_root = base.aut_root;
+  best.memory = base.memory;
+  best.computation = base.computation;
+  best.user_root = base.root;
+  return best;
+}
+
+Plan plan_rooted(const Tree &T) {
+  const int k = T.k;
   Plan P;
   P.k = k;
   P.root = T.root;
+  P.user_root = T.root;
   P.parent = T.parent;
 
   // full-subtree codes in the template's own rooting

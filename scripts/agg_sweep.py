@@ -22,6 +22,7 @@ ap.add_argument("--segs", default="4096")
 ap.add_argument("--precision", default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--check", action="store_true", help="compare every variant's count with the first")
+ap.add_argument("--fixed-root", default="0")
 args = ap.parse_args()
 
 knobs = []
@@ -35,8 +36,9 @@ t = time.time()
 g = cfg.graph()
 print(f"graph {cfg.name}: n={g.n} 2m={g.nnz} gen {time.time() - t:.1f}s", flush=True)
 prec = args.precision or cfg.precision
-for seg in map(int, args.segs.split(",")):
-    ctx = cc.cc_create(device=0, precision=cc.CC_FP32 if prec == "fp32" else cc.CC_FP64, segment_len=seg)
+for seg, fr in itertools.product(map(int, args.segs.split(",")), map(int, args.fixed_root.split(","))):
+    ctx = cc.cc_create(device=0, precision=cc.CC_FP32 if prec == "fp32" else cc.CC_FP64, segment_len=seg,
+                       fixed_root=fr)
     t = time.time()
     cc.cc_load_graph(ctx, g.n, g.row_ptr, g.col)
     cc.cc_set_template(ctx, cfg.parent)
@@ -58,7 +60,7 @@ for seg in map(int, args.segs.split(",")):
         st = cc.cc_last_stats(ctx)
         if ref is None:
             ref = xs
-        rec = {"env": dict(combo), "seg": seg, "load_s": round(load_s, 1),
+        rec = {"env": dict(combo), "seg": seg, "fixed_root": fr, "load_s": round(load_s, 1),
                "gather_GBs": round(st["agg_bytes"] / best["gather"] / 1e6, 1),
                "same_as_first": xs == ref,
                **{k: round(v, 3) for k, v in best.items()}}
