@@ -139,9 +139,10 @@ def cc_last_profile(ctx) -> dict:
 
 
 def cc_last_stats(ctx) -> dict:
-    buf = np.zeros(5, dtype=np.float64)
-    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 5))
-    return dict(updates=buf[0], model_bytes=buf[1], agg_bytes=buf[2], launches=buf[3], peak_table_bytes=buf[4])
+    buf = np.zeros(6, dtype=np.float64)
+    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 6))
+    return dict(updates=buf[0], model_bytes=buf[1], agg_bytes=buf[2], launches=buf[3], peak_table_bytes=buf[4],
+                fused_root=int(buf[5]))
 
 
 # ------------------------------------------------------------------ host-only

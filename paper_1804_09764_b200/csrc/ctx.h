@@ -40,6 +40,7 @@ struct Pass {
   int64_t nnz = 0;             // adjacency entries covered
   const int64_t *beg = nullptr, *end = nullptr;  // device
   uint16_t *goff = nullptr;    // n_items x 16 colour-group ends (per colouring)
+  dev::ItemDesc *desc = nullptr;  // n_items descriptors (per colouring)
   int64_t items() const { return n_seg + n_light; }
   dev::AggWork view() const {
     dev::AggWork w;
@@ -106,7 +107,7 @@ struct cc_ctx {
 
   // profile / stats of the last count
   double prof[cc::PH_N + 1] = {0};
-  double stats[5] = {0};
+  double stats[6] = {0};
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;

@@ -38,6 +38,19 @@ __device__ __forceinline__ void add_vec(double *acc, const double2 &v) {
   acc[1] += v.y;
 }
 
+__device__ __forceinline__ void add_same(float4 &a, const float4 &b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+__device__ __forceinline__ void add_same(double2 &a, const double2 &b) {
+  a.x += b.x;
+  a.y += b.y;
+}
+__device__ __forceinline__ float vec_at(const float4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+__device__ __forceinline__ double vec_at(const double2 &v, int i) { return i == 0 ? v.x : v.y; }
+
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // SplitMix64 finaliser (reading C-2)
   uint64_t z = x + 0x9E3779B97F4A7C15ULL;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;

@@ -58,6 +58,7 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
   w.seg_b = c->pupload(seg_b);
   w.seg_e = c->pupload(seg_e);
   w.goff = c->pmalloc<uint16_t>((size_t)std::max<int64_t>(w.items(), 1) * 16);
+  w.desc = c->pmalloc<dev::ItemDesc>((size_t)std::max<int64_t>(w.items(), 1));
   c->max_hv = std::max(c->max_hv, w.n_hv);
   c->max_seg = std::max(c->max_seg, w.n_seg);
 }
@@ -169,13 +170,23 @@ namespace {
 
 void csort(cc_ctx *c, Pass &p) {
   c->stats[3] += dev::launch_csort(p.beg, p.end, c->d_col, c->d_colors, p.view(), c->d_col_sorted, p.goff,
-                                   c->num_sms, c->s_main);
+                                   p.desc, c->num_sms, c->s_main);
   c->check_launch();
-  c->stats[1] += (double)p.nnz * 14.0 + (double)p.items() * 32.0;
+  c->stats[1] += (double)p.nnz * 14.0 + (double)p.items() * 64.0;
 }
 
+// Fused root: the root step's neighbour sum is consumed in the gather's
+// epilogue (X_v into per_vertex) instead of being written to HBM.
+struct RootFuse {
+  int mode = 0;  // 1: A' = table A; 2: A' = the neighbour sum itself
+  const void *A = nullptr;
+  int64_t ldA = 0;
+  int WA = 0;
+  double *per_vertex = nullptr;
+};
+
 // N'' = neighbour sum of the passive table P' (size p >= 2) over one pass.
-void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate) {
+void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, const RootFuse *rf = nullptr) {
   const int k = c->plan.k, elem = c->elem();
   const int W_in = (int)binom(k - 1, p - 1), W_out = (int)binom(k - 1, p);
   dev::GatherArgs a;
@@ -183,6 +194,7 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate) {
   a.end = w.end;
   a.col = c->d_col_sorted;
   a.goff = w.goff;
+  a.desc = w.desc;
   a.colors = c->d_colors;
   a.src = P;
   a.ld_src = c->ld_of(W_in);
@@ -209,6 +221,14 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate) {
   }
   a.scratch = static_cast<double *>(scratch);
   a.arrive = c->d_arrive;
+  if (rf) {
+    a.root_mode = rf->mode;
+    a.rA = rf->A;
+    a.ldA = rf->ldA;
+    a.WA = rf->WA;
+    a.comp = c->d_comp;
+    a.per_vertex = rf->per_vertex;
+  }
   cudaEvent_t b = c->begin(c->s_main);
   c->stats[3] += dev::launch_gather(elem, a, c->num_sms, c->s_main);
   c->check_launch();
@@ -218,7 +238,9 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate) {
   // colour differs from the row vertex's (expected fraction (k-1)/k) + N'' rows
   // written (+ read when accumulating)
   const double rows = (double)w.nnz * (double)(k - 1) / k * W_in * elem;
-  const double bytes = (double)w.nnz * 4.0 + rows + (double)(w.n_light + w.n_hv) * W_out * elem * (1 + accumulate);
+  const double out_bytes = rf ? (double)(w.n_light + w.n_hv) * (8.0 + (rf->mode == 1 ? (double)rf->WA * elem : 0.0))
+                              : (double)(w.n_light + w.n_hv) * W_out * elem * (1 + accumulate);
+  const double bytes = (double)w.nnz * 4.0 + rows + out_bytes;
   c->stats[0] += (double)w.nnz * (double)binom(k, p);  // U: dense edge x colour-set updates
   c->stats[1] += bytes;
   c->stats[2] += bytes;
@@ -272,7 +294,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
 void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out) {
   const Plan &pl = c->plan;
   const int k = pl.k, elem = c->elem();
-  std::fill(c->stats, c->stats + 5, 0.0);
+  std::fill(c->stats, c->stats + 6, 0.0);
   c->ev_used = 0;
   c->ev_log.clear();
   c->cur_bytes = c->peak_bytes = 0;
@@ -298,6 +320,36 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     c->sorted_valid = true;
   }
 
+  // Fused root (world 1): when the root step's neighbour sum N''(P) is needed
+  // by no other step, the root is evaluated in the gather's epilogue and
+  // N''(P) never reaches HBM.  Mode 2: the root's active part is the lift of
+  // the same passive (T_active = N''(P), e.g. two identical subtrees under
+  // the root), so the lift is deferred to the root as well.
+  const int sr = (int)pl.steps.size() - 1;
+  int fuse = 0, defer_lift = -1;
+  std::vector<int> last_use(pl.table_last_use);
+  {
+    const Step &rs = pl.steps[sr];
+    const char *f = getenv("CC_FUSED_ROOT");
+    if (c->opt.world == 1 && dump_table < 0 && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
+      const int P = rs.passive;
+      int s_l = -1, users = 0;
+      for (int s = 0; s < sr; ++s) {
+        if (pl.steps[s].out == rs.active) s_l = s;
+        if (pl.steps[s].passive == P) ++users;
+      }
+      if (rs.a > 1 && s_l >= 0 && pl.steps[s_l].a == 1 && pl.steps[s_l].passive == P && users == 1 &&
+          pl.table_last_use[rs.active] == sr) {
+        fuse = 2;
+        defer_lift = s_l;
+        last_use[P] = sr;
+      } else if (users == 0 && rs.a > 1) {
+        fuse = 1;
+      }
+    }
+  }
+
+  c->stats[5] = fuse;
   Bufs bufs(c);
   const int nt = (int)pl.tables.size();
   std::vector<int> T(nt, -1), Nb(nt, -1);
@@ -306,11 +358,28 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   for (int s = 0; s < (int)pl.steps.size(); ++s)
     if (pl.steps[s].p == 1) last_hist_use = s;
   double *per_vertex = nullptr;
-  if (root_out) per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
+  if (root_out || fuse) per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
 
   for (int s = 0; s < (int)pl.steps.size(); ++s) {
     const Step &st = pl.steps[s];
     const int Wa = (int)binom(k - 1, st.a - 1), Wp = (int)binom(k - 1, st.p), Wt = (int)binom(k - 1, st.t - 1);
+    if (s == defer_lift) continue;  // T_out = N''(P) is evaluated inside the fused root
+    if (s == sr && fuse) {
+      cc::RootFuse rf;
+      rf.mode = fuse;
+      rf.A = fuse == 1 ? bufs.ptr(T[st.active]) : nullptr;
+      rf.ldA = c->ld_of(Wa);
+      rf.WA = Wa;
+      rf.per_vertex = per_vertex;
+      gather_pass(c, c->p_full, bufs.ptr(T[st.passive]), st.p, nullptr, 0, &rf);
+      cudaEvent_t b = c->begin(c->s_main);
+      c->stats[3] += dev::launch_root(8, nullptr, 0, 0, per_vertex, 1, nullptr, n, c->d_partials, c->n_partials,
+                                      nullptr, c->d_result, c->s_main);
+      c->check_launch();
+      c->end(PH_ROOT, c->s_main, b);
+      c->stats[1] += (double)n * 8.0;
+      break;
+    }
     int nbuf;  // buffer of N''
     if (st.p == 1) {
       if (hist < 0) {
@@ -357,7 +426,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     }
     if (dump_table < 0) {  // release dead tables / neighbour sums
       for (int id = 0; id < nt; ++id) {
-        if (T[id] >= 0 && pl.table_last_use[id] == s) {
+        if (T[id] >= 0 && last_use[id] == s) {
           bufs.unref(T[id]);
           T[id] = -1;
         }

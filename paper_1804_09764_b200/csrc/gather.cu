@@ -15,8 +15,10 @@
 //                  Heavy neighbour lists are split into segments (Alg. 4,
 //                  PAPER.md lines 494-523) whose partial rows the last
 //                  arriving segment sums in segment order (deterministic).
-//   k_gather       the same computation with plain register loads (kept as
-//                  the comparison variant, CC_GATHER_IMPL=reg).
+//   k_gather_ldg   the same sum for rows of > 8 vectors: one warp per item,
+//                  plain LDG.128 rows, U rows in flight, ~20 instructions per
+//                  row (the ring's per-row bookkeeping made it issue-bound);
+//                  optionally evaluates the root step in its epilogue.
 #include <algorithm>
 #include <cstdlib>
 
@@ -27,13 +29,18 @@ namespace dev {
 
 namespace {
 
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // ------------------------------------------------------------------ colour sort
 // One warp per item.  Pass 1 counts colours; pass 2 places each neighbour at
 // base[colour] + (rank among equal colours in this 32-wide window): stable.
 __global__ void __launch_bounds__(256) k_csort(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
                                                const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
                                                AggWork work, int32_t *__restrict__ col_out,
-                                               uint16_t *__restrict__ goff) {
+                                               uint16_t *__restrict__ goff, ItemDesc *__restrict__ desc) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
@@ -41,7 +48,8 @@ __global__ void __launch_bounds__(256) k_csort(const int64_t *__restrict__ beg, 
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; it < n_items; it += nwarps) {
     int32_t v;
     int64_t b, e;
-    item_range(work, beg, end, it, v, b, e);
+    const bool heavy = item_range(work, beg, end, it, v, b, e);
+    const int cv = colors[v];
     int cnt[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) cnt[j] = 0;
@@ -51,14 +59,29 @@ __global__ void __launch_bounds__(256) k_csort(const int64_t *__restrict__ beg, 
       for (int j = 0; j < 16; ++j) cnt[j] += (c == j);
     }
     int base[16];
-    int run = 0;
+    int run = 0, cv_lo = 0, skip = 0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
       base[j] = run;
+      if (j == cv) {
+        cv_lo = run;
+        skip = cnt[j];
+      }
       run += cnt[j];
       if (lane == j) goff[it * 16 + j] = (uint16_t)run;
+    }
+    if (lane == 0) {
+      ItemDesc d;
+      d.b = b;
+      d.v = v;
+      d.n_s = (int32_t)(e - b) - skip;
+      d.cv_lo = cv_lo;
+      d.skip = skip;
+      d.cv = cv;
+      d.heavy = heavy ? 1 : 0;
+      desc[it] = d;
     }
     for (int64_t p0 = b; p0 < e; p0 += 32) {
       const bool ok = p0 + lane < e;
@@ -153,6 +176,43 @@ __device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const doubl
       drow[j] = (T)x;
     }
   }
+}
+
+// Fused root epilogue (root_mode 1 / 2): X_v = sum_{X'} A'(v, X') N''(v, comp X')
+// in fp64, written to per_vertex[v]; a heavy vertex's segments are first
+// summed (in segment order) by the last arriving segment.
+template <typename T>
+__device__ __forceinline__ void root_epilogue(const GatherArgs &a, double *sacc, int64_t it, int32_t v, bool heavy,
+                                              int lane) {
+  if (heavy) {
+    double *sp = a.scratch + it * a.ld_scratch;
+    for (int j = lane; j < a.W_out; j += 32) sp[j] = sacc[j];
+    __threadfence();
+    __syncwarp();
+    const int32_t hv = a.work.seg_hv[it];
+    unsigned prev = 0;
+    if (lane == 0) prev = atomicAdd(&a.arrive[hv], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != (unsigned)(a.work.hv_nseg[hv] - 1)) return;
+    __threadfence();
+    const int32_t s0 = a.work.hv_first[hv], ns = a.work.hv_nseg[hv];
+    for (int j = lane; j < a.W_out; j += 32) {
+      double x = 0.0;
+      for (int s = 0; s < ns; ++s) x += __ldcg(a.scratch + (int64_t)(s0 + s) * a.ld_scratch + j);
+      sacc[j] = x;
+    }
+    __syncwarp();
+  }
+  double d = 0.0;
+  if (a.root_mode == 2) {
+    for (int x = lane; x < a.WA; x += 32) d += sacc[x] * sacc[__ldg(a.comp + x)];
+  } else {
+    const T *ar = static_cast<const T *>(a.rA) + (int64_t)v * a.ldA;
+    for (int x = lane; x < a.WA; x += 32) d += (double)ar[x] * sacc[__ldg(a.comp + x)];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  if (lane == 0) a.per_vertex[v] = d;
 }
 
 // expand one colour group's column sums into N'' (map injective per colour pair)
@@ -340,72 +400,167 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
   }
 }
 
-// ------------------------------------------------------------------ gather, register rounds
-template <typename T, int G, int NV, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_gather(GatherArgs a, int nch) {
+// ------------------------------------------------------------------ gather, lean register rows
+// One warp per item; lane l owns the 16-byte column vectors l, l+32, ... of
+// the pass.  The item's colour groups are contiguous in the colour-sorted
+// neighbour list (goff), so a group's rows are read from positions
+// [b + lo_g, b + hi_g) directly: 32 neighbour ids per coalesced load, then U
+// rows in flight per lane (U x NV independent LDG.128), summed in the storage
+// type over chunks of <= 32 rows and expanded into the fp64 N'' row in shared
+// memory through the colour-pair map (held in registers for the group).  The
+// next item's descriptor and group ends are loaded while the current item
+// runs.  Per row: one SHFL, one address, NV loads and 4 NV (fp32) adds.
+__device__ __forceinline__ void load_desc(const GatherArgs &a, int64_t it, int lane, int4 &x, int4 &y, int &go) {
+  const int4 *d = reinterpret_cast<const int4 *>(a.desc + it);
+  x = __ldg(d);
+  y = __ldg(d + 1);
+  go = lane < 16 ? (int)__ldg(a.goff + it * 16 + lane) : 0;
+}
+
+template <typename T, int NV, int U>
+__global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
-  constexpr int CAP = G * NV * VW;
-  extern __shared__ double sacc_all[];
-  const int lane = threadIdx.x & (G - 1);
-  const unsigned gmask = group_mask<G>();
-  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
+  constexpr int CAP = 32 * NV * VW;  // columns per pass
+  extern __shared__ double sacc_ldg[];
+  const int lane = threadIdx.x & 31;
+  double *sacc = sacc_ldg + (threadIdx.x >> 5) * (int64_t)a.W_out;
   const int64_t n_items = a.work.n_seg + a.work.n_light;
-  double *sacc = sacc_all + (threadIdx.x / G) * (int64_t)a.W_out;
-  const T *__restrict__ src = static_cast<const T *>(a.src);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const char *__restrict__ srcb = static_cast<const char *>(a.src);
+  const uint32_t ld_bytes = (uint32_t)(a.ld_src * sizeof(T));
+  // (L2 evict-last hints for hub rows measured neutral here: plain loads)
 
-  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
-    int32_t v;
-    int64_t b, e;
-    const bool heavy = item_range(a.work, a.beg, a.end, it, v, b, e);
-    const int cv = a.colors[v];
-    for (int j = lane; j < a.W_out; j += G) sacc[j] = 0.0;
-    __syncwarp(gmask);
-    const uint16_t *go = a.goff + it * 16;
-    int gstart = 0;
-    for (int cu = 0; cu < a.k; ++cu) {
-      const int gend = go[cu];
-      if (cu != cv && gend > gstart) {
-        for (int ch = 0; ch < nch; ++ch) {
-          const int c0 = ch * CAP + lane * VW;
-          bool valid[NV];
+  int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int4 dx = make_int4(0, 0, 0, 0), dy = make_int4(0, 0, 0, 0);
+  int go_n = 0;
+  if (it < n_items) load_desc(a, it, lane, dx, dy, go_n);
+  for (; it < n_items; it += nw) {
+    const int64_t b = (int64_t)(((uint64_t)(uint32_t)dx.y << 32) | (uint32_t)dx.x);
+    const int32_t v = dx.z;
+    const int cv = dy.z;
+    const bool heavy = dy.w != 0;
+    const int hi_l = go_n;
+    const int lo_l = __shfl_up_sync(0xffffffffu, hi_l, 1);
+    // non-empty colour groups other than v's own
+    unsigned gm = __ballot_sync(0xffffffffu, lane < a.k && lane != cv && hi_l > (lane == 0 ? 0 : lo_l));
+    if (it + nw < n_items) load_desc(a, it + nw, lane, dx, dy, go_n);  // prefetch the next item
+    for (int j = lane; j < a.W_out; j += 32) sacc[j] = 0.0;
+    __syncwarp();
+    for (int ch = 0; ch < nch; ++ch) {
+      const int c0 = ch * CAP + lane * VW;
+      // byte offsets of the lane's vectors in a row; lanes past the row end
+      // re-read vector 0 of the pass (same sector as lane 0: no extra
+      // traffic) and their sums are dropped by the map (0xFFFF)
+      bool valid[NV];
 #pragma unroll
-          for (int j = 0; j < NV; ++j) valid[j] = c0 + j * G * VW < a.W_in;
-          double acc[NV][VW];
+      for (int j = 0; j < NV; ++j) valid[j] = c0 + j * 32 * VW < a.W_in;
+      // lane base: its first vector of the pass (lanes past the row end of
+      // slot j skip that load; their sums are dropped by the map, 0xFFFF)
+      const char *lbase = srcb + (size_t)c0 * sizeof(T);
+      for (unsigned g = gm; g; g &= g - 1) {
+        const int cu = __ffs(g) - 1;
+        const int lo = cu == 0 ? 0 : __shfl_sync(0xffffffffu, hi_l, cu - 1);
+        const int hi = __shfl_sync(0xffffffffu, hi_l, cu);
+        // colour-pair map of this group, for the lane's columns
+        uint16_t m[NV][VW];
+        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
 #pragma unroll
-          for (int j = 0; j < NV; ++j)
-#pragma unroll
-            for (int q = 0; q < VW; ++q) acc[j][q] = 0.0;
-          for (int64_t e0 = b + gstart; e0 < b + gend; e0 += G) {
-            const int cnt = (int)min((int64_t)G, b + gend - e0);
-            const int32_t my_u = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
-            for (int j0 = 0; j0 < cnt; j0 += U) {
-              V vals[U][NV];
-#pragma unroll
-              for (int uu = 0; uu < U; ++uu) {
-                const int32_t u = __shfl_sync(gmask, my_u, (j0 + uu) & (G - 1), G);
-                const T *row = src + (int64_t)u * a.ld_src + c0;
-#pragma unroll
-                for (int j = 0; j < NV; ++j) {
-                  if (j0 + uu < cnt && valid[j]) vals[uu][j] = ldg_vec(row + j * G * VW);
-                  else zero_vec(vals[uu][j]);
-                }
-              }
-#pragma unroll
-              for (int uu = 0; uu < U; ++uu)
-#pragma unroll
-                for (int j = 0; j < NV; ++j) add_vec(acc[j], vals[uu][j]);
+        for (int j = 0; j < NV; ++j) {
+          if (valid[j]) {
+            if constexpr (VW == 4) {
+              const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + c0 + j * 32 * VW));
+              m[j][0] = w.x & 0xFFFF;
+              m[j][1 % VW] = w.x >> 16;
+              m[j][2 % VW] = w.y & 0xFFFF;
+              m[j][3 % VW] = w.y >> 16;
+            } else {
+              const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + c0 + j * 32 * VW));
+              m[j][0] = w & 0xFFFF;
+              m[j][1 % VW] = w >> 16;
             }
+          } else {
+#pragma unroll
+            for (int q = 0; q < VW; ++q) m[j][q] = 0xFFFF;
           }
-          expand<NV, VW, G>(a, cu, cv, c0, acc, sacc);
         }
-        __syncwarp(gmask);
+        int32_t u_next = lane < hi - lo ? __ldg(a.col + b + lo + lane) : 0;
+        for (int p = lo; p < hi; p += 32) {
+          const int cnt = min(32, hi - p);
+          const int32_t my_u = u_next;
+          if (p + 32 < hi) u_next = p + 32 + lane < hi ? __ldg(a.col + b + p + 32 + lane) : 0;  // next chunk's ids
+          V blk[NV];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) zero_vec(blk[j]);
+          int r = 0;
+          V x[U][NV];
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+            for (int j = 0; j < NV; ++j) zero_vec(x[uu][j]);
+          for (; r + U <= cnt; r += U) {  // full blocks of U rows: no row predicates
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+              const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, r + uu);
+              const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
+#pragma unroll
+              for (int j = 0; j < NV; ++j)
+                if (valid[j]) x[uu][j] = __ldg(row + 32 * j);
+            }
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+              for (int j = 0; j < NV; ++j) add_same(blk[j], x[uu][j]);
+          }
+          if (r < cnt) {  // tail
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+              const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, (r + uu) & 31);
+              const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
+#pragma unroll
+              for (int j = 0; j < NV; ++j) {
+                if (r + uu < cnt && valid[j]) x[uu][j] = __ldg(row + 32 * j);
+                else zero_vec(x[uu][j]);
+              }
+            }
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+              for (int j = 0; j < NV; ++j) add_same(blk[j], x[uu][j]);
+          }
+          // fp32: a block of <= 32 rows summed in fp32, then in fp64 (C-6)
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            const double e[4] = {(double)vec_at(blk[j], 0), (double)vec_at(blk[j], 1), (double)vec_at(blk[j], 2 % VW),
+                                 (double)vec_at(blk[j], 3 % VW)};
+#pragma unroll
+            for (int q = 0; q < VW; ++q)
+              if (m[j][q] != 0xFFFF) sacc[m[j][q]] += e[q];
+          }
+        }
+        __syncwarp();  // groups of different colours may map to the same N'' entries
       }
-      gstart = gend;
     }
-    gather_epilogue<T, G>(a, sacc, it, v, heavy, lane, gmask);
-    __syncwarp(gmask);
+    if (a.root_mode) root_epilogue<T>(a, sacc, it, v, heavy, lane);
+    else gather_epilogue<T, 32>(a, sacc, it, v, heavy, lane, 0xffffffffu);
+    __syncwarp();
   }
+}
+
+template <typename T, int NV, int U>
+void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = 32 * NV * VW;
+  auto kern = k_gather_ldg<T, NV, U>;
+  const size_t row = (size_t)a.W_out * sizeof(double);
+  int warps = 8;
+  while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
+  const int threads = warps * 32;
+  const size_t smem = row * warps;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, threads, smem, num_sms);
+  const int nch = (a.W_in + CAP - 1) / CAP;
+  kern<<<grid, threads, smem, s>>>(a, nch);
 }
 
 // ------------------------------------------------------------------ launchers
@@ -425,37 +580,30 @@ void ring_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   kern<<<grid, threads, smem, s>>>(a, nch);
 }
 
-template <typename T, int G, int NV, int U, int MINB = 1>
-void reg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
-  constexpr int VW = Vec<T>::W;
-  constexpr int CAP = G * NV * VW;
-  auto kern = k_gather<T, G, NV, U, MINB>;
-  const size_t row = (size_t)a.W_out * sizeof(double);
-  int groups = 256 / G;
-  while (groups > 1 && row * groups > 96 * 1024) groups /= 2;
-  const int threads = groups * G;
-  const size_t smem = row * groups;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, threads, smem, num_sms);
-  const int nch = (a.W_in + CAP - 1) / CAP;
-  kern<<<grid, threads, smem, s>>>(a, nch);
-}
-
-int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
 template <typename T>
 void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   const int wvec = (a.W_in + VW - 1) / VW;
-  const char *impl = getenv("CC_GATHER_IMPL");  // "reg": register rounds; default: cp.async ring
-  if (impl && impl[0] == 'r' && impl[1] == 'e') {
-    if (wvec <= 4) reg_go<T, 4, 1, 4, 3>(a, num_sms, s);
-    else if (wvec <= 8) reg_go<T, 8, 1, 4, 3>(a, num_sms, s);
-    else if (wvec <= 16) reg_go<T, 16, 1, 8, 3>(a, num_sms, s);
-    else reg_go<T, 32, 1, 4, 4>(a, num_sms, s);
+  const char *impl = getenv("CC_GATHER_IMPL");  // "ring" / "ldg" for every width; default: by width
+  // default: rows of <= 8 vectors (a few lanes per row) go to the cp.async
+  // ring with sub-warp groups; wider rows to the lean kernel (measured,
+  // profiles/r1/SUMMARY.md).  The fused root exists in the lean kernel only.
+  const bool lean = impl ? impl[0] == 'l' : wvec > 8;
+  if (lean || a.root_mode) {
+    const int lv = env_int("CC_LDG_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
+    if (wvec <= 32) {
+      if (lv == 1) ldg_go<T, 1, 4>(a, num_sms, s);
+      else ldg_go<T, 1, 8>(a, num_sms, s);
+    } else if (wvec <= 64) {
+      if (lv == 1) ldg_go<T, 2, 4>(a, num_sms, s);
+      else ldg_go<T, 2, 8>(a, num_sms, s);
+    } else if (wvec <= 96) {
+      if (lv == 1) ldg_go<T, 3, 2>(a, num_sms, s);
+      else ldg_go<T, 3, 4>(a, num_sms, s);
+    } else {
+      if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);
+      else ldg_go<T, 4, 2>(a, num_sms, s);
+    }
     return;
   }
   const int vr = env_int("CC_RING_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
@@ -463,27 +611,20 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
   else if (wvec <= 8) ring_go<T, 8, 1, 16, 2>(a, num_sms, s);
   else if (wvec <= 16) ring_go<T, 16, 1, 16, 2>(a, num_sms, s);
   else if (wvec <= 32) ring_go<T, 32, 1, 16, 2>(a, num_sms, s);
-  else if (wvec <= 64) {
-    if (vr == 1) ring_go<T, 32, 2, 4, 2>(a, num_sms, s);
-    else ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
-  } else {
-    switch (vr) {
-      case 1: ring_go<T, 32, 4, 5, 2>(a, num_sms, s); break;
-      case 2: ring_go<T, 32, 4, 3, 2>(a, num_sms, s); break;
-      case 3: ring_go<T, 32, 4, 6, 2>(a, num_sms, s); break;
-      default: ring_go<T, 32, 4, 4, 2>(a, num_sms, s); break;
-    }
-  }
+  else if (wvec <= 64) ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
+  else if (vr == 1) ring_go<T, 32, 4, 5, 2>(a, num_sms, s);
+  else ring_go<T, 32, 4, 4, 2>(a, num_sms, s);
 }
 
 }  // namespace
 
 int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
-                 const AggWork &work, int32_t *col_out, uint16_t *goff, int num_sms, cudaStream_t s) {
+                 const AggWork &work, int32_t *col_out, uint16_t *goff, ItemDesc *desc, int num_sms,
+                 cudaStream_t s) {
   if (work.n_seg + work.n_light == 0) return 0;
   static int grid = 0;
   if (!grid) grid = persistent_grid(k_csort, 256, 0, num_sms);
-  k_csort<<<grid, 256, 0, s>>>(beg, end, col, colors, work, col_out, goff);
+  k_csort<<<grid, 256, 0, s>>>(beg, end, col, colors, work, col_out, goff, desc);
   return 1;
 }
 

@@ -97,55 +97,87 @@ __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_
   }
 }
 
-// Lane-per-vertex combine: a CTA stages 32 vertices' A' / N'' rows in shared
-// memory as [column][33] (stride 33: conflict-free both for the transposing
-// stores and for the lane-indexed loads); each warp takes output columns s,
-// reads the split (x, y) warp-uniformly from L1 and every lane accumulates
-// its own vertex: 2 conflict-free LDS per FMA.  Outputs are staged in shared
-// memory and written back as whole rows.
+// Lane-per-vertex combine (persistent, one CTA of 8 warps per SM): tiles of
+// 32 vertices' A' and N'' rows are staged TRANSPOSED in shared memory as
+// [column][33] by cp.async (double-buffered: tile i+1 streams in while tile i
+// is computed); the split table sits in shared memory when it fits.  Each
+// warp takes groups of 8 output colour sets; per split q one warp-uniform
+// 32-byte read of the table gives 8 (x, y) pairs, and every lane accumulates
+// its own vertex: 2 conflict-free LDS per FMA (shared-memory bound, not HBM).
 template <typename T>
-__global__ void __launch_bounds__(256) k_combine_lane(const T *__restrict__ A, int64_t ldA, int WA,
-                                                      const T *__restrict__ N, int64_t ldN, int WN,
-                                                      const uint32_t *__restrict__ split, int nq, int64_t n,
-                                                      T *__restrict__ out, int64_t ldO, int WO) {
+__device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool ok) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if constexpr (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 4 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 1) k_combine_lane(const T *__restrict__ A, int64_t ldA, int WA,
+                                                         const T *__restrict__ N, int64_t ldN, int WN,
+                                                         const uint32_t *__restrict__ split, int nq, int64_t n,
+                                                         T *__restrict__ out, int64_t ldO, int WO, int nbuf,
+                                                         int split_smem) {
   constexpr int S = 33;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *As = reinterpret_cast<T *>(smem_raw);  // [WA][33]
-  T *Ns = As + S * WA;                      // [WN][33]
-  T *Os = Ns + S * WN;                      // [WO][33]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int W = WA + WN;
+  T *bufs = reinterpret_cast<T *>(smem_raw);  // nbuf x [W][33]: A' columns then N'' columns
+  const int WOp = (WO + 7) & ~7;
+  const uint32_t *sp = split;
+  if (split_smem) {
+    uint32_t *ss = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * S * W);
+    for (int i = threadIdx.x; i < nq * WOp; i += blockDim.x) ss[i] = split[i];
+    sp = ss;
+  }
   const int64_t ntiles = (n + 31) / 32;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  auto stage = [&](int64_t tile, T *b) {
     const int64_t v0 = tile * 32;
-    const int nv = (int)min((int64_t)32, n - v0);
-    for (int r = warp; r < 32; r += nwarp) {  // a warp stages whole rows (coalesced reads)
-      const bool ok = r < nv;
-      for (int x = lane; x < WA; x += 32) As[x * S + r] = ok ? A[(v0 + r) * ldA + x] : (T)0;
-      for (int y = lane; y < WN; y += 32) Ns[y * S + r] = ok ? N[(v0 + r) * ldN + y] : (T)0;
+    for (int r = warp; r < 32; r += nwarp) {
+      const bool ok = v0 + r < n;
+      const int64_t vr = ok ? v0 + r : 0;
+      for (int x = lane; x < WA; x += 32) cp_async_elem(b + x * S + r, A + vr * ldA + x, ok);
+      for (int y = lane; y < WN; y += 32) cp_async_elem(b + (WA + y) * S + r, N + vr * ldN + y, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) stage(tile, bufs);
+  __syncthreads();  // split table staged
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    T *cur = bufs + (size_t)(nbuf == 2 ? (it & 1) : 0) * S * W;
+    if (nbuf == 2) {
+      if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs + (size_t)((it + 1) & 1) * S * W);
+      else asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
-    // 8 outputs per warp pass: two warp-uniform 16-byte split loads per q feed
-    // 8 independent FMA chains (the split table rows are padded to 8 entries)
-    const int WOp = (WO + 7) & ~7;
+    const T *As = cur + lane;
+    const T *Ns = cur + WA * S + lane;
+    const int64_t v = tile * 32 + lane;
     for (int g = warp; g < WOp / 8; g += nwarp) {
       T acc[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = (T)0;
-      const uint4 *sp = reinterpret_cast<const uint4 *>(split) + 2 * g;
+      const uint4 *e = reinterpret_cast<const uint4 *>(sp) + 2 * g;
+#pragma unroll 2
       for (int q = 0; q < nq; ++q) {
-        const uint4 e0 = __ldg(sp + (int64_t)q * (WOp / 4)), e1 = __ldg(sp + (int64_t)q * (WOp / 4) + 1);
+        const uint4 e0 = e[(int64_t)q * (WOp / 4)], e1 = e[(int64_t)q * (WOp / 4) + 1];
         const uint32_t xy[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fma(As[(xy[j] & 0xFFFF) * S + lane], Ns[(xy[j] >> 16) * S + lane], acc[j]);
+        for (int j = 0; j < 8; ++j) acc[j] = fma(As[(xy[j] & 0xFFFF) * S], Ns[(xy[j] >> 16) * S], acc[j]);
       }
+      if (v < n) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (8 * g + j < WO) Os[(8 * g + j) * S + lane] = acc[j];
+        for (int j = 0; j < 8; ++j)
+          if (8 * g + j < WO) out[v * ldO + 8 * g + j] = acc[j];
+      }
     }
-    __syncthreads();
-    for (int r = warp; r < nv; r += nwarp)
-      for (int s = lane; s < WO; s += 32) out[(v0 + r) * ldO + s] = Os[s * S + r];
-    __syncthreads();
+    __syncthreads();  // the buffer is refilled two tiles later (or next tile when single-buffered)
+    if (nbuf == 1 && tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs);
   }
 }
 
@@ -223,14 +255,19 @@ void combine_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, 
 template <typename T>
 void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
                    int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
-  const char *impl = getenv("CC_COMBINE_IMPL");  // "lane": lane-per-vertex kernel (default: V-tile, measured faster)
-  const size_t lane_smem = (size_t)(WA + WN + WO) * 33 * sizeof(T);
-  if (lane_smem <= 200 * 1024 && impl && impl[0] == 'l') {
+  const char *impl = getenv("CC_COMBINE_IMPL");  // "tile": V-tile kernel; default: lane-per-vertex
+  const size_t tile_bytes = (size_t)(WA + WN) * 33 * sizeof(T);
+  const size_t split_bytes = (size_t)nq * ((WO + 7) & ~7) * 4;
+  const size_t cap = 227 * 1024;
+  if (!(impl && impl[0] == 't') && tile_bytes <= cap) {
+    const int nbuf = 2 * tile_bytes <= cap ? 2 : 1;
+    const int split_smem = nbuf * tile_bytes + split_bytes <= cap ? 1 : 0;
+    const size_t smem = nbuf * tile_bytes + (split_smem ? split_bytes : 0);
     auto kern = k_combine_lane<T>;
-    if (lane_smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lane_smem);
-    const int grid = persistent_grid(kern, 256, lane_smem, num_sms);
-    kern<<<grid, 256, lane_smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split,
-                                      nq, n, static_cast<T *>(out), ldO, WO);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = persistent_grid(kern, 256, smem, num_sms);
+    kern<<<grid, 256, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq, n,
+                                 static_cast<T *>(out), ldO, WO, nbuf, split_smem);
     return;
   }
   // wide rows: tile of V vertices (padded rows); k <= 16 bounds a row by

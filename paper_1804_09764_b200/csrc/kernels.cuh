@@ -32,11 +32,26 @@ struct AggWork {
   int64_t n_seg = 0, n_hv = 0;
 };
 
+// Per-colouring descriptor of one work item (written by the colour sort):
+// the item's neighbour stream is its colour-sorted range minus the group of
+// the row vertex's own colour (those neighbours contribute nothing).
+struct ItemDesc {
+  int64_t b;      // first neighbour position of the item
+  int32_t v;      // row vertex
+  int32_t n_s;    // stream length = (e - b) - skip
+  int32_t cv_lo;  // start of the own-colour group (relative to b)
+  int32_t skip;   // size of the own-colour group
+  int32_t cv;     // colour of v
+  int32_t heavy;  // 1 for a heavy-vertex segment
+};
+static_assert(sizeof(ItemDesc) == 32, "ItemDesc is loaded as two 16-byte vectors");
+
 struct GatherArgs {
   const int64_t *beg;     // per vertex: first neighbour position of this pass
   const int64_t *end;     // per vertex: one past the last
   const int32_t *col;     // neighbour ids, colour-sorted within each item
   const uint16_t *goff;   // per item: 16 cumulative colour-group end offsets (relative to item begin)
+  const ItemDesc *desc;   // per item descriptor (bulk gather)
   const uint8_t *colors;  // colour of every row (owned | halo)
   const void *src;        // passive table P' (rows x ld_src), W_in = C(k-1, p-1) valid columns
   int64_t ld_src;
@@ -53,13 +68,23 @@ struct GatherArgs {
   int64_t ld_scratch;
   unsigned int *arrive;   // n_hv counters (zeroed before launch)
   AggWork work;
+  // Fused root (the root step's neighbour sum is needed nowhere else): the
+  // epilogue does not write N'' but X_v = sum_{X'} A'(v, X') N''(v, comp X')
+  // (Eq. 2 at the root + Eq. 3's summand) into per_vertex[v].
+  int root_mode = 0;      // 0: write N''; 1: A' = table rA; 2: A' = N'' itself (root active = lift of this passive)
+  const void *rA = nullptr;
+  int64_t ldA = 0;
+  int WA = 0;
+  const uint16_t *comp = nullptr;  // comp[X'] = rank of [k-1] \ X' in C(k-1, p)
+  double *per_vertex = nullptr;
 };
 
 int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *out, cudaStream_t s);
 // Colour-sort every item's neighbour range (stable) into col_out and record
 // the 16 cumulative colour-group offsets of the item.
 int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
-                 const AggWork &work, int32_t *col_out, uint16_t *goff, int num_sms, cudaStream_t s);
+                 const AggWork &work, int32_t *col_out, uint16_t *goff, ItemDesc *desc, int num_sms,
+                 cudaStream_t s);
 // N''(v, {y}) = #{u in N(v) : sq_{c_v}(col u) = y}, k-1 columns.
 int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                 const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s);

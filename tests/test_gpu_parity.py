@@ -109,6 +109,43 @@ def test_small_suite_heavy_segments_and_chunks_do_not_change_results():
         assert count(g, parent, colors=col, precision="fp32") == pytest.approx(want, rel=TOL_FP32)
 
 
+# ------------------------------------------------------------------ fused root (root evaluated in the gather epilogue)
+FUSED_CASES = [
+    ([-1, 0, 0, 1, 1, 2, 2], 2),  # two identical subtrees under the root: self dot (mode 2)
+    ([-1, 0, 1, 0, 3], 2),        # P5 rooted at its centre
+    ([-1, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6], 2),  # configs[4]'s template
+    ([-1, 0, 0, 2], 1),           # root with a leaf and a P2 child: dot with the active table (mode 1)
+]
+
+
+@pytest.mark.parametrize("parent,mode", FUSED_CASES)
+def test_fused_root_exact(parent, mode, monkeypatch):
+    cc = lib()
+    k = len(parent)
+    graphs = [synth.gnp(60, 0.25, 11), synth.scaled_twin(synth.CONFIGS[3], 10, 16).graph()]
+    for gi, g in enumerate(graphs):
+        col = oracle.color(g.n, k, 40 + gi)
+        want = oracle.dp_count(g, parent, col, oracle.NUM_EXACT, want_root=True)
+        for seg in (0, 3):
+            with context(g, parent, fixed_root=1, segment_len=seg) as ctx:
+                cc.cc_set_colors(ctx, col)
+                x = cc.cc_count_colorful(ctx)
+                assert cc.cc_last_stats(ctx)["fused_root"] == mode
+                root = cc.cc_get_subtree_counts(ctx, parent.index(-1), g.n, k, k)
+                monkeypatch.setenv("CC_FUSED_ROOT", "0")
+                x_unfused = cc.cc_count_colorful(ctx)
+                assert cc.cc_last_stats(ctx)["fused_root"] == 0
+                monkeypatch.delenv("CC_FUSED_ROOT")
+            # exact while every partial sum stays below 2^53; the 15-vertex tree's
+            # root products do not, so the bar there is the fp64 1e-12
+            assert rel_err(x, float(want.total)) <= TOL_FP64, (parent, gi, seg)
+            assert rel_err(x_unfused, float(want.total)) <= TOL_FP64, (parent, gi, seg)
+            assert_close_entries(root, want.root.reshape(-1, 1), TOL_FP64, f"fused root per vertex {parent}")
+        with context(g, parent, "fp32", fixed_root=1) as ctx:
+            cc.cc_set_colors(ctx, col)
+            assert rel_err(cc.cc_count_colorful(ctx), float(want.total)) <= TOL_FP32
+
+
 # ------------------------------------------------------------------ configs[1]: fp64 1e-12 per entry, fp32 1e-4
 def test_config1_fp64_every_entry_and_fp32_total():
     cfg = synth.CONFIGS[1]
