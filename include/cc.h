@@ -177,6 +177,15 @@ cc_status cc_template_info(cc_ctx *ctx, int64_t *aut, int64_t *aut_root, int32_t
  * World must be 1. */
 cc_status cc_get_subtree_counts(cc_ctx *ctx, int32_t x, double *out);
 
+/* Row-sampled variant of cc_get_subtree_counts (test hook for graphs whose
+ * full tables do not fit host memory): out[i * C(k, s) + r] = C(vertices[i],
+ * T_x, S_r) for the nv ORIGINAL vertex ids given, same colex layout; the root
+ * (x = parent -1 vertex) gives one column.  Runs one colouring's DP with the
+ * user's rooting; the fused root stays on (the sampled rows are copied right
+ * after their table is produced).  world == 1 only.  Errors: CC_ERR_ARG (bad
+ * x / id / pointer), CC_ERR_STATE. */
+cc_status cc_get_subtree_rows(cc_ctx *ctx, int32_t x, const int32_t *vertices, int32_t nv, double *out);
+
 /* Timing of the last cc_count_colorful, in ms, per phase (device events):
  * out[0] = total, then per DP step.  *n receives the number written. */
 cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);

@@ -138,6 +138,15 @@ def cc_last_profile(ctx) -> dict:
     return dict(zip(PROFILE_FIELDS, buf[:n.value].tolist()))
 
 
+def cc_get_subtree_rows(ctx, x: int, vertices, k: int, s: int) -> np.ndarray:
+    """Rows of the full-subtree table of template vertex x for the given original vertex ids."""
+    vs = np.ascontiguousarray(vertices, dtype=np.int32)
+    w = math.comb(k, s)
+    out = np.zeros((vs.size, w), dtype=np.float64)
+    _check(ctx, _lib.cc_get_subtree_rows(ctx, int(x), _p(vs), int(vs.size), _p(out)))
+    return out
+
+
 def cc_last_stats(ctx) -> dict:
     buf = np.zeros(6, dtype=np.float64)
     _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 6))

@@ -48,6 +48,7 @@ SIGNATURES = {
     "cc_get_colors": (c_i32, [vp, vp]),
     "cc_template_info": (c_i32, [vp, vp, vp, vp]),
     "cc_get_subtree_counts": (c_i32, [vp, c_i32, vp]),
+    "cc_get_subtree_rows": (c_i32, [vp, c_i32, vp, c_i32, vp]),
     "cc_last_profile": (c_i32, [vp, vp, c_i32, vp]),
     "cc_last_stats": (c_i32, [vp, vp, c_i32]),
     "cc_colex_rank": (c_i64, [c_u32]),

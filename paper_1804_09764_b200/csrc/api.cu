@@ -111,6 +111,7 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
     int l2 = 0;
     CUDA_OK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, opt->device));
     if (l2 > 0) c->l2_bytes = l2;
+    CUDA_OK(cudaDeviceGetAttribute(&c->l2_persist_max, cudaDevAttrMaxPersistingL2CacheSize, opt->device));
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
     cudaMemPool_t pool;
@@ -302,6 +303,70 @@ cc_status cc_get_subtree_counts(cc_ctx *c, int32_t x, double *out) {
         const int64_t ci = compressed_index(sets[r], col[i]);
         if (ci >= 0) row[r] = tab[(size_t)i * Wc + ci];
       }
+    }
+  }
+  API_END(c)
+}
+
+cc_status cc_get_subtree_rows(cc_ctx *c, int32_t x, const int32_t *vertices, int32_t nv, double *out) {
+  API_BEGIN(c)
+  if (!c->has_graph || !c->has_template || !c->has_colors) throw Error(CC_ERR_STATE, "needs graph, template, colouring");
+  if (c->opt.world != 1) throw Error(CC_ERR_STATE, "cc_get_subtree_rows needs world == 1");
+  if (x < 0 || x >= c->plan.k || nv < 0 || (nv && (!vertices || !out)))
+    throw Error(CC_ERR_ARG, "bad template vertex, count or NULL pointer");
+  struct Restore {
+    cc_ctx *c;
+    ~Restore() {
+      try {
+        cc::replan(c, false);
+      } catch (...) {
+      }
+    }
+  } restore{c};
+  cc::replan(c, true);
+  const auto &pl = c->plan;
+  const auto &R = c->part;
+  const int k = pl.k;
+  const int tid = pl.full_table[x];
+  // original id -> internal row (owned rows only; isolated vertices: -1)
+  std::vector<int64_t> inv((size_t)c->n_global, -1);
+  for (int64_t i = 0; i < R.n_own; ++i) inv[R.own_orig[i]] = i;
+  std::vector<int64_t> rows;
+  for (int32_t i = 0; i < nv; ++i) {
+    if (vertices[i] < 0 || vertices[i] >= c->n_global) throw Error(CC_ERR_ARG, "vertex id out of range");
+    if (inv[vertices[i]] >= 0) rows.push_back(inv[vertices[i]]);
+  }
+  std::vector<uint8_t> col((size_t)c->n_crow);
+  if (!col.empty()) CUDA_OK(cudaMemcpy(col.data(), c->d_colors, col.size(), cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> colour_of((size_t)c->n_global, 0);
+  for (int64_t i = 0; i < R.n_own; ++i) colour_of[R.own_orig[i]] = col[i];
+  for (size_t i = 0; i < R.iso_orig.size(); ++i) colour_of[R.iso_orig[i]] = col[c->n_rows + i];
+  double X = 0;
+  if (tid == -2) {  // root: per-vertex count, one column
+    std::vector<double> root;
+    if (k > 1) cc::run_count(c, &X, -1, nullptr, &root);
+    for (int32_t i = 0; i < nv; ++i)
+      out[i] = k == 1 ? 1.0 : (inv[vertices[i]] >= 0 ? root[inv[vertices[i]]] : 0.0);
+  } else if (tid == -1) {  // a leaf: the single-vertex table
+    for (int32_t i = 0; i < nv; ++i)
+      for (int j = 0; j < k; ++j) out[(size_t)i * k + j] = j == colour_of[vertices[i]] ? 1.0 : 0.0;
+  } else {
+    std::vector<double> tab;
+    if (!rows.empty()) cc::run_count(c, &X, tid, &tab, nullptr, &rows);
+    const int s = pl.tables[tid].size;
+    const int64_t Wd = cc::binom(k, s), Wc = cc::binom(k - 1, s - 1);
+    std::vector<uint32_t> sets((size_t)Wd);
+    for (int64_t r = 0; r < Wd; ++r) sets[r] = cc::colex_unrank(s, r);
+    size_t j = 0;
+    for (int32_t i = 0; i < nv; ++i) {
+      double *row = out + (size_t)i * Wd;
+      std::fill(row, row + Wd, 0.0);
+      if (inv[vertices[i]] < 0) continue;  // isolated: no embedding of a tree with >= 2 vertices
+      for (int64_t r = 0; r < Wd; ++r) {
+        const int64_t ci = compressed_index(sets[r], colour_of[vertices[i]]);
+        if (ci >= 0) row[r] = tab[j * Wc + ci];
+      }
+      ++j;
     }
   }
   API_END(c)

@@ -74,6 +74,7 @@ struct cc_ctx {
   bool poisoned = false;
   int num_sms = 148;
   int64_t l2_bytes = 126LL << 20;
+  int l2_persist_max = 0;  // cudaDevAttrMaxPersistingL2CacheSize
   cudaStream_t s_main = nullptr, s_comm = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<void *> persistent;  // cudaMalloc'd: graph, plan tables (freed on reload / destroy)
@@ -143,7 +144,18 @@ struct cc_ctx {
   }
   void *amalloc(size_t bytes, cudaStream_t s) {
     void *p = nullptr;
-    CUDA_OK(cudaMallocAsync(&p, std::max<size_t>(bytes, 256), s));
+    cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(bytes, 256), s);
+    if (e == cudaErrorMemoryAllocation) {
+      // freed blocks stay mapped in the pool (release threshold = max) and may
+      // be too fragmented for one large table: return them and retry once
+      (void)cudaGetLastError();
+      cudaMemPool_t pool;
+      CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, opt.device));
+      CUDA_OK(cudaStreamSynchronize(s));
+      CUDA_OK(cudaMemPoolTrimTo(pool, 0));
+      e = cudaMallocAsync(&p, std::max<size_t>(bytes, 256), s);
+    }
+    CUDA_OK(e);
     cur_bytes += bytes;
     peak_bytes = std::max(peak_bytes, cur_bytes);
     return p;
@@ -186,5 +198,10 @@ void launch_colouring(cc_ctx *c, uint64_t seed);
 // One colouring's DP.  dump_table >= 0 keeps every table and returns table
 // `dump_table` (compressed rows, owned order) in *dump; root_out receives the
 // per-vertex root values.
-void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out);
+// dump_table >= 0: copy that table (compressed rows) into *dump -- every
+// owned row (dump_rows == nullptr; disables the fused root and releases) or
+// only the internal rows listed in *dump_rows (copied right after the step
+// that produces the table; nothing else changes).
+void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out,
+               const std::vector<int64_t> *dump_rows = nullptr);
 }  // namespace cc

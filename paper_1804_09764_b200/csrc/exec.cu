@@ -229,10 +229,31 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
     a.comp = c->d_comp;
     a.per_vertex = rf->per_vertex;
   }
+  // Optional L2 persistence window over the hub rows of the source table
+  // (rows are degree-ordered, hubs first): CC_L2_PERSIST_MB > 0 sets aside
+  // that much L2 for them while this gather runs.
+  const char *pm = getenv("CC_L2_PERSIST_MB");
+  const size_t persist = pm ? std::min<size_t>((size_t)atof(pm) * (1 << 20), (size_t)c->l2_persist_max) : 0;
+  if (persist > 0) {
+    CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+    cudaStreamAttrValue attr = {};
+    attr.accessPolicyWindow.base_ptr = P;
+    attr.accessPolicyWindow.num_bytes = std::min<size_t>(persist, (size_t)c->n_rows * a.ld_src * elem);
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CUDA_OK(cudaStreamSetAttribute(c->s_main, cudaStreamAttributeAccessPolicyWindow, &attr));
+  }
   cudaEvent_t b = c->begin(c->s_main);
   c->stats[3] += dev::launch_gather(elem, a, c->num_sms, c->s_main);
   c->check_launch();
   c->end(PH_GATHER, c->s_main, b);
+  if (persist > 0) {
+    cudaStreamAttrValue attr = {};
+    attr.accessPolicyWindow.num_bytes = 0;
+    CUDA_OK(cudaStreamSetAttribute(c->s_main, cudaStreamAttributeAccessPolicyWindow, &attr));
+    CUDA_OK(cudaCtxResetPersistingL2Cache());
+  }
   if (scratch) c->afree(scratch, sbytes, c->s_main);
   // algorithmic bytes: index stream + compressed rows of the neighbours whose
   // colour differs from the row vertex's (expected fraction (k-1)/k) + N'' rows
@@ -291,7 +312,8 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
 
 }  // namespace
 
-void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out) {
+void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out,
+               const std::vector<int64_t> *dump_rows) {
   const Plan &pl = c->plan;
   const int k = pl.k, elem = c->elem();
   std::fill(c->stats, c->stats + 6, 0.0);
@@ -307,15 +329,12 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   cudaEvent_t t0 = c->ev(), t1 = c->ev();
   CUDA_OK(cudaEventRecord(t0, c->s_main));
 
-  // colour-sort the neighbour ranges of every pass (once per colouring)
-  if (!c->sorted_valid) {
+  // world > 1: colour-sort the neighbour ranges of both passes (once per
+  // colouring); world 1 sorts below, fused with the leaf level (hist)
+  if (c->opt.world > 1 && !c->sorted_valid) {
     cudaEvent_t b = c->begin(c->s_main);
-    if (c->opt.world == 1) {
-      csort(c, c->p_full);
-    } else {
-      csort(c, c->p_local);
-      csort(c, c->p_remote);
-    }
+    csort(c, c->p_local);
+    csort(c, c->p_remote);
     c->end(PH_CSORT, c->s_main, b);
     c->sorted_valid = true;
   }
@@ -331,7 +350,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   {
     const Step &rs = pl.steps[sr];
     const char *f = getenv("CC_FUSED_ROOT");
-    if (c->opt.world == 1 && dump_table < 0 && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
+    if (c->opt.world == 1 && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
       const int P = rs.passive;
       int s_l = -1, users = 0;
       for (int s = 0; s < sr; ++s) {
@@ -359,6 +378,19 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     if (pl.steps[s].p == 1) last_hist_use = s;
   double *per_vertex = nullptr;
   if (root_out || fuse) per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
+  if (c->opt.world == 1) {  // colour sort + leaf level N''(v, {y}) in one pass over the adjacency
+    if (last_hist_use >= 0) hist = bufs.make((size_t)rows * c->ld_of(k - 1) * elem);
+    cudaEvent_t b = c->begin(c->s_main);
+    Pass &p = c->p_full;
+    c->stats[3] += dev::launch_csort_hist(elem, p.beg, p.end, c->d_col, c->d_colors, p.view(), k, c->d_col_sorted,
+                                          p.goff, p.desc, hist >= 0 ? bufs.ptr(hist) : nullptr, c->ld_of(k - 1), rows,
+                                          c->num_sms, c->s_main);
+    c->check_launch();
+    c->end(PH_CSORT, c->s_main, b);
+    c->sorted_valid = true;
+    c->stats[1] += (double)p.nnz * 9.0 + (double)p.items() * 64.0 + (hist >= 0 ? (double)n * (k - 1) * elem : 0.0);
+    if (hist >= 0) c->stats[0] += (double)c->part.col.size() * k;  // U counts C(k,1) = k colour sets per entry
+  }
 
   for (int s = 0; s < (int)pl.steps.size(); ++s) {
     const Step &st = pl.steps[s];
@@ -424,7 +456,20 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       c->end(PH_COMBINE, c->s_main, b);
       c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;
     }
-    if (dump_table < 0) {  // release dead tables / neighbour sums
+    if (dump_rows && st.out == dump_table && st.out >= 0 && T[st.out] >= 0) {  // sampled rows of this table
+      const int W = (int)binom(k - 1, pl.tables[dump_table].size - 1);
+      const size_t ld = (size_t)c->ld_of(W);
+      std::vector<char> raw(dump_rows->size() * (size_t)W * elem);
+      for (size_t i = 0; i < dump_rows->size(); ++i)
+        CUDA_OK(cudaMemcpyAsync(raw.data() + i * W * elem,
+                                static_cast<char *>(bufs.ptr(T[st.out])) + (size_t)(*dump_rows)[i] * ld * elem,
+                                (size_t)W * elem, cudaMemcpyDeviceToHost, c->s_main));
+      CUDA_OK(cudaStreamSynchronize(c->s_main));
+      dump->assign(dump_rows->size() * (size_t)W, 0.0);
+      for (size_t i = 0; i < dump->size(); ++i)
+        (*dump)[i] = elem == 8 ? reinterpret_cast<double *>(raw.data())[i] : reinterpret_cast<float *>(raw.data())[i];
+    }
+    if (dump_table < 0 || dump_rows) {  // release dead tables / neighbour sums
       for (int id = 0; id < nt; ++id) {
         if (T[id] >= 0 && last_use[id] == s) {
           bufs.unref(T[id]);
@@ -449,7 +494,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   CUDA_OK(cudaEventRecord(t1, c->s_main));
   double host_x = 0;
   CUDA_OK(cudaMemcpyAsync(&host_x, c->d_result, sizeof(double), cudaMemcpyDeviceToHost, c->s_main));
-  if (dump && dump_table >= 0 && T[dump_table] >= 0) {
+  if (dump && !dump_rows && dump_table >= 0 && T[dump_table] >= 0) {
     const int W = (int)binom(k - 1, pl.tables[dump_table].size - 1);
     std::vector<char> raw((size_t)n * c->ld_of(W) * elem);
     if (!raw.empty())

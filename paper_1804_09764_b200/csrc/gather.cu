@@ -97,6 +97,119 @@ __global__ void __launch_bounds__(256) k_csort(const int64_t *__restrict__ beg, 
   }
 }
 
+// Colour sort v2 (world 1), fused with the leaf level (hist, p = 1).  One
+// warp per item; colour groups via __match_any_sync (one instruction per 32
+// neighbours instead of one ballot per colour); the first 4 x 32 neighbours
+// stay in registers between the counting and the placing pass; the next
+// item's vertex and range are prefetched one and two items ahead.  Writes the
+// colour-sorted list, the 16 cumulative group ends, the item descriptor and
+// N''(v, {y}) (heavy segments add their counts atomically into zeroed rows:
+// small integers, exact in fp32/fp64).
+template <typename T>
+__global__ void __launch_bounds__(256) k_csort2(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+                                                const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
+                                                AggWork work, int k, int32_t *__restrict__ col_out,
+                                                uint16_t *__restrict__ goff, ItemDesc *__restrict__ desc,
+                                                T *__restrict__ hist, int64_t ldh) {
+  constexpr int R = 4;  // neighbour chunks of 32 kept in registers
+  __shared__ int cnt_all[8][32];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int *cs = cnt_all[threadIdx.x >> 5];
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const int64_t n_items = work.n_seg + work.n_light;
+  auto vertex_of = [&](int64_t it) -> int32_t {
+    return it < work.n_seg ? work.seg_v[it] : (it < n_items ? work.light[it - work.n_seg] : 0);
+  };
+  int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  int32_t v_next = vertex_of(it);             // stage 1 of item it
+  int32_t v_next2 = vertex_of(it + nwarps);   // stage 1 of item it + nw
+  for (; it < n_items; it += nwarps) {
+    const int32_t v = v_next;
+    const bool heavy = it < work.n_seg;
+    const int64_t b = heavy ? work.seg_b[it] : beg[v];
+    const int64_t e = heavy ? work.seg_e[it] : end[v];
+    const int cv = colors[v];
+    v_next = v_next2;
+    v_next2 = vertex_of(it + 2 * nwarps);
+    const int d = (int)(e - b);
+    cs[lane] = 0;
+    __syncwarp();
+    int32_t ur[R];
+    int cr[R];
+#pragma unroll
+    for (int ci = 0; ci < R; ++ci) {
+      const bool ok = ci * 32 + lane < d;
+      ur[ci] = ok ? __ldg(col + b + ci * 32 + lane) : 0;
+      cr[ci] = ok ? (int)colors[ur[ci]] : 16 + lane % 16;  // invalid lanes: own groups, never counted
+    }
+#pragma unroll
+    for (int ci = 0; ci < R; ++ci) {
+      if (ci * 32 < d) {
+        const unsigned m = __match_any_sync(0xffffffffu, cr[ci]);
+        if (cr[ci] < 16 && (m & lt) == 0) cs[cr[ci]] += __popc(m);
+        __syncwarp();
+      }
+    }
+    for (int o = R * 32; o < d; o += 32) {
+      const bool ok = o + lane < d;
+      const int32_t u = ok ? __ldg(col + b + o + lane) : 0;
+      const int c = ok ? (int)colors[u] : 16 + lane % 16;
+      const unsigned m = __match_any_sync(0xffffffffu, c);
+      if (c < 16 && (m & lt) == 0) cs[c] += __popc(m);
+      __syncwarp();
+    }
+    const int cnt = lane < 16 ? cs[lane] : 0;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int excl = incl - cnt;
+    if (lane < 16) goff[it * 16 + lane] = (uint16_t)incl;
+    if (hist && lane < k && lane != cv) {
+      T *p = hist + (int64_t)v * ldh + (lane < cv ? lane : lane - 1);  // squeeze: sq_{c_v}(lane)
+      if (heavy) atomicAdd(p, (T)cnt);
+      else *p = (T)cnt;
+    }
+    const int skip = __shfl_sync(0xffffffffu, cnt, cv), cv_lo = __shfl_sync(0xffffffffu, excl, cv);
+    if (lane == 0) {
+      ItemDesc dsc;
+      dsc.b = b;
+      dsc.v = v;
+      dsc.n_s = d - skip;
+      dsc.cv_lo = cv_lo;
+      dsc.skip = skip;
+      dsc.cv = cv;
+      dsc.heavy = heavy ? 1 : 0;
+      desc[it] = dsc;
+    }
+    // placing pass: cs[c] = running start of colour c
+    __syncwarp();
+    if (lane < 16) cs[lane] = excl;
+    __syncwarp();
+    auto place = [&](int32_t u, int c, bool ok) {
+      const unsigned m = __match_any_sync(0xffffffffu, c);
+      const int base = ok ? cs[c] : 0;
+      __syncwarp();
+      if (ok) {
+        col_out[b + base + __popc(m & lt)] = u;
+        if ((m & lt) == 0) cs[c] = base + __popc(m);
+      }
+      __syncwarp();
+    };
+#pragma unroll
+    for (int ci = 0; ci < R; ++ci)
+      if (ci * 32 < d) place(ur[ci], cr[ci], ci * 32 + lane < d);
+    for (int o = R * 32; o < d; o += 32) {
+      const bool ok = o + lane < d;
+      const int32_t u = ok ? __ldg(col + b + o + lane) : 0;
+      place(u, ok ? (int)colors[u] : 16 + lane % 16, ok);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ hist (p = 1)
 // Heavy segments add their counts atomically into a zeroed row: the values
 // are small integers, exact in fp32/fp64, so the result is order-independent.
@@ -417,7 +530,7 @@ __device__ __forceinline__ void load_desc(const GatherArgs &a, int64_t it, int l
   go = lane < 16 ? (int)__ldg(a.goff + it * 16 + lane) : 0;
 }
 
-template <typename T, int NV, int U>
+template <typename T, int NV, int U, bool PF = false>
 __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
@@ -499,6 +612,19 @@ __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
 #pragma unroll
             for (int j = 0; j < NV; ++j) zero_vec(x[uu][j]);
           for (; r + U <= cnt; r += U) {  // full blocks of U rows: no row predicates
+            if constexpr (PF) {  // L2 prefetch of the next block's rows (no registers held)
+#pragma unroll
+              for (int uu = 0; uu < U; ++uu) {
+                const int rn = r + U + uu;
+                const uint32_t un = (uint32_t)__shfl_sync(0xffffffffu, my_u, rn & 31);
+                if (rn < cnt) {
+                  const char *rowp = lbase + (uint64_t)un * ld_bytes;
+#pragma unroll
+                  for (int j = 0; j < NV; ++j)
+                    if (valid[j] && (lane & 7) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + 512 * j));
+                }
+              }
+            }
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
               const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, r + uu);
@@ -547,11 +673,11 @@ __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
   }
 }
 
-template <typename T, int NV, int U>
+template <typename T, int NV, int U, bool PF = false>
 void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = 32 * NV * VW;
-  auto kern = k_gather_ldg<T, NV, U>;
+  auto kern = k_gather_ldg<T, NV, U, PF>;
   const size_t row = (size_t)a.W_out * sizeof(double);
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
@@ -593,12 +719,15 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
     const int lv = env_int("CC_LDG_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
     if (wvec <= 32) {
       if (lv == 1) ldg_go<T, 1, 4>(a, num_sms, s);
+      else if (lv == 3) ldg_go<T, 1, 8, true>(a, num_sms, s);
       else ldg_go<T, 1, 8>(a, num_sms, s);
     } else if (wvec <= 64) {
       if (lv == 1) ldg_go<T, 2, 4>(a, num_sms, s);
+      else if (lv == 3) ldg_go<T, 2, 8, true>(a, num_sms, s);
       else ldg_go<T, 2, 8>(a, num_sms, s);
     } else if (wvec <= 96) {
       if (lv == 1) ldg_go<T, 3, 2>(a, num_sms, s);
+      else if (lv == 3) ldg_go<T, 3, 4, true>(a, num_sms, s);
       else ldg_go<T, 3, 4>(a, num_sms, s);
     } else {
       if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);
@@ -626,6 +755,29 @@ int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, con
   if (!grid) grid = persistent_grid(k_csort, 256, 0, num_sms);
   k_csort<<<grid, 256, 0, s>>>(beg, end, col, colors, work, col_out, goff, desc);
   return 1;
+}
+
+int launch_csort_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
+                      const AggWork &work, int k, int32_t *col_out, uint16_t *goff, ItemDesc *desc, void *hist,
+                      int64_t ldh, int64_t hist_rows, int num_sms, cudaStream_t s) {
+  if (work.n_seg + work.n_light == 0) return 0;
+  int launches = 1;
+  if (hist && work.n_seg) {  // heavy rows accumulate segment counts atomically
+    cudaMemsetAsync(hist, 0, (size_t)hist_rows * ldh * elem, s);
+    ++launches;
+  }
+  if (elem == 8) {
+    static int grid = 0;
+    if (!grid) grid = persistent_grid(k_csort2<double>, 256, 0, num_sms);
+    k_csort2<double><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, col_out, goff, desc,
+                                          static_cast<double *>(hist), ldh);
+  } else {
+    static int grid = 0;
+    if (!grid) grid = persistent_grid(k_csort2<float>, 256, 0, num_sms);
+    k_csort2<float><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, col_out, goff, desc,
+                                         static_cast<float *>(hist), ldh);
+  }
+  return launches;
 }
 
 int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,

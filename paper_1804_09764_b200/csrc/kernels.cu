@@ -113,8 +113,8 @@ __device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool ok) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256, 1) k_combine_lane(const T *__restrict__ A, int64_t ldA, int WA,
+template <typename T, int OUT>
+__global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A, int64_t ldA, int WA,
                                                          const T *__restrict__ N, int64_t ldN, int WN,
                                                          const uint32_t *__restrict__ split, int nq, int64_t n,
                                                          T *__restrict__ out, int64_t ldO, int WO, int nbuf,
@@ -123,11 +123,12 @@ __global__ void __launch_bounds__(256, 1) k_combine_lane(const T *__restrict__ A
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int W = WA + WN;
+  const size_t bstride = ((size_t)S * W * sizeof(T) + 15) / 16 * 16 / sizeof(T);  // 16-byte aligned buffers
   T *bufs = reinterpret_cast<T *>(smem_raw);  // nbuf x [W][33]: A' columns then N'' columns
   const int WOp = (WO + 7) & ~7;
   const uint32_t *sp = split;
   if (split_smem) {
-    uint32_t *ss = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * S * W);
+    uint32_t *ss = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * bstride);
     for (int i = threadIdx.x; i < nq * WOp; i += blockDim.x) ss[i] = split[i];
     sp = ss;
   }
@@ -146,9 +147,9 @@ __global__ void __launch_bounds__(256, 1) k_combine_lane(const T *__restrict__ A
   if (tile < ntiles) stage(tile, bufs);
   __syncthreads();  // split table staged
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    T *cur = bufs + (size_t)(nbuf == 2 ? (it & 1) : 0) * S * W;
+    T *cur = bufs + (size_t)(nbuf == 2 ? (it & 1) : 0) * bstride;
     if (nbuf == 2) {
-      if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs + (size_t)((it + 1) & 1) * S * W);
+      if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs + (size_t)((it + 1) & 1) * bstride);
       else asm volatile("cp.async.commit_group;\n" ::: "memory");
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
@@ -158,22 +159,29 @@ __global__ void __launch_bounds__(256, 1) k_combine_lane(const T *__restrict__ A
     const T *As = cur + lane;
     const T *Ns = cur + WA * S + lane;
     const int64_t v = tile * 32 + lane;
-    for (int g = warp; g < WOp / 8; g += nwarp) {
-      T acc[8];
+    for (int g = warp; g < (WO + OUT - 1) / OUT; g += nwarp) {
+      T acc[OUT];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = (T)0;
-      const uint4 *e = reinterpret_cast<const uint4 *>(sp) + 2 * g;
+      for (int j = 0; j < OUT; ++j) acc[j] = (T)0;
+      const uint4 *e = reinterpret_cast<const uint4 *>(sp) + (OUT / 4) * g;
 #pragma unroll 2
       for (int q = 0; q < nq; ++q) {
-        const uint4 e0 = e[(int64_t)q * (WOp / 4)], e1 = e[(int64_t)q * (WOp / 4) + 1];
-        const uint32_t xy[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+        uint32_t xy[OUT];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fma(As[(xy[j] & 0xFFFF) * S], Ns[(xy[j] >> 16) * S], acc[j]);
+        for (int h = 0; h < OUT / 4; ++h) {
+          const uint4 eh = e[(int64_t)q * (WOp / 4) + h];
+          xy[4 * h + 0] = eh.x;
+          xy[4 * h + 1] = eh.y;
+          xy[4 * h + 2] = eh.z;
+          xy[4 * h + 3] = eh.w;
+        }
+#pragma unroll
+        for (int j = 0; j < OUT; ++j) acc[j] = fma(As[(xy[j] & 0xFFFF) * S], Ns[(xy[j] >> 16) * S], acc[j]);
       }
       if (v < n) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (8 * g + j < WO) out[v * ldO + 8 * g + j] = acc[j];
+        for (int j = 0; j < OUT; ++j)
+          if (OUT * g + j < WO) out[v * ldO + OUT * g + j] = acc[j];
       }
     }
     __syncthreads();  // the buffer is refilled two tiles later (or next tile when single-buffered)
@@ -256,17 +264,19 @@ template <typename T>
 void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
                    int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
   const char *impl = getenv("CC_COMBINE_IMPL");  // "tile": V-tile kernel; default: lane-per-vertex
-  const size_t tile_bytes = (size_t)(WA + WN) * 33 * sizeof(T);
+  const size_t tile_bytes = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
   const size_t split_bytes = (size_t)nq * ((WO + 7) & ~7) * 4;
   const size_t cap = 227 * 1024;
   if (!(impl && impl[0] == 't') && tile_bytes <= cap) {
     const int nbuf = 2 * tile_bytes <= cap ? 2 : 1;
     const int split_smem = nbuf * tile_bytes + split_bytes <= cap ? 1 : 0;
     const size_t smem = nbuf * tile_bytes + (split_smem ? split_bytes : 0);
-    auto kern = k_combine_lane<T>;
+    // 16 warps; output groups of 4 or 8 colour sets, whichever balances the warps better
+    const int r8 = ((WO + 7) / 8 + 15) / 16, r4 = ((WO + 3) / 4 + 15) / 16;
+    auto kern = 2 * r8 <= r4 ? k_combine_lane<T, 8> : k_combine_lane<T, 4>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = persistent_grid(kern, 256, smem, num_sms);
-    kern<<<grid, 256, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq, n,
+    const int grid = persistent_grid(kern, 512, smem, num_sms);
+    kern<<<grid, 512, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq, n,
                                  static_cast<T *>(out), ldO, WO, nbuf, split_smem);
     return;
   }
