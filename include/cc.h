@@ -157,6 +157,16 @@ cc_status cc_count_colorful(cc_ctx *ctx, double *colorful_maps);
 cc_status cc_estimate(cc_ctx *ctx, int32_t iterations, uint64_t seed0, double *estimate,
                       double *per_iter);
 
+/* The paper's estimator (Alg. 1 last line, lines 180-181): run
+ * `iterations` colourings with seeds seed0 + j, form C_j = X_j k^k/k!/|Aut(T)|,
+ * split them in iteration order into `groups` groups of equal size (the
+ * remainder one per group from the front), and return the median of the
+ * group means (mean of the two middle ones for an even count).  groups = 1
+ * is cc_estimate.  per_iter (nullable) receives the X_j.  Collective.
+ * Errors: CC_ERR_ARG unless 1 <= groups <= iterations. */
+cc_status cc_estimate_mom(cc_ctx *ctx, int32_t iterations, uint64_t seed0, int32_t groups, double *estimate,
+                          double *per_iter);
+
 /* ---- test and bench hooks (off the hot path) ---------------------------- */
 
 /* Use a caller-supplied colouring: colors[v] in [0, k) for every ORIGINAL
@@ -200,6 +210,15 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
 
 /* ---- host-only introspection (no GPU needed; used by CPU tests) --------- */
+
+/* Median of means of n colourful counts X (as cc_estimate_mom, no GPU). */
+cc_status cc_median_of_means(const double *X, int32_t n, int32_t k, int64_t aut, int32_t groups, double *out);
+
+/* Niter = ceil(constant * e^k * ln(1/delta) / eps^2), at least 1 (PAPER.md
+ * Alg. 1 line 3, line 154: Niter = O(e^k log(1/delta) / eps^2); the constant
+ * is the caller's).  CC_ERR_ARG unless eps > 0, 0 < delta <= 1, k >= 1,
+ * constant > 0. */
+cc_status cc_niter(double eps, double delta, int32_t k, double constant, int64_t *out);
 
 /* Colex rank of the colour set `mask` (bit c = colour c) among sets of the
  * same size: rank(S) = sum_i C(s_i, i+1), s_0 < s_1 < ... (combinatorial

@@ -59,6 +59,10 @@ def _load():
         lib.or_dp_count.argtypes = [i64, vp, vp, i32, vp, vp, i32, i32, vp, vp, vp, vp, vp]
         lib.or_estimate.restype = ctypes.c_double
         lib.or_estimate.argtypes = [i32, vp, i32, u64]
+        lib.or_mom.restype = ctypes.c_double
+        lib.or_mom.argtypes = [i32, vp, i32, u64, i32]
+        lib.or_niter.restype = ctypes.c_int64
+        lib.or_niter.argtypes = [ctypes.c_double, ctypes.c_double, i32, ctypes.c_double]
         _lib = lib
     return _lib
 
@@ -169,3 +173,20 @@ def estimate(X, k: int, aut_t: int) -> float:
     """mean_j X_j * k^k/k! / |Aut(T)| (readings C-1, C-10)."""
     X = np.ascontiguousarray(X, dtype=np.float64)
     return float(_load().or_estimate(len(X), X.ctypes.data, k, aut_t))
+
+
+def median_of_means(X, k: int, aut_t: int, t: int) -> float:
+    """Median of t group means of C_j = X_j k^k/k!/|Aut(T)| (Alg. 1 last line; SPEC.md 455-463)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    r = _load().or_mom(len(X), X.ctypes.data, k, aut_t, t)
+    if r < 0:
+        raise OracleError("median_of_means: need 1 <= t <= len(X)")
+    return float(r)
+
+
+def niter(eps: float, delta: float, k: int, c: float = 1.0) -> int:
+    """Niter = ceil(c e^k ln(1/delta) / eps^2), >= 1 (Alg. 1 line 3)."""
+    r = int(_load().or_niter(eps, delta, k, c))
+    if r < 0:
+        raise OracleError("niter: need eps > 0, 0 < delta <= 1, k >= 1, c > 0")
+    return r

@@ -28,6 +28,14 @@
  *   or_estimate    : mean_j X_j * k^k/k! / |Aut(T)| (PAPER.md lines 146-147,
  *                    176; reading C-1 divides maps by |Aut(T)|; reading C-10
  *                    takes the mean).
+ *   or_mom         : median of means (Alg. 1 last line, lines
+ *                    180-181): C_j = X_j k^k/k!/|Aut(T)|, t groups of equal
+ *                    size in iteration order (remainder one per group from
+ *                    the front), median of the group
+ *                    means (mean of the middle two for even t).
+ *   or_niter       : Niter = ceil(c e^k ln(1/delta) / eps^2), >= 1 (Alg. 1
+ *                    line 3; constant c = 1 by default,
+ *                    SPEC.md lines 441-446).
  *   or_aut         : |Aut(T)| = #injective edge-preserving maps T -> T
  *                    (brute force of the definition on G = T).
  * Numeric types of the DP: exact unsigned __int128 with overflow detection,
@@ -320,6 +328,37 @@ int or_dp_count(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
   }
   subsets_free(&ss);
   return rc;
+}
+
+/* Median of means (Alg. 1 last line, lines 180-181). */
+static int cmp_ld(const void *a, const void *b) {
+  const long double x = *(const long double *)a, y = *(const long double *)b;
+  return x < y ? -1 : x > y;
+}
+double or_mom(int32_t iters, const double *X, int32_t k, uint64_t aut, int32_t t) {
+  if (iters < 1 || t < 1 || t > iters) return -1.0;
+  long double scale = 1;
+  for (int i = 1; i <= k; ++i) scale *= (long double)k / i; /* k^k / k! */
+  long double *Z = (long double *)malloc(sizeof(long double) * (size_t)t);
+  int pos = 0;
+  for (int g = 0; g < t; ++g) {
+    const int size = iters / t + (g < iters % t ? 1 : 0);
+    long double s = 0;
+    for (int j = 0; j < size; ++j) s += (long double)X[pos + j] * scale / (long double)aut;
+    pos += size;
+    Z[g] = s / size;
+  }
+  qsort(Z, (size_t)t, sizeof(long double), cmp_ld);
+  const long double med = t % 2 ? Z[t / 2] : (Z[t / 2 - 1] + Z[t / 2]) / 2;
+  free(Z);
+  return (double)med;
+}
+
+/* Niter = ceil(c e^k ln(1/delta) / eps^2), at least 1 (Alg. 1 line 3). */
+int64_t or_niter(double eps, double delta, int32_t k, double c) {
+  if (!(eps > 0) || !(delta > 0) || !(delta <= 1) || k < 1 || !(c > 0)) return -1;
+  const double v = ceil(c * exp((double)k) * log(1.0 / delta) / (eps * eps));
+  return v < 1 ? 1 : (int64_t)v;
 }
 
 /* Estimator (Alg. 1, lines 146-147 and 176; readings C-1, C-10):

@@ -138,6 +138,26 @@ def cc_last_profile(ctx) -> dict:
     return dict(zip(PROFILE_FIELDS, buf[:n.value].tolist()))
 
 
+def cc_estimate_mom(ctx, iterations: int, seed0: int, groups: int, per_iter: bool = False):
+    est = ctypes.c_double()
+    xs = np.zeros(iterations, dtype=np.float64)
+    _check(ctx, _lib.cc_estimate_mom(ctx, iterations, seed0, groups, ctypes.byref(est), _p(xs)))
+    return (est.value, xs) if per_iter else est.value
+
+
+def cc_median_of_means(xs, k: int, aut: int, groups: int) -> float:
+    x = np.ascontiguousarray(xs, dtype=np.float64)
+    out = ctypes.c_double()
+    _check(None, _lib.cc_median_of_means(_p(x), int(x.size), k, aut, groups, ctypes.byref(out)))
+    return out.value
+
+
+def cc_niter(eps: float, delta: float, k: int, constant: float = 1.0) -> int:
+    out = ctypes.c_int64()
+    _check(None, _lib.cc_niter(eps, delta, k, constant, ctypes.byref(out)))
+    return out.value
+
+
 def cc_get_subtree_rows(ctx, x: int, vertices, k: int, s: int) -> np.ndarray:
     """Rows of the full-subtree table of template vertex x for the given original vertex ids."""
     vs = np.ascontiguousarray(vertices, dtype=np.int32)

@@ -49,6 +49,9 @@ SIGNATURES = {
     "cc_template_info": (c_i32, [vp, vp, vp, vp]),
     "cc_get_subtree_counts": (c_i32, [vp, c_i32, vp]),
     "cc_get_subtree_rows": (c_i32, [vp, c_i32, vp, c_i32, vp]),
+    "cc_estimate_mom": (c_i32, [vp, c_i32, c_u64, c_i32, vp, vp]),
+    "cc_median_of_means": (c_i32, [vp, c_i32, c_i32, c_i64, c_i32, vp]),
+    "cc_niter": (c_i32, [c_dbl, c_dbl, c_i32, c_dbl, vp]),
     "cc_last_profile": (c_i32, [vp, vp, c_i32, vp]),
     "cc_last_stats": (c_i32, [vp, vp, c_i32]),
     "cc_colex_rank": (c_i64, [c_u32]),

@@ -1,5 +1,7 @@
 // api.cu -- the C ABI of include/cc.h: argument checks, state machine,
 // error conversion (no C++ exception crosses the boundary).
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 
@@ -111,7 +113,6 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
     int l2 = 0;
     CUDA_OK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, opt->device));
     if (l2 > 0) c->l2_bytes = l2;
-    CUDA_OK(cudaDeviceGetAttribute(&c->l2_persist_max, cudaDevAttrMaxPersistingL2CacheSize, opt->device));
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
     cudaMemPool_t pool;
@@ -239,6 +240,23 @@ cc_status cc_estimate(cc_ctx *c, int32_t iterations, uint64_t seed0, double *est
   long double scale = 1;  // k^k / k!
   for (int i = 1; i <= c->plan.k; ++i) scale *= (long double)c->plan.k / i;
   *estimate = (double)(mean * scale / (long double)c->plan.aut);
+  if (per_iter) std::copy(xs.begin(), xs.end(), per_iter);
+  API_END(c)
+}
+
+cc_status cc_estimate_mom(cc_ctx *c, int32_t iterations, uint64_t seed0, int32_t groups, double *estimate,
+                          double *per_iter) {
+  API_BEGIN(c)
+  if (iterations < 1 || groups < 1 || groups > iterations || !estimate)
+    throw Error(CC_ERR_ARG, "need 1 <= groups <= iterations and estimate != NULL");
+  if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_estimate_mom needs a graph and a template");
+  std::vector<double> xs((size_t)iterations);
+  for (int j = 0; j < iterations; ++j) {
+    cc::launch_colouring(c, seed0 + (uint64_t)j);
+    cc::run_count(c, &xs[j], -1, nullptr, nullptr);
+  }
+  const cc_status st = cc_median_of_means(xs.data(), iterations, c->plan.k, c->plan.aut, groups, estimate);
+  if (st != CC_OK) throw Error(st, "median of means");
   if (per_iter) std::copy(xs.begin(), xs.end(), per_iter);
   API_END(c)
 }
@@ -388,6 +406,31 @@ cc_status cc_last_stats(cc_ctx *c, double *out, int32_t cap) {
 }
 
 // ---------------------------------------------------------------- host-only
+cc_status cc_median_of_means(const double *X, int32_t n, int32_t k, int64_t aut, int32_t groups, double *out) {
+  if (!X || !out || n < 1 || groups < 1 || groups > n || k < 1 || aut < 1) return CC_ERR_ARG;
+  long double scale = 1;  // k^k / k!
+  for (int i = 1; i <= k; ++i) scale *= (long double)k / i;
+  std::vector<long double> z((size_t)groups);
+  int64_t pos = 0;
+  for (int g = 0; g < groups; ++g) {  // equal sizes in iteration order, remainder from the front
+    const int64_t size = n / groups + (g < n % groups ? 1 : 0);
+    long double s = 0;
+    for (int64_t j = 0; j < size; ++j) s += (long double)X[pos + j];
+    pos += size;
+    z[g] = s / size * scale / (long double)aut;
+  }
+  std::sort(z.begin(), z.end());
+  *out = (double)(groups % 2 ? z[groups / 2] : (z[groups / 2 - 1] + z[groups / 2]) / 2);
+  return CC_OK;
+}
+
+cc_status cc_niter(double eps, double delta, int32_t k, double constant, int64_t *out) {
+  if (!out || !(eps > 0) || !(delta > 0) || !(delta <= 1) || k < 1 || !(constant > 0)) return CC_ERR_ARG;
+  const double v = std::ceil(constant * std::exp((double)k) * std::log(1.0 / delta) / (eps * eps));
+  *out = v < 1 ? 1 : (int64_t)v;
+  return CC_OK;
+}
+
 int64_t cc_colex_rank(uint32_t mask) { return mask >> cc::kMaxK ? -1 : cc::colex_rank(mask); }
 
 uint32_t cc_colex_unrank(int32_t s, int64_t r) {

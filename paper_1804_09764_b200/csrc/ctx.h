@@ -74,7 +74,6 @@ struct cc_ctx {
   bool poisoned = false;
   int num_sms = 148;
   int64_t l2_bytes = 126LL << 20;
-  int l2_persist_max = 0;  // cudaDevAttrMaxPersistingL2CacheSize
   cudaStream_t s_main = nullptr, s_comm = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<void *> persistent;  // cudaMalloc'd: graph, plan tables (freed on reload / destroy)

@@ -229,31 +229,10 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
     a.comp = c->d_comp;
     a.per_vertex = rf->per_vertex;
   }
-  // Optional L2 persistence window over the hub rows of the source table
-  // (rows are degree-ordered, hubs first): CC_L2_PERSIST_MB > 0 sets aside
-  // that much L2 for them while this gather runs.
-  const char *pm = getenv("CC_L2_PERSIST_MB");
-  const size_t persist = pm ? std::min<size_t>((size_t)atof(pm) * (1 << 20), (size_t)c->l2_persist_max) : 0;
-  if (persist > 0) {
-    CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-    cudaStreamAttrValue attr = {};
-    attr.accessPolicyWindow.base_ptr = P;
-    attr.accessPolicyWindow.num_bytes = std::min<size_t>(persist, (size_t)c->n_rows * a.ld_src * elem);
-    attr.accessPolicyWindow.hitRatio = 1.0f;
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    CUDA_OK(cudaStreamSetAttribute(c->s_main, cudaStreamAttributeAccessPolicyWindow, &attr));
-  }
   cudaEvent_t b = c->begin(c->s_main);
   c->stats[3] += dev::launch_gather(elem, a, c->num_sms, c->s_main);
   c->check_launch();
   c->end(PH_GATHER, c->s_main, b);
-  if (persist > 0) {
-    cudaStreamAttrValue attr = {};
-    attr.accessPolicyWindow.num_bytes = 0;
-    CUDA_OK(cudaStreamSetAttribute(c->s_main, cudaStreamAttributeAccessPolicyWindow, &attr));
-    CUDA_OK(cudaCtxResetPersistingL2Cache());
-  }
   if (scratch) c->afree(scratch, sbytes, c->s_main);
   // algorithmic bytes: index stream + compressed rows of the neighbours whose
   // colour differs from the row vertex's (expected fraction (k-1)/k) + N'' rows

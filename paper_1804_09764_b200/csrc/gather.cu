@@ -530,7 +530,7 @@ __device__ __forceinline__ void load_desc(const GatherArgs &a, int64_t it, int l
   go = lane < 16 ? (int)__ldg(a.goff + it * 16 + lane) : 0;
 }
 
-template <typename T, int NV, int U, bool PF = false>
+template <typename T, int NV, int U>
 __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
@@ -612,19 +612,6 @@ __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
 #pragma unroll
             for (int j = 0; j < NV; ++j) zero_vec(x[uu][j]);
           for (; r + U <= cnt; r += U) {  // full blocks of U rows: no row predicates
-            if constexpr (PF) {  // L2 prefetch of the next block's rows (no registers held)
-#pragma unroll
-              for (int uu = 0; uu < U; ++uu) {
-                const int rn = r + U + uu;
-                const uint32_t un = (uint32_t)__shfl_sync(0xffffffffu, my_u, rn & 31);
-                if (rn < cnt) {
-                  const char *rowp = lbase + (uint64_t)un * ld_bytes;
-#pragma unroll
-                  for (int j = 0; j < NV; ++j)
-                    if (valid[j] && (lane & 7) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + 512 * j));
-                }
-              }
-            }
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
               const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, r + uu);
@@ -673,11 +660,11 @@ __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
   }
 }
 
-template <typename T, int NV, int U, bool PF = false>
+template <typename T, int NV, int U>
 void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = 32 * NV * VW;
-  auto kern = k_gather_ldg<T, NV, U, PF>;
+  auto kern = k_gather_ldg<T, NV, U>;
   const size_t row = (size_t)a.W_out * sizeof(double);
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
@@ -719,15 +706,12 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
     const int lv = env_int("CC_LDG_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
     if (wvec <= 32) {
       if (lv == 1) ldg_go<T, 1, 4>(a, num_sms, s);
-      else if (lv == 3) ldg_go<T, 1, 8, true>(a, num_sms, s);
       else ldg_go<T, 1, 8>(a, num_sms, s);
     } else if (wvec <= 64) {
       if (lv == 1) ldg_go<T, 2, 4>(a, num_sms, s);
-      else if (lv == 3) ldg_go<T, 2, 8, true>(a, num_sms, s);
       else ldg_go<T, 2, 8>(a, num_sms, s);
     } else if (wvec <= 96) {
       if (lv == 1) ldg_go<T, 3, 2>(a, num_sms, s);
-      else if (lv == 3) ldg_go<T, 3, 4, true>(a, num_sms, s);
       else ldg_go<T, 3, 4>(a, num_sms, s);
     } else {
       if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);

@@ -25,6 +25,11 @@ namespace dev {
 
 namespace {
 
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // ------------------------------------------------------------------ colour
 __global__ void k_color(const int32_t *__restrict__ orig, int64_t n, uint64_t seed, int k,
                         uint8_t *__restrict__ out) {
@@ -113,33 +118,56 @@ __device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool ok) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
 }
 
-template <typename T, int OUT>
+template <typename T, int V>
+struct LaneVec;
+template <typename T>
+struct LaneVec<T, 1> {
+  using type = T;
+  __device__ static T at(const T &x, int) { return x; }
+};
+template <>
+struct LaneVec<float, 2> {
+  using type = float2;
+  __device__ static float at(const float2 &x, int i) { return i ? x.y : x.x; }
+};
+template <>
+struct LaneVec<double, 2> {
+  using type = double2;
+  __device__ static double at(const double2 &x, int i) { return i ? x.y : x.x; }
+};
+
+// V vertices per lane (tile = 32 V vertices): element (v, c) of the staged
+// tile sits at [c][v / V][v % V] with a row stride of 33 vectors, so a lane
+// reads its V vertices of column c with one conflict-free V-wide LDS and one
+// address computation serves V FMAs.
+template <typename T, int OUT, int V, bool SS>
 __global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A, int64_t ldA, int WA,
                                                          const T *__restrict__ N, int64_t ldN, int WN,
                                                          const uint32_t *__restrict__ split, int nq, int64_t n,
                                                          T *__restrict__ out, int64_t ldO, int WO, int nbuf,
                                                          int split_smem) {
-  constexpr int S = 33;
+  constexpr int S = 33;       // row stride in V-vectors
+  constexpr int TV = 32 * V;  // vertices per tile
+  using LV = typename LaneVec<T, V>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int W = WA + WN;
-  const size_t bstride = ((size_t)S * W * sizeof(T) + 15) / 16 * 16 / sizeof(T);  // 16-byte aligned buffers
-  T *bufs = reinterpret_cast<T *>(smem_raw);  // nbuf x [W][33]: A' columns then N'' columns
+  const size_t bstride = ((size_t)S * V * W * sizeof(T) + 15) / 16 * 16 / sizeof(T);  // 16-byte aligned buffers
+  T *bufs = reinterpret_cast<T *>(smem_raw);  // nbuf x [W][33][V]: A' columns then N'' columns
   const int WOp = (WO + 7) & ~7;
-  const uint32_t *sp = split;
-  if (split_smem) {
-    uint32_t *ss = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * bstride);
+  // split table: shared memory (SS) or read-only global (L1-resident)
+  uint32_t *ss = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * bstride);
+  if constexpr (SS)
     for (int i = threadIdx.x; i < nq * WOp; i += blockDim.x) ss[i] = split[i];
-    sp = ss;
-  }
-  const int64_t ntiles = (n + 31) / 32;
+  const int64_t ntiles = (n + TV - 1) / TV;
   auto stage = [&](int64_t tile, T *b) {
-    const int64_t v0 = tile * 32;
-    for (int r = warp; r < 32; r += nwarp) {
+    const int64_t v0 = tile * TV;
+    for (int r = warp; r < TV; r += nwarp) {
       const bool ok = v0 + r < n;
       const int64_t vr = ok ? v0 + r : 0;
-      for (int x = lane; x < WA; x += 32) cp_async_elem(b + x * S + r, A + vr * ldA + x, ok);
-      for (int y = lane; y < WN; y += 32) cp_async_elem(b + (WA + y) * S + r, N + vr * ldN + y, ok);
+      T *dst = b + (r / V) * V + (r % V);
+      for (int x = lane; x < WA; x += 32) cp_async_elem(dst + (size_t)x * S * V, A + vr * ldA + x, ok);
+      for (int y = lane; y < WN; y += 32) cp_async_elem(dst + (size_t)(WA + y) * S * V, N + vr * ldN + y, ok);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -156,33 +184,45 @@ __global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
-    const T *As = cur + lane;
-    const T *Ns = cur + WA * S + lane;
-    const int64_t v = tile * 32 + lane;
+    // byte bases of the lane's vectors: one IMAD per operand address
+    const char *Ab = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + lane);
+    const char *Nb = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + (size_t)WA * S + lane);
+    constexpr uint32_t CB = S * sizeof(LV);  // bytes per staged column
+    const int64_t vb = tile * TV + (int64_t)lane * V;
     for (int g = warp; g < (WO + OUT - 1) / OUT; g += nwarp) {
-      T acc[OUT];
+      T acc[OUT][V];
 #pragma unroll
-      for (int j = 0; j < OUT; ++j) acc[j] = (T)0;
-      const uint4 *e = reinterpret_cast<const uint4 *>(sp) + (OUT / 4) * g;
+      for (int j = 0; j < OUT; ++j)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[j][i] = (T)0;
+      const uint4 *e = reinterpret_cast<const uint4 *>(SS ? ss : split) + (OUT / 4) * g;
 #pragma unroll 2
       for (int q = 0; q < nq; ++q) {
         uint32_t xy[OUT];
 #pragma unroll
         for (int h = 0; h < OUT / 4; ++h) {
-          const uint4 eh = e[(int64_t)q * (WOp / 4) + h];
+          const uint4 eh = SS ? e[q * (WOp / 4) + h] : __ldg(e + (int64_t)q * (WOp / 4) + h);
           xy[4 * h + 0] = eh.x;
           xy[4 * h + 1] = eh.y;
           xy[4 * h + 2] = eh.z;
           xy[4 * h + 3] = eh.w;
         }
 #pragma unroll
-        for (int j = 0; j < OUT; ++j) acc[j] = fma(As[(xy[j] & 0xFFFF) * S], Ns[(xy[j] >> 16) * S], acc[j]);
-      }
-      if (v < n) {
+        for (int j = 0; j < OUT; ++j) {
+          const LV av = *reinterpret_cast<const LV *>(Ab + (xy[j] & 0xFFFF) * CB);
+          const LV nv = *reinterpret_cast<const LV *>(Nb + (xy[j] >> 16) * CB);
 #pragma unroll
-        for (int j = 0; j < OUT; ++j)
-          if (OUT * g + j < WO) out[v * ldO + OUT * g + j] = acc[j];
+          for (int i = 0; i < V; ++i)
+            acc[j][i] = fma(LaneVec<T, V>::at(av, i), LaneVec<T, V>::at(nv, i), acc[j][i]);
+        }
       }
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        if (vb + i < n) {
+#pragma unroll
+          for (int j = 0; j < OUT; ++j)
+            if (OUT * g + j < WO) out[(vb + i) * ldO + OUT * g + j] = acc[j][i];
+        }
     }
     __syncthreads();  // the buffer is refilled two tiles later (or next tile when single-buffered)
     if (nbuf == 1 && tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs);
@@ -264,16 +304,31 @@ template <typename T>
 void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
                    int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
   const char *impl = getenv("CC_COMBINE_IMPL");  // "tile": V-tile kernel; default: lane-per-vertex
-  const size_t tile_bytes = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
   const size_t split_bytes = (size_t)nq * ((WO + 7) & ~7) * 4;
   const size_t cap = 227 * 1024;
-  if (!(impl && impl[0] == 't') && tile_bytes <= cap) {
-    const int nbuf = 2 * tile_bytes <= cap ? 2 : 1;
+  // V = 2 vertices per lane (one address per 2 FMAs) when a single buffer of
+  // 64-vertex tiles plus the split table fits; else V = 1, double-buffered
+  const int vpref = env_int("CC_COMBINE_V", 2);
+  const size_t tile2 = ((size_t)(WA + WN) * 33 * 2 * sizeof(T) + 15) / 16 * 16;
+  const size_t tile1 = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
+  const int V = (vpref == 2 && tile2 + split_bytes <= cap) ? 2 : 1;
+  const size_t tile_bytes = V == 2 ? tile2 : tile1;
+  // the lane kernel pays a staging pass per tile: it wins only when the
+  // split walk does enough FMAs per staged entry (measured: (9;6,3) at 11.7
+  // FMA/entry wins, (4;3,1) at 2.1 loses)
+  const double intensity = (double)WO * nq / (double)(WA + WN + WO);
+  const bool lane_ok = impl ? impl[0] != 't' : intensity >= 4.0;
+  if (lane_ok && tile_bytes <= cap) {
+    const int nbuf = V == 1 && 2 * tile_bytes <= cap ? 2 : 1;
     const int split_smem = nbuf * tile_bytes + split_bytes <= cap ? 1 : 0;
     const size_t smem = nbuf * tile_bytes + (split_smem ? split_bytes : 0);
     // 16 warps; output groups of 4 or 8 colour sets, whichever balances the warps better
     const int r8 = ((WO + 7) / 8 + 15) / 16, r4 = ((WO + 3) / 4 + 15) / 16;
-    auto kern = 2 * r8 <= r4 ? k_combine_lane<T, 8> : k_combine_lane<T, 4>;
+    const bool o8 = 2 * r8 <= r4;
+    auto kern = V == 2 ? (split_smem ? (o8 ? k_combine_lane<T, 8, 2, true> : k_combine_lane<T, 4, 2, true>)
+                                     : (o8 ? k_combine_lane<T, 8, 2, false> : k_combine_lane<T, 4, 2, false>))
+                       : (split_smem ? (o8 ? k_combine_lane<T, 8, 1, true> : k_combine_lane<T, 4, 1, true>)
+                                     : (o8 ? k_combine_lane<T, 8, 1, false> : k_combine_lane<T, 4, 1, false>));
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = persistent_grid(kern, 512, smem, num_sms);
     kern<<<grid, 512, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq, n,

@@ -298,6 +298,17 @@ def test_estimator_matches_oracle_formula():
     assert est == pytest.approx(oracle.estimate(want_x, 4, oracle.aut(parent)), rel=1e-14)
 
 
+def test_median_of_means_estimator_matches_oracle():
+    cc = lib()
+    g = synth.gnp(40, 0.3, 3)
+    parent = [-1, 0, 1, 1]
+    with context(g, parent) as ctx:
+        est, xs = cc.cc_estimate_mom(ctx, 21, 500, 5, per_iter=True)
+    want_x = [oracle.dp_count(g, parent, oracle.color(g.n, 4, 500 + j), oracle.NUM_EXACT).total for j in range(21)]
+    assert list(xs) == [float(v) for v in want_x]
+    assert est == pytest.approx(oracle.median_of_means(want_x, 4, oracle.aut(parent), 5), rel=1e-14)
+
+
 # ------------------------------------------------------------------ errors
 def test_errors_are_reported():
     cc = lib()

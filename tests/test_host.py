@@ -139,3 +139,23 @@ def test_partition_invariants(cc, world):
         # hubs first within the rank
         d = deg[p["own_orig"]]
         assert np.all(d[:-1] >= d[1:])
+
+
+def test_median_of_means_and_niter_match_the_oracle(cc):
+    """The library's host-side estimator pieces against the oracle's (both
+    pinned to PAPER.md Alg. 1 / SPEC.md worked values in test_oracle_pins)."""
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 5, 7, 10, 33):
+        xs = rng.integers(0, 10 ** 6, n).astype(np.float64)
+        for t in sorted({1, 2, 3, n // 2 or 1, n}):
+            if t > n:
+                continue
+            for k, aut in ((3, 1), (7, 6), (12, 8)):
+                got = cc.cc_median_of_means(xs, k, aut, t)
+                assert got == pytest.approx(oracle.median_of_means(xs, k, aut, t), rel=1e-15), (n, t, k)
+    for eps, delta, k in ((0.5, 0.1, 3), (0.1, 0.01, 7), (0.05, 0.5, 12), (0.5, 1.0, 3)):
+        assert cc.cc_niter(eps, delta, k) == oracle.niter(eps, delta, k)
+    with pytest.raises(cc.CCError):
+        cc.cc_median_of_means([1.0], 3, 1, 2)
+    with pytest.raises(cc.CCError):
+        cc.cc_niter(0.0, 0.1, 3)

@@ -342,3 +342,31 @@ def test_table3_intensity_values():
         m = sum(math.comb(k, t) for t, _ in subs)
         c = sum(math.comb(k, t) * math.comb(t, 1) for t, _ in subs)
         assert m == int(mem) and c == int(comp) and round(c / m, 1) == float(inten), name
+
+
+def test_niter_spec_values():
+    """Niter = ceil(c e^k ln(1/delta) / eps^2) (Alg. 1 line 3; SPEC.md
+    lines 441-446 worked values)."""
+    assert oracle.niter(0.5, 0.1, 3) == 185  # S:444: ceil(20.0855 x 2.3026 / 0.25)
+    assert oracle.niter(0.5, 1.0, 3) == 1  # S:445: delta -> 1 clamps to 1
+    for eps in (0.5, 0.3, 0.1):  # S:446: halving eps quadruples Niter up to the ceiling
+        a, b = oracle.niter(eps, 0.05, 5), oracle.niter(eps / 2, 0.05, 5)
+        assert 4 * a - 4 <= b <= 4 * a
+    assert oracle.niter(0.5, 0.1, 3, c=2.0) == math.ceil(2 * math.exp(3) * math.log(10) / 0.25)
+
+
+def test_median_of_means_spec_values():
+    """Median of group means (Alg. 1 last line, lines 180-181; SPEC.md
+    lines 455-463): groups of floor(N/t) in iteration order, remainder one per
+    group from the front; mean of the two middle values for even t."""
+    s3 = 27 / 6  # k = 3 scale k^k/k!, |Aut| = 1
+    assert oracle.median_of_means([0, 0, 0, 100], 3, 1, 4) == 0.0  # S:461 outlier robustness
+    assert oracle.median_of_means([7.0] * 9, 3, 1, 3) == pytest.approx(7 * s3, rel=1e-15)  # S:460 constant
+    xs = [1.0, 2.0, 4.0, 8.0, 16.0]
+    assert oracle.median_of_means(xs, 3, 1, 1) == pytest.approx(oracle.estimate(xs, 3, 1), rel=1e-15)  # S:462
+    # N = 5, t = 2: groups {1, 2, 4} and {8, 16}; even t -> mean of the two group means
+    assert oracle.median_of_means(xs, 3, 1, 2) == pytest.approx(((7 / 3) + 12) / 2 * s3, rel=1e-15)
+    # N = 7, t = 3: sizes 3, 2, 2 -> means 2, 4.5, 7 -> median 4.5 (|Aut| = 2 halves it)
+    assert oracle.median_of_means([1, 2, 3, 4, 5, 6, 8], 3, 2, 3) == pytest.approx(4.5 * s3 / 2, rel=1e-15)
+    with pytest.raises(oracle.OracleError):
+        oracle.median_of_means([1.0], 3, 1, 2)
