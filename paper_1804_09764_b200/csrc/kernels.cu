@@ -314,10 +314,11 @@ void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ld
   const int V = (vpref == 2 && tile2 + split_bytes <= cap) ? 2 : 1;
   const size_t tile_bytes = V == 2 ? tile2 : tile1;
   // the lane kernel pays a staging pass per tile: it wins only when the
-  // split walk does enough FMAs per staged entry (measured: (9;6,3) at 11.7
-  // FMA/entry wins, (4;3,1) at 2.1 loses)
+  // split walk does enough FMAs per staged entry (measured: (9;6,3) of
+  // config 3 at 11.7 FMA/entry wins, config 2's (7;4,3) at 6.7 and (4;3,1)
+  // at 2.1 lose)
   const double intensity = (double)WO * nq / (double)(WA + WN + WO);
-  const bool lane_ok = impl ? impl[0] != 't' : intensity >= 4.0;
+  const bool lane_ok = impl ? impl[0] != 't' : intensity >= 8.0;
   if (lane_ok && tile_bytes <= cap) {
     const int nbuf = V == 1 && 2 * tile_bytes <= cap ? 2 : 1;
     const int split_smem = nbuf * tile_bytes + split_bytes <= cap ? 1 : 0;
