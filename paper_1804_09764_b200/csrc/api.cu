@@ -191,15 +191,18 @@ cc_status cc_set_colors(cc_ctx *c, const uint8_t *colors) {
   API_BEGIN(c)
   if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_set_colors needs a graph and a template");
   if (!colors && c->n_global) throw Error(CC_ERR_ARG, "colors is NULL");
-  const auto &R = c->part;
-  std::vector<uint8_t> h((size_t)c->n_crow);
-  for (int64_t i = 0; i < R.n_own; ++i) h[i] = colors[R.own_orig[i]];
-  for (int64_t i = 0; i < R.n_halo; ++i) h[R.n_own + i] = colors[R.halo_orig[i]];
-  for (size_t i = 0; i < R.iso_orig.size(); ++i) h[c->n_rows + i] = colors[R.iso_orig[i]];
-  for (auto x : h)
-    if (x >= c->plan.k) throw Error(CC_ERR_ARG, "colour out of [0, k)");
-  if (!h.empty()) CUDA_OK(cudaMemcpyAsync(c->d_colors, h.data(), h.size(), cudaMemcpyHostToDevice, c->s_main));
+  // one H2D copy of the caller's array (DMA when it is pinned), then the
+  // permutation to the internal row order and the range check on the device
+  unsigned bad = 0;
+  if (c->n_global) {
+    CUDA_OK(cudaMemsetAsync(c->d_bad, 0, sizeof(unsigned), c->s_main));
+    CUDA_OK(cudaMemcpyAsync(c->d_color_stage, colors, (size_t)c->n_global, cudaMemcpyHostToDevice, c->s_main));
+    cc::dev::launch_permute_colors(c->d_color_stage, c->d_orig, c->n_crow, c->plan.k, c->d_colors, c->d_bad, c->s_main);
+    c->check_launch();
+    CUDA_OK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, c->s_main));
+  }
   CUDA_OK(cudaStreamSynchronize(c->s_main));
+  if (bad) throw Error(CC_ERR_ARG, "colour out of [0, k)");
   c->has_colors = true;
   c->sorted_valid = false;
   API_END(c)

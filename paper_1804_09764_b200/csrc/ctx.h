@@ -86,6 +86,8 @@ struct cc_ctx {
   int64_t *d_rp = nullptr, *d_mid = nullptr;
   int32_t *d_col = nullptr, *d_col_sorted = nullptr, *d_orig = nullptr, *d_send_idx = nullptr;
   uint8_t *d_colors = nullptr;
+  uint8_t *d_color_stage = nullptr;  // n_global bytes: a caller's colouring in original order
+  unsigned *d_bad = nullptr;
   cc::Pass p_full, p_local, p_remote;  // world 1: p_full; world > 1: p_local + p_remote (+ p_full for hist)
   int64_t max_seg = 0, max_hv = 0;
 

@@ -98,6 +98,8 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
   c->n_crow = (int64_t)orig.size();
   c->d_orig = c->pupload(orig);
   c->d_colors = c->pmalloc<uint8_t>((size_t)std::max<int64_t>(c->n_crow, 1));
+  c->d_color_stage = c->pmalloc<uint8_t>((size_t)std::max<int64_t>(c->n_global, 1));
+  c->d_bad = c->pmalloc<unsigned>(1);
   std::vector<int64_t> beg(R.rp.begin(), R.rp.end() - 1), end(R.rp.begin() + 1, R.rp.end());
   build_pass(c, beg, end, false, c->p_full);
   c->p_full.beg = c->d_rp;

@@ -151,13 +151,23 @@ __global__ void __launch_bounds__(256) k_csort2(const int64_t *__restrict__ beg,
         __syncwarp();
       }
     }
-    for (int o = R * 32; o < d; o += 32) {
-      const bool ok = o + lane < d;
-      const int32_t u = ok ? __ldg(col + b + o + lane) : 0;
-      const int c = ok ? (int)colors[u] : 16 + lane % 16;
-      const unsigned m = __match_any_sync(0xffffffffu, c);
-      if (c < 16 && (m & lt) == 0) cs[c] += __popc(m);
-      __syncwarp();
+    for (int o0 = R * 32; o0 < d; o0 += R * 32) {  // long lists: R chunks of loads in flight
+      int cq[R];
+#pragma unroll
+      for (int ci = 0; ci < R; ++ci) {
+        const int o = o0 + ci * 32;
+        const bool ok = o + lane < d;
+        const int32_t u = ok ? __ldg(col + b + o + lane) : 0;
+        cq[ci] = ok ? (int)colors[u] : 16 + lane % 16;
+      }
+#pragma unroll
+      for (int ci = 0; ci < R; ++ci) {
+        if (o0 + ci * 32 < d) {
+          const unsigned m = __match_any_sync(0xffffffffu, cq[ci]);
+          if (cq[ci] < 16 && (m & lt) == 0) cs[cq[ci]] += __popc(m);
+          __syncwarp();
+        }
+      }
     }
     const int cnt = lane < 16 ? cs[lane] : 0;
     int incl = cnt;
@@ -202,10 +212,19 @@ __global__ void __launch_bounds__(256) k_csort2(const int64_t *__restrict__ beg,
 #pragma unroll
     for (int ci = 0; ci < R; ++ci)
       if (ci * 32 < d) place(ur[ci], cr[ci], ci * 32 + lane < d);
-    for (int o = R * 32; o < d; o += 32) {
-      const bool ok = o + lane < d;
-      const int32_t u = ok ? __ldg(col + b + o + lane) : 0;
-      place(u, ok ? (int)colors[u] : 16 + lane % 16, ok);
+    for (int o0 = R * 32; o0 < d; o0 += R * 32) {
+      int32_t uq[R];
+      int cq[R];
+#pragma unroll
+      for (int ci = 0; ci < R; ++ci) {
+        const int o = o0 + ci * 32;
+        const bool ok = o + lane < d;
+        uq[ci] = ok ? __ldg(col + b + o + lane) : 0;
+        cq[ci] = ok ? (int)colors[uq[ci]] : 16 + lane % 16;
+      }
+#pragma unroll
+      for (int ci = 0; ci < R; ++ci)
+        if (o0 + ci * 32 < d) place(uq[ci], cq[ci], o0 + ci * 32 + lane < d);
     }
   }
 }
@@ -701,7 +720,7 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
   // default: rows of <= 8 vectors (a few lanes per row) go to the cp.async
   // ring with sub-warp groups; wider rows to the lean kernel (measured,
   // profiles/r1/SUMMARY.md).  The fused root exists in the lean kernel only.
-  const bool lean = impl ? impl[0] == 'l' : wvec > 8;
+  const bool lean = impl ? impl[0] == 'l' : wvec > 16;
   if (lean || a.root_mode) {
     const int lv = env_int("CC_LDG_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
     if (wvec <= 32) {
@@ -720,9 +739,18 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
     return;
   }
   const int vr = env_int("CC_RING_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
-  if (wvec <= 4) ring_go<T, 4, 1, 16, 2>(a, num_sms, s);
-  else if (wvec <= 8) ring_go<T, 8, 1, 16, 2>(a, num_sms, s);
-  else if (wvec <= 16) ring_go<T, 16, 1, 16, 2>(a, num_sms, s);
+  // narrow rows: small rings (more resident groups) measured faster
+  // (p = 2: D 16 -> 4: 12.3 -> 9.0 ms; p = 3: G 16 x 1 -> 8 x 2 vectors,
+  // D 4: 31.5 -> 19.8 ms, the lean kernel 27.8 ms)
+  if (wvec <= 4) {
+    if (vr == 2) ring_go<T, 4, 1, 3, 2>(a, num_sms, s);
+    else ring_go<T, 4, 1, 4, 2>(a, num_sms, s);
+  } else if (wvec <= 8) ring_go<T, 8, 1, 4, 2>(a, num_sms, s);
+  else if (wvec <= 16) {
+    if (vr == 2) ring_go<T, 8, 2, 3, 2>(a, num_sms, s);
+    else if (vr == 3) ring_go<T, 16, 1, 4, 2>(a, num_sms, s);
+    else ring_go<T, 8, 2, 4, 2>(a, num_sms, s);
+  }
   else if (wvec <= 32) ring_go<T, 32, 1, 16, 2>(a, num_sms, s);
   else if (wvec <= 64) ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
   else if (vr == 1) ring_go<T, 32, 4, 5, 2>(a, num_sms, s);

@@ -40,6 +40,19 @@ __global__ void k_color(const int32_t *__restrict__ orig, int64_t n, uint64_t se
   }
 }
 
+// A caller-supplied colouring (original ids) -> the internal row order, with
+// the range check [0, k) on the device (bad[0] |= 1 on a violation).
+__global__ void k_permute_colors(const uint8_t *__restrict__ by_orig, const int32_t *__restrict__ orig, int64_t n,
+                                 int k, uint8_t *__restrict__ out, unsigned *__restrict__ bad) {
+  bool ok = true;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t c = by_orig[orig[i]];
+    ok &= c < k;
+    out[i] = c;
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
 // ------------------------------------------------------------------ combine (a >= 2)
 // V vertices per CTA: their A' and N'' rows are staged in shared memory
 // TRANSPOSED (column-major over the tile's vertices), so one 16-byte load
@@ -355,6 +368,14 @@ int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *
   if (n == 0) return 0;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   k_color<<<grid, 256, 0, s>>>(orig, n, seed, k, out);
+  return 1;
+}
+
+int launch_permute_colors(const uint8_t *by_orig, const int32_t *orig, int64_t n, int k, uint8_t *out, unsigned *bad,
+                          cudaStream_t s) {
+  if (n == 0) return 0;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_permute_colors<<<grid, 256, 0, s>>>(by_orig, orig, n, k, out, bad);
   return 1;
 }
 

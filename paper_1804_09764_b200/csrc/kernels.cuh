@@ -80,6 +80,9 @@ struct GatherArgs {
 };
 
 int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *out, cudaStream_t s);
+// out[i] = by_orig[orig[i]] for i < n; *bad |= 1 if a colour is >= k.
+int launch_permute_colors(const uint8_t *by_orig, const int32_t *orig, int64_t n, int k, uint8_t *out, unsigned *bad,
+                          cudaStream_t s);
 // Colour-sort every item's neighbour range (stable) into col_out and record
 // the 16 cumulative colour-group offsets of the item.
 int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
