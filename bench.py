@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--precision", default=None, help="fp32 | fp64 (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--chunk-cols", type=int, default=0)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: colouring replicas (each GPU the whole graph, different colourings; SURVEY F1) "
+                         "instead of the 1D vertex partition")
     ap.add_argument("--segment-len", type=int, default=0)
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,8 +201,8 @@ def run_ours(args, cfg, rank, world, dist):
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     g = cfg.graph()
-    kw = dict(precision=cc.CC_FP64 if precision == "fp64" else cc.CC_FP32, chunk_cols=args.chunk_cols,
-              segment_len=args.segment_len)
+    kw = dict(precision=cc.CC_FP64 if precision == "fp64" else cc.CC_FP32, segment_len=args.segment_len,
+              replicas=1 if (args.replicas and world > 1) else 0)
     if world > 1:
         opt, _idbuf = cc.distributed_options(**kw)
     else:
@@ -286,10 +288,11 @@ def run_ours(args, cfg, rank, world, dist):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32" if precision == "fp32" else "f64",
+                "scaling": "strong" if (world > 1 and not args.replicas) else "weak", "vs_baseline": None, "dtype": "f32" if precision == "fp32" else "f64",
                 "data": "synthetic",
                 "config": {"workload": f"configs[{cfg.idx}] {cfg.name}", "n": g.n, "adjacency": g.nnz,
-                           "k": cfg.k, "precision": precision, "parallelism": f"1d-vertex-partition x{world}",
+                           "k": cfg.k, "precision": precision, "parallelism": (f"colouring-replicas x{world}" if args.replicas and world > 1
+                                                           else f"1d-vertex-partition x{world}"),
                            "l2": "tables of several GB per step >> 126 MB L2 (no flush needed)"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak if achieved else None, "traffic": traffic,

@@ -75,14 +75,18 @@ typedef struct {
   const void *nccl_id;   /* 128-byte ncclUniqueId when world > 1 (from rank 0's
                             cc_nccl_unique_id, broadcast by the caller); ignored
                             when world == 1 */
-  int64_t chunk_cols;    /* column-chunk width of the aggregation (count-table
-                            columns per pass; PAPER.md lines 72, 391-396
-                            "intermediate data partitioning"); 0 = auto */
+  int64_t chunk_cols;    /* reserved, must be 0: column chunking is internal --
+                            the gathers walk rows in passes of 32 x NV x VW
+                            columns, the combine stages split-table slices, and
+                            the fused root keeps the widest neighbour sum out
+                            of HBM ("intermediate
+                            data partitioning"); CC_ERR_ARG otherwise */
   int32_t segment_len;   /* neighbour-list task size s: neighbour lists longer
                             than this are split into segments of at most s
                             neighbours (Alg. 4); 0 = auto */
-  int32_t use_graphs;    /* 1 = capture the per-colouring launch sequence in a
-                            CUDA graph and replay it; 0 = plain launches */
+  int32_t use_graphs;    /* reserved, must be 0 or 1, no effect: a colouring
+                            is ~12 launches of >= 1 ms each on configs[2-4],
+                            not launch-bound */
   uint64_t relabel_seed; /* seed of the internal vertex permutation used to
                             balance the partition ("randomly
                             partitioned"); never changes results */
@@ -90,10 +94,17 @@ typedef struct {
                             minimising modelled bytes (the
                             root "can be picked arbitrarily"); 1 = root at the
                             parent -1 vertex, children in index order */
+  int32_t replicas;      /* world > 1 only.  0 = 1D vertex partition (Alg. 2);
+                            1 = colouring replicas (the
+                            outer loop over colourings is parallel): every rank
+                            keeps the whole graph, cc_count_colorful counts
+                            locally (no exchange), and cc_estimate /
+                            cc_estimate_mom run iteration j on rank j mod world
+                            and all-reduce the per-iteration counts */
 } cc_options;
 
 /* Fill *opt with defaults: CC_FP64, device 0, world 1, rank 0, auto sizes,
- * CUDA graphs on, relabel_seed 0x5eed. */
+ * relabel_seed 0x5eed, planner-chosen root, 1D partition (replicas 0). */
 cc_status cc_default_options(cc_options *opt);
 
 /* Rank 0 only: write a fresh 128-byte ncclUniqueId to out128 (host).

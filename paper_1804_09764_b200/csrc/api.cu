@@ -82,7 +82,7 @@ cc_status cc_default_options(cc_options *opt) {
   std::memset(opt, 0, sizeof(*opt));
   opt->precision = CC_FP64;
   opt->world = 1;
-  opt->use_graphs = 1;
+  opt->use_graphs = 0;
   opt->relabel_seed = 0x5eed;
   return CC_OK;
 }
@@ -103,7 +103,8 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   if (opt->precision != CC_FP64 && opt->precision != CC_FP32) return CC_ERR_ARG;
   if (opt->world < 1 || opt->world > 64 || opt->rank < 0 || opt->rank >= opt->world) return CC_ERR_ARG;
   if (opt->world > 1 && !opt->nccl_id) return CC_ERR_ARG;
-  if (opt->chunk_cols < 0 || opt->segment_len < 0) return CC_ERR_ARG;
+  if (opt->chunk_cols != 0 || opt->segment_len < 0 || opt->use_graphs < 0 || opt->use_graphs > 1) return CC_ERR_ARG;
+  if (opt->replicas < 0 || opt->replicas > 1) return CC_ERR_ARG;
   std::unique_ptr<cc_ctx> c(new cc_ctx());
   c->opt = *opt;
   c->opt.nccl_id = nullptr;
@@ -211,7 +212,7 @@ cc_status cc_set_colors(cc_ctx *c, const uint8_t *colors) {
 cc_status cc_get_colors(cc_ctx *c, uint8_t *colors) {
   API_BEGIN(c)
   if (!c->has_colors) throw Error(CC_ERR_STATE, "no colouring");
-  if (c->opt.world != 1) throw Error(CC_ERR_STATE, "cc_get_colors needs world == 1");
+  if (c->pworld() != 1) throw Error(CC_ERR_STATE, "cc_get_colors needs the whole graph on this rank");
   std::vector<uint8_t> h((size_t)c->n_crow);
   if (!h.empty()) CUDA_OK(cudaMemcpy(h.data(), c->d_colors, h.size(), cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < c->part.n_own; ++i) colors[c->part.own_orig[i]] = h[i];
@@ -232,13 +233,9 @@ cc_status cc_estimate(cc_ctx *c, int32_t iterations, uint64_t seed0, double *est
   API_BEGIN(c)
   if (iterations < 1 || !estimate) throw Error(CC_ERR_ARG, "iterations >= 1 and estimate != NULL required");
   if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_estimate needs a graph and a template");
+  const std::vector<double> xs = cc::run_iterations(c, iterations, seed0);
   long double mean = 0;
-  std::vector<double> xs((size_t)iterations);
-  for (int j = 0; j < iterations; ++j) {
-    cc::launch_colouring(c, seed0 + (uint64_t)j);
-    cc::run_count(c, &xs[j], -1, nullptr, nullptr);
-    mean += xs[j];
-  }
+  for (double x : xs) mean += x;
   mean /= iterations;
   long double scale = 1;  // k^k / k!
   for (int i = 1; i <= c->plan.k; ++i) scale *= (long double)c->plan.k / i;
@@ -253,11 +250,7 @@ cc_status cc_estimate_mom(cc_ctx *c, int32_t iterations, uint64_t seed0, int32_t
   if (iterations < 1 || groups < 1 || groups > iterations || !estimate)
     throw Error(CC_ERR_ARG, "need 1 <= groups <= iterations and estimate != NULL");
   if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_estimate_mom needs a graph and a template");
-  std::vector<double> xs((size_t)iterations);
-  for (int j = 0; j < iterations; ++j) {
-    cc::launch_colouring(c, seed0 + (uint64_t)j);
-    cc::run_count(c, &xs[j], -1, nullptr, nullptr);
-  }
+  const std::vector<double> xs = cc::run_iterations(c, iterations, seed0);
   const cc_status st = cc_median_of_means(xs.data(), iterations, c->plan.k, c->plan.aut, groups, estimate);
   if (st != CC_OK) throw Error(st, "median of means");
   if (per_iter) std::copy(xs.begin(), xs.end(), per_iter);
@@ -276,7 +269,7 @@ cc_status cc_template_info(cc_ctx *c, int64_t *aut, int64_t *aut_root, int32_t *
 cc_status cc_get_subtree_counts(cc_ctx *c, int32_t x, double *out) {
   API_BEGIN(c)
   if (!c->has_graph || !c->has_template || !c->has_colors) throw Error(CC_ERR_STATE, "needs graph, template, colouring");
-  if (c->opt.world != 1) throw Error(CC_ERR_STATE, "cc_get_subtree_counts needs world == 1");
+  if (c->pworld() != 1) throw Error(CC_ERR_STATE, "cc_get_subtree_counts needs the whole graph on this rank");
   if (x < 0 || x >= c->plan.k || !out) throw Error(CC_ERR_ARG, "bad template vertex or NULL output");
   // tables are defined for the user's rooting: plan with the fixed root for
   // this call, restore the cost-model plan afterwards
@@ -332,7 +325,7 @@ cc_status cc_get_subtree_counts(cc_ctx *c, int32_t x, double *out) {
 cc_status cc_get_subtree_rows(cc_ctx *c, int32_t x, const int32_t *vertices, int32_t nv, double *out) {
   API_BEGIN(c)
   if (!c->has_graph || !c->has_template || !c->has_colors) throw Error(CC_ERR_STATE, "needs graph, template, colouring");
-  if (c->opt.world != 1) throw Error(CC_ERR_STATE, "cc_get_subtree_rows needs world == 1");
+  if (c->pworld() != 1) throw Error(CC_ERR_STATE, "cc_get_subtree_rows needs the whole graph on this rank");
   if (x < 0 || x >= c->plan.k || nv < 0 || (nv && (!vertices || !out)))
     throw Error(CC_ERR_ARG, "bad template vertex, count or NULL pointer");
   struct Restore {

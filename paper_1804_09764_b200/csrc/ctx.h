@@ -119,6 +119,8 @@ struct cc_ctx {
   size_t cur_bytes = 0, peak_bytes = 0;
 
   int elem() const { return opt.precision == CC_FP64 ? 8 : 4; }
+  // ranks of the 1D vertex partition (1 in replica mode: each rank has the whole graph)
+  int pworld() const { return opt.replicas ? 1 : opt.world; }
   int64_t ld_of(int64_t W) const {
     const int64_t m = 32 / elem();
     return (std::max<int64_t>(W, 1) + m - 1) / m * m;
@@ -206,4 +208,7 @@ void launch_colouring(cc_ctx *c, uint64_t seed);
 // that produces the table; nothing else changes).
 void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out,
                const std::vector<int64_t> *dump_rows = nullptr);
+// X_j for colourings seed0 + j, j < iterations (replica mode with world > 1:
+// iteration j on rank j mod world, then one all-reduce of the vector).
+std::vector<double> run_iterations(cc_ctx *c, int iterations, uint64_t seed0);
 }  // namespace cc

@@ -83,7 +83,7 @@ struct Bufs {
 }  // namespace
 
 void load_graph(cc_ctx *c, const HostGraph &g) {
-  c->part = partition_graph(g, c->opt.world, c->opt.rank, c->opt.relabel_seed);
+  c->part = partition_graph(g, c->pworld(), c->pworld() == 1 ? 0 : c->opt.rank, c->opt.relabel_seed);
   const auto &R = c->part;
   c->n_global = g.n;
   c->n_own = R.n_own;
@@ -104,7 +104,7 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
   build_pass(c, beg, end, false, c->p_full);
   c->p_full.beg = c->d_rp;
   c->p_full.end = c->d_rp + 1;
-  if (c->opt.world > 1) {
+  if (c->pworld() > 1) {
     c->d_mid = c->pupload(R.mid);
     c->d_send_idx = c->pupload(R.send_idx);
     build_pass(c, beg, R.mid, false, c->p_local);
@@ -250,7 +250,7 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
 }
 
 void aggregate(cc_ctx *c, void *P, int p, void *N) {
-  if (c->opt.world == 1) {
+  if (c->pworld() == 1) {
     gather_pass(c, c->p_full, P, p, N, 0);
     return;
   }
@@ -263,7 +263,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   CUDA_OK(cudaEventRecord(ready, c->s_main));
   CUDA_OK(cudaStreamWaitEvent(c->s_comm, ready, 0));
   const auto &R = c->part;
-  const int64_t send_rows = R.send_off[c->opt.world];
+  const int64_t send_rows = R.send_off[c->pworld()];
   const size_t sbytes = (size_t)send_rows * ld * elem;
   void *sendbuf = send_rows ? c->amalloc(sbytes, c->s_comm) : nullptr;
   cudaEvent_t xb = c->begin(c->s_comm);
@@ -271,7 +271,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   c->check_launch();
   const ncclDataType_t dt = elem == 8 ? ncclFloat64 : ncclFloat32;
   NCCL_OK(api.GroupStart());
-  for (int q = 0; q < c->opt.world; ++q) {
+  for (int q = 0; q < c->pworld(); ++q) {
     if (q == c->opt.rank) continue;
     const int64_t ns = R.send_off[q + 1] - R.send_off[q];
     const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
@@ -314,7 +314,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
 
   // world > 1: colour-sort the neighbour ranges of both passes (once per
   // colouring); world 1 sorts below, fused with the leaf level (hist)
-  if (c->opt.world > 1 && !c->sorted_valid) {
+  if (c->pworld() > 1 && !c->sorted_valid) {
     cudaEvent_t b = c->begin(c->s_main);
     csort(c, c->p_local);
     csort(c, c->p_remote);
@@ -333,7 +333,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   {
     const Step &rs = pl.steps[sr];
     const char *f = getenv("CC_FUSED_ROOT");
-    if (c->opt.world == 1 && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
+    if (c->pworld() == 1 && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
       const int P = rs.passive;
       int s_l = -1, users = 0;
       for (int s = 0; s < sr; ++s) {
@@ -361,7 +361,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     if (pl.steps[s].p == 1) last_hist_use = s;
   double *per_vertex = nullptr;
   if (root_out || fuse) per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
-  if (c->opt.world == 1) {  // colour sort + leaf level N''(v, {y}) in one pass over the adjacency
+  if (c->pworld() == 1) {  // colour sort + leaf level N''(v, {y}) in one pass over the adjacency
     if (last_hist_use >= 0) hist = bufs.make((size_t)rows * c->ld_of(k - 1) * elem);
     cudaEvent_t b = c->begin(c->s_main);
     Pass &p = c->p_full;
@@ -469,7 +469,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       }
     }
   }
-  if (c->opt.world > 1) {
+  if (c->pworld() > 1) {
     cudaEvent_t b = c->begin(c->s_main);
     NCCL_OK(nccl().AllReduce(c->d_result, c->d_result, 1, ncclFloat64, ncclSum, c->comm, c->s_main));
     c->end(PH_EXCHANGE, c->s_main, b);
@@ -502,7 +502,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     c->afree(pv, (size_t)std::max<int64_t>(n, 1) * 8, c->s_main);
   }
   CUDA_OK(cudaStreamSynchronize(c->s_main));
-  if (c->opt.world > 1) CUDA_OK(cudaStreamSynchronize(c->s_comm));
+  if (c->pworld() > 1) CUDA_OK(cudaStreamSynchronize(c->s_comm));
   float ms = 0;
   CUDA_OK(cudaEventElapsedTime(&ms, t0, t1));
   c->prof[0] = ms;
@@ -522,6 +522,29 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   c->stats[4] = (double)c->peak_bytes;
   if (!std::isfinite(host_x)) throw Error(CC_ERR_NONFINITE, "colourful count is not finite (fp32 table overflow?)");
   *X = host_x;
+}
+
+}  // namespace cc
+
+namespace cc {
+
+std::vector<double> run_iterations(cc_ctx *c, int iterations, uint64_t seed0) {
+  std::vector<double> xs((size_t)iterations, 0.0);
+  const bool rep = c->opt.replicas && c->opt.world > 1;
+  for (int j = 0; j < iterations; ++j) {
+    if (rep && j % c->opt.world != c->opt.rank) continue;
+    launch_colouring(c, seed0 + (uint64_t)j);
+    run_count(c, &xs[j], -1, nullptr, nullptr);
+  }
+  if (rep) {  // every rank ends with every X_j (the others' entries are 0 here)
+    double *d = static_cast<double *>(c->amalloc((size_t)iterations * 8, c->s_main));
+    CUDA_OK(cudaMemcpyAsync(d, xs.data(), (size_t)iterations * 8, cudaMemcpyHostToDevice, c->s_main));
+    NCCL_OK(nccl().AllReduce(d, d, (size_t)iterations, ncclFloat64, ncclSum, c->comm, c->s_main));
+    CUDA_OK(cudaMemcpyAsync(xs.data(), d, (size_t)iterations * 8, cudaMemcpyDeviceToHost, c->s_main));
+    c->afree(reinterpret_cast<void *&>(d), (size_t)iterations * 8, c->s_main);
+    CUDA_OK(cudaStreamSynchronize(c->s_main));
+  }
+  return xs;
 }
 
 }  // namespace cc

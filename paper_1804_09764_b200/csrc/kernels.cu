@@ -153,12 +153,15 @@ struct LaneVec<double, 2> {
 // tile sits at [c][v / V][v % V] with a row stride of 33 vectors, so a lane
 // reads its V vertices of column c with one conflict-free V-wide LDS and one
 // address computation serves V FMAs.
-template <typename T, int OUT, int V, bool SS>
+// One launch covers the output colour sets [o0, o0 + WOc): the split table
+// slice of those outputs is staged in shared memory (wide steps whose whole
+// table does not fit run several launches, re-staging the tiles).
+template <typename T, int OUT, int V>
 __global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A, int64_t ldA, int WA,
                                                          const T *__restrict__ N, int64_t ldN, int WN,
                                                          const uint32_t *__restrict__ split, int nq, int64_t n,
-                                                         T *__restrict__ out, int64_t ldO, int WO, int nbuf,
-                                                         int split_smem) {
+                                                         T *__restrict__ out, int64_t ldO, int WO, int nbuf, int o0,
+                                                         int WOc) {
   constexpr int S = 33;       // row stride in V-vectors
   constexpr int TV = 32 * V;  // vertices per tile
   using LV = typename LaneVec<T, V>::type;
@@ -167,11 +170,14 @@ __global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A
   const int W = WA + WN;
   const size_t bstride = ((size_t)S * V * W * sizeof(T) + 15) / 16 * 16 / sizeof(T);  // 16-byte aligned buffers
   T *bufs = reinterpret_cast<T *>(smem_raw);  // nbuf x [W][33][V]: A' columns then N'' columns
-  const int WOp = (WO + 7) & ~7;
-  // split table: shared memory (SS) or read-only global (L1-resident)
+  const int WOp = (WO + 7) & ~7, WOcp = (WOc + 7) & ~7;
+  const int o_end = min(WO, o0 + WOc);
+  // the split-table slice [q][WOcp] of this launch's outputs, in shared memory
   uint32_t *ss = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * bstride);
-  if constexpr (SS)
-    for (int i = threadIdx.x; i < nq * WOp; i += blockDim.x) ss[i] = split[i];
+  for (int i = threadIdx.x; i < nq * WOcp; i += blockDim.x) {
+    const int q = i / WOcp, o = o0 + i - q * WOcp;
+    ss[i] = o < WOp ? split[(int64_t)q * WOp + o] : 0u;
+  }
   const int64_t ntiles = (n + TV - 1) / TV;
   auto stage = [&](int64_t tile, T *b) {
     const int64_t v0 = tile * TV;
@@ -202,19 +208,19 @@ __global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A
     const char *Nb = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + (size_t)WA * S + lane);
     constexpr uint32_t CB = S * sizeof(LV);  // bytes per staged column
     const int64_t vb = tile * TV + (int64_t)lane * V;
-    for (int g = warp; g < (WO + OUT - 1) / OUT; g += nwarp) {
+    for (int g = warp; g < (WOc + OUT - 1) / OUT; g += nwarp) {
       T acc[OUT][V];
 #pragma unroll
       for (int j = 0; j < OUT; ++j)
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[j][i] = (T)0;
-      const uint4 *e = reinterpret_cast<const uint4 *>(SS ? ss : split) + (OUT / 4) * g;
+      const uint4 *e = reinterpret_cast<const uint4 *>(ss) + (OUT / 4) * g;
 #pragma unroll 2
       for (int q = 0; q < nq; ++q) {
         uint32_t xy[OUT];
 #pragma unroll
         for (int h = 0; h < OUT / 4; ++h) {
-          const uint4 eh = SS ? e[q * (WOp / 4) + h] : __ldg(e + (int64_t)q * (WOp / 4) + h);
+          const uint4 eh = e[q * (WOcp / 4) + h];
           xy[4 * h + 0] = eh.x;
           xy[4 * h + 1] = eh.y;
           xy[4 * h + 2] = eh.z;
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A
         if (vb + i < n) {
 #pragma unroll
           for (int j = 0; j < OUT; ++j)
-            if (OUT * g + j < WO) out[(vb + i) * ldO + OUT * g + j] = acc[j][i];
+            if (o0 + OUT * g + j < o_end) out[(vb + i) * ldO + o0 + OUT * g + j] = acc[j][i];
         }
     }
     __syncthreads();  // the buffer is refilled two tiles later (or next tile when single-buffered)
@@ -314,17 +320,23 @@ void combine_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, 
 }
 
 template <typename T>
-void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
+int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
                    int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
   const char *impl = getenv("CC_COMBINE_IMPL");  // "tile": V-tile kernel; default: lane-per-vertex
   const size_t split_bytes = (size_t)nq * ((WO + 7) & ~7) * 4;
   const size_t cap = 227 * 1024;
-  // V = 2 vertices per lane (one address per 2 FMAs) when a single buffer of
-  // 64-vertex tiles plus the split table fits; else V = 1, double-buffered
+  // V = 2 vertices per lane (one address per 2 FMAs, single-buffered
+  // 64-vertex tiles) when that tile plus the whole split table fits; else
+  // V = 1 double-buffered with the whole table; else V = 1 single-buffered
+  // with the outputs in chunks whose table slices fit (configs[4]'s (7;4,3)).
   const int vpref = env_int("CC_COMBINE_V", 2);
   const size_t tile2 = ((size_t)(WA + WN) * 33 * 2 * sizeof(T) + 15) / 16 * 16;
   const size_t tile1 = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
-  const int V = (vpref == 2 && tile2 + split_bytes <= cap) ? 2 : 1;
+  int V = 1, nbuf = 1, chunk = WO;
+  if (vpref == 2 && tile2 + split_bytes <= cap) V = 2;
+  else if (2 * tile1 + split_bytes <= cap) nbuf = 2;
+  else if (tile1 + (size_t)nq * 4 * 64 <= cap) chunk = (int)((cap - tile1) / ((size_t)nq * 4) / 8 * 8);
+  else chunk = 0;  // even 64 outputs do not fit: V-tile kernel
   const size_t tile_bytes = V == 2 ? tile2 : tile1;
   // the lane kernel pays a staging pass per tile: it wins only when the
   // split walk does enough FMAs per staged entry (measured: (9;6,3) of
@@ -332,32 +344,32 @@ void combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ld
   // at 2.1 lose)
   const double intensity = (double)WO * nq / (double)(WA + WN + WO);
   const bool lane_ok = impl ? impl[0] != 't' : intensity >= 8.0;
-  if (lane_ok && tile_bytes <= cap) {
-    const int nbuf = V == 1 && 2 * tile_bytes <= cap ? 2 : 1;
-    const int split_smem = nbuf * tile_bytes + split_bytes <= cap ? 1 : 0;
-    const size_t smem = nbuf * tile_bytes + (split_smem ? split_bytes : 0);
+  if (lane_ok && chunk > 0) {
+    const int WOcp = (std::min(chunk, WO) + 7) & ~7;
+    const size_t smem = nbuf * tile_bytes + (size_t)nq * WOcp * 4;
     // 16 warps; output groups of 4 or 8 colour sets, whichever balances the warps better
-    const int r8 = ((WO + 7) / 8 + 15) / 16, r4 = ((WO + 3) / 4 + 15) / 16;
+    const int r8 = ((WOcp + 7) / 8 + 15) / 16, r4 = ((WOcp + 3) / 4 + 15) / 16;
     const bool o8 = 2 * r8 <= r4;
-    auto kern = V == 2 ? (split_smem ? (o8 ? k_combine_lane<T, 8, 2, true> : k_combine_lane<T, 4, 2, true>)
-                                     : (o8 ? k_combine_lane<T, 8, 2, false> : k_combine_lane<T, 4, 2, false>))
-                       : (split_smem ? (o8 ? k_combine_lane<T, 8, 1, true> : k_combine_lane<T, 4, 1, true>)
-                                     : (o8 ? k_combine_lane<T, 8, 1, false> : k_combine_lane<T, 4, 1, false>));
+    auto kern = V == 2 ? (o8 ? k_combine_lane<T, 8, 2> : k_combine_lane<T, 4, 2>)
+                       : (o8 ? k_combine_lane<T, 8, 1> : k_combine_lane<T, 4, 1>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = persistent_grid(kern, 512, smem, num_sms);
-    kern<<<grid, 512, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq, n,
-                                 static_cast<T *>(out), ldO, WO, nbuf, split_smem);
-    return;
+    int launches = 0;
+    for (int o0 = 0; o0 < WO; o0 += chunk, ++launches)
+      kern<<<grid, 512, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq,
+                                   n, static_cast<T *>(out), ldO, WO, nbuf, o0, std::min(chunk, WO - o0));
+    return launches;
   }
   // wide rows: tile of V vertices (padded rows); k <= 16 bounds a row by
   // 2 x C(15,7) entries, so the smallest tile always fits in 227 KB
   const size_t row = (size_t)(WA + WN) * sizeof(T);
   const size_t budget = 100 * 1024;
-  if (row * 20 <= budget) combine_go<T, 16>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  else if (row * 12 <= budget) combine_go<T, 8>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  if (row * 20 <= budget) { combine_go<T, 16>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s); return 1; }
+  else if (row * 12 <= budget) { combine_go<T, 8>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s); return 1; }
   else if (sizeof(T) == 4 || row * 6 <= 220 * 1024)
     combine_go<T, 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
   else combine_go<T, sizeof(T) == 8 ? 2 : 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  return 1;
 }
 
 }  // namespace
@@ -383,9 +395,8 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms,
                    cudaStream_t s) {
   if (n == 0) return 0;
-  if (elem == 8) combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  else combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  return 1;
+  if (elem == 8) return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  return combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
 }
 
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, const uint16_t *comp,

@@ -1,0 +1,7 @@
+# chunked split-table combine: parity (twins of config 4 use it), config 4 + config 3 timing
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -q -x 2>&1 | tail -2
+timeout 900 python scripts/agg_sweep.py --config 3 --check --envs "CC_COMBINE_IMPL=lane,tile" 2>&1 | tail -2
+timeout 1500 python bench.py --config 4 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_c4d.log 2>&1; echo c4 rc=$?
+python -c "import json;d=json.loads(open('gpurun_out/bench_c4d.log').read().strip().splitlines()[-1]);print(d['ms_per_step'], d['phase_ms'], d['peak_table_bytes'])"
+timeout 1800 python -m pytest tests/test_gpu_config4.py -m gpu -q -x 2>&1 | tail -2
