@@ -278,20 +278,32 @@ __global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ beg, c
 // ------------------------------------------------------------------ shared epilogue
 // Write the item's N'' row (light vertex) or its partial (heavy segment; the
 // last arriving segment of the vertex sums all partials in segment order).
-template <typename T, int G>
-__device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const double *sacc, int64_t it, int32_t v,
+// fp32 shared-memory N'' rows hold value x 2^-64 (an exact power-of-two
+// scale): integer counts up to 6e57 stay in range (configs[4]'s root row
+// reaches ~1e38 unscaled) and 1 stays a normal number.
+template <typename AccT>
+struct AccScale {
+  static constexpr double in = 1.0, out = 1.0;
+};
+template <>
+struct AccScale<float> {
+  static constexpr double in = 0x1p-64, out = 0x1p64;
+};
+
+template <typename T, int G, typename AccT = double>
+__device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const AccT *sacc, int64_t it, int32_t v,
                                                 bool heavy, int lane, unsigned gmask) {
   T *drow = static_cast<T *>(a.dst) + (int64_t)v * a.ld_dst;
   if (!heavy) {
     for (int j = lane; j < a.W_out; j += G) {
-      double x = sacc[j];
+      double x = (double)sacc[j] * AccScale<AccT>::out;
       if (a.accumulate) x += (double)drow[j];
       drow[j] = (T)x;
     }
     return;
   }
   double *sp = a.scratch + it * a.ld_scratch;
-  for (int j = lane; j < a.W_out; j += G) sp[j] = sacc[j];
+  for (int j = lane; j < a.W_out; j += G) sp[j] = (double)sacc[j] * AccScale<AccT>::out;
   __threadfence();
   __syncwarp(gmask);
   const int32_t hv = a.work.seg_hv[it];
@@ -313,12 +325,12 @@ __device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const doubl
 // Fused root epilogue (root_mode 1 / 2): X_v = sum_{X'} A'(v, X') N''(v, comp X')
 // in fp64, written to per_vertex[v]; a heavy vertex's segments are first
 // summed (in segment order) by the last arriving segment.
-template <typename T>
-__device__ __forceinline__ void root_epilogue(const GatherArgs &a, double *sacc, int64_t it, int32_t v, bool heavy,
+template <typename T, typename AccT = double>
+__device__ __forceinline__ void root_epilogue(const GatherArgs &a, AccT *sacc, int64_t it, int32_t v, bool heavy,
                                               int lane) {
   if (heavy) {
     double *sp = a.scratch + it * a.ld_scratch;
-    for (int j = lane; j < a.W_out; j += 32) sp[j] = sacc[j];
+    for (int j = lane; j < a.W_out; j += 32) sp[j] = (double)sacc[j] * AccScale<AccT>::out;
     __threadfence();
     __syncwarp();
     const int32_t hv = a.work.seg_hv[it];
@@ -331,16 +343,17 @@ __device__ __forceinline__ void root_epilogue(const GatherArgs &a, double *sacc,
     for (int j = lane; j < a.W_out; j += 32) {
       double x = 0.0;
       for (int s = 0; s < ns; ++s) x += __ldcg(a.scratch + (int64_t)(s0 + s) * a.ld_scratch + j);
-      sacc[j] = x;
+      sacc[j] = (AccT)(x * AccScale<AccT>::in);
     }
     __syncwarp();
   }
   double d = 0.0;
   if (a.root_mode == 2) {
-    for (int x = lane; x < a.WA; x += 32) d += sacc[x] * sacc[__ldg(a.comp + x)];
+    for (int x = lane; x < a.WA; x += 32)
+      d += ((double)sacc[x] * AccScale<AccT>::out) * ((double)sacc[__ldg(a.comp + x)] * AccScale<AccT>::out);
   } else {
     const T *ar = static_cast<const T *>(a.rA) + (int64_t)v * a.ldA;
-    for (int x = lane; x < a.WA; x += 32) d += (double)ar[x] * sacc[__ldg(a.comp + x)];
+    for (int x = lane; x < a.WA; x += 32) d += (double)ar[x] * ((double)sacc[__ldg(a.comp + x)] * AccScale<AccT>::out);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
@@ -549,14 +562,14 @@ __device__ __forceinline__ void load_desc(const GatherArgs &a, int64_t it, int l
   go = lane < 16 ? (int)__ldg(a.goff + it * 16 + lane) : 0;
 }
 
-template <typename T, int NV, int U>
+template <typename T, int NV, int U, typename AccT = double>
 __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = 32 * NV * VW;  // columns per pass
-  extern __shared__ double sacc_ldg[];
+  extern __shared__ __align__(16) unsigned char sacc_raw[];
   const int lane = threadIdx.x & 31;
-  double *sacc = sacc_ldg + (threadIdx.x >> 5) * (int64_t)a.W_out;
+  AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)a.W_out;
   const int64_t n_items = a.work.n_seg + a.work.n_light;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const char *__restrict__ srcb = static_cast<const char *>(a.src);
@@ -667,14 +680,14 @@ __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
                                  (double)vec_at(blk[j], 3 % VW)};
 #pragma unroll
             for (int q = 0; q < VW; ++q)
-              if (m[j][q] != 0xFFFF) sacc[m[j][q]] += e[q];
+              if (m[j][q] != 0xFFFF) sacc[m[j][q]] += (AccT)(e[q] * AccScale<AccT>::in);
           }
         }
         __syncwarp();  // groups of different colours may map to the same N'' entries
       }
     }
-    if (a.root_mode) root_epilogue<T>(a, sacc, it, v, heavy, lane);
-    else gather_epilogue<T, 32>(a, sacc, it, v, heavy, lane, 0xffffffffu);
+    if (a.root_mode) root_epilogue<T, AccT>(a, sacc, it, v, heavy, lane);
+    else gather_epilogue<T, 32, AccT>(a, sacc, it, v, heavy, lane, 0xffffffffu);
     __syncwarp();
   }
 }
@@ -683,8 +696,12 @@ template <typename T, int NV, int U>
 void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = 32 * NV * VW;
-  auto kern = k_gather_ldg<T, NV, U>;
-  const size_t row = (size_t)a.W_out * sizeof(double);
+  // fp32 tables with N'' rows wider than 1600 entries (configs[4]'s root:
+  // 3432) keep the shared-memory row in fp32 so that 16 warps fit per SM
+  // (each entry adds at most k-1 colour-group block sums; C-6)
+  const bool acc32 = sizeof(T) == 4 && a.W_out > 1600;
+  auto kern = acc32 ? k_gather_ldg<T, NV, U, float> : k_gather_ldg<T, NV, U, double>;
+  const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
   const int threads = warps * 32;

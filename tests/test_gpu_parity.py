@@ -146,6 +146,35 @@ def test_fused_root_exact(parent, mode, monkeypatch):
             assert rel_err(cc.cc_count_colorful(ctx), float(want.total)) <= TOL_FP32
 
 
+def test_subtree_rows_match_the_full_dump_and_the_oracle():
+    """cc_get_subtree_rows (the sampled-row hook used at configs[4] scale)
+    returns the same rows as the full-table dump and the oracle, including
+    isolated vertices (zero rows) and the root column."""
+    cc = lib()
+    cfg = synth.scaled_twin(synth.CONFIGS[4], 10, 16)
+    g0 = cfg.graph()
+    g = synth.from_edges(g0.n + 3, np.stack(g0.edges(), axis=1))  # + 3 isolated vertices
+    k = cfg.k
+    col = oracle.color(g.n, k, 9)
+    rng = np.random.default_rng(4)
+    verts = np.concatenate([rng.choice(g0.n, 12, replace=False), [g.n - 1, g.n - 2]]).astype(np.int32)
+    sizes = subtree_sizes(cfg.parent)
+    with context(g, cfg.parent) as ctx:
+        cc.cc_set_colors(ctx, col)
+        got = {}
+        for x in (1, 3, 7):  # B7, B3 and a leaf
+            got[x] = rows = cc.cc_get_subtree_rows(ctx, x, verts, k, sizes[x])
+            full = cc.cc_get_subtree_counts(ctx, x, g.n, k, sizes[x])
+            assert np.array_equal(rows, full[verts]), x
+            ref = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE, keep_x=x).table
+            assert_close_entries(rows, ref[verts], TOL_FP64, f"rows x={x}")
+        root = cc.cc_get_subtree_rows(ctx, 0, verts, k, k)
+        want = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE, want_root=True).root
+        assert_close_entries(root[:, 0], want[verts], TOL_FP64, "root rows")
+        assert np.all(got[1][-2:] == 0) and np.all(got[3][-2:] == 0)  # isolated: no tree of >= 2 vertices
+        assert np.array_equal(got[7][-2:].sum(axis=1), [1.0, 1.0])  # ... but the single vertex maps
+
+
 # ------------------------------------------------------------------ configs[1]: fp64 1e-12 per entry, fp32 1e-4
 def test_config1_fp64_every_entry_and_fp32_total():
     cfg = synth.CONFIGS[1]
