@@ -248,6 +248,16 @@ uint32_t cc_colex_unrank(int32_t s, int64_t r);
  * available in out.  CC_ERR_ARG if too small. */
 cc_status cc_split_table(int32_t k, int32_t t, int32_t a, uint32_t *out, int64_t cap);
 
+/* The Z-block cover of a combine step (outputs of size ts, actives of size
+ * as, passives of size ts - as, in a K-colour universe) used by the
+ * register-blocked combine: *n_blocks blocks of *ld uint16 entries each --
+ * the colex ranks of the block's C(ts+1, as) active sets and C(ts+1, ts-as)
+ * passive sets (local colex order) and of its ts+1 outputs Z \ {z}
+ * (0xFFFF = owned by another block).  out may be NULL to query the sizes;
+ * CC_ERR_ARG if cap is too small. */
+cc_status cc_zblock_table(int32_t K, int32_t ts, int32_t as, uint16_t *out, int64_t cap, int32_t *n_blocks,
+                          int32_t *ld);
+
 /* Plan a template without a context.  steps_out receives, per step, 6 int32:
  * t, a, p, active table id (-1 = single vertex), passive table id (-1 = single
  * vertex), output table id (-1 = root).  Also |Aut(T)|, |Aut_rho(T)|, and

@@ -189,6 +189,14 @@ def cc_split_table(k: int, t: int, a: int) -> np.ndarray:
     return out.reshape(math.comb(t, a), math.comb(k, t))
 
 
+def cc_zblock_table(K: int, ts: int, as_: int) -> np.ndarray:
+    nb, ld = ctypes.c_int32(), ctypes.c_int32()
+    _check(None, _lib.cc_zblock_table(K, ts, as_, None, 0, ctypes.byref(nb), ctypes.byref(ld)))
+    out = np.zeros(nb.value * ld.value, dtype=np.uint16)
+    _check(None, _lib.cc_zblock_table(K, ts, as_, _p(out), out.size, ctypes.byref(nb), ctypes.byref(ld)))
+    return out.reshape(nb.value, ld.value)
+
+
 def cc_plan_template(parent) -> dict:
     par = np.ascontiguousarray(parent, dtype=np.int32)
     steps = np.zeros((64, 6), dtype=np.int32)

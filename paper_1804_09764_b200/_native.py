@@ -57,6 +57,7 @@ SIGNATURES = {
     "cc_colex_rank": (c_i64, [c_u32]),
     "cc_colex_unrank": (c_u32, [c_i32, c_i64]),
     "cc_split_table": (c_i32, [c_i32, c_i32, c_i32, vp, c_i64]),
+    "cc_zblock_table": (c_i32, [c_i32, c_i32, c_i32, vp, c_i64, vp, vp]),
     "cc_plan_template": (c_i32, [c_i32, vp, vp, c_i32, vp, vp, vp, vp, vp]),
     "cc_plan_template_auto": (c_i32, [c_i32, vp, c_dbl, c_i32, vp, c_i32, vp, vp, vp]),
     "cc_partition_plan":(c_i32, [c_i64, vp, vp, c_i32, c_i32, c_u64, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -51,6 +51,8 @@ void free_persistent(cc_ctx *c) {
   c->d_colors = nullptr;
   c->p_full = c->p_local = c->p_remote = cc::Pass();
   c->d_split.clear();
+  c->d_ztab.clear();
+  c->zblocks.clear();
   c->d_map.clear();
   c->d_comp = nullptr;
   c->d_partials = c->d_result = nullptr;
@@ -439,6 +441,20 @@ cc_status cc_split_table(int32_t k, int32_t t, int32_t a, uint32_t *out, int64_t
   auto tab = cc::split_table(k, t, a);
   if ((int64_t)tab.size() > cap) return CC_ERR_ARG;
   std::copy(tab.begin(), tab.end(), out);
+  return CC_OK;
+}
+
+cc_status cc_zblock_table(int32_t K, int32_t ts, int32_t as, uint16_t *out, int64_t cap, int32_t *n_blocks,
+                          int32_t *ld) {
+  if (K < 2 || K > cc::kMaxK || ts < 2 || ts >= K || as < 1 || as >= ts || !n_blocks || !ld) return CC_ERR_ARG;
+  int nb = 0;
+  auto tab = cc::zblock_table(K, ts, as, &nb);
+  *n_blocks = nb;
+  *ld = (int32_t)cc::zblock_ld(ts, as);
+  if (out) {
+    if ((int64_t)tab.size() > cap) return CC_ERR_ARG;
+    std::copy(tab.begin(), tab.end(), out);
+  }
   return CC_OK;
 }
 

@@ -105,3 +105,65 @@ std::vector<uint16_t> complement_table(int k, int a) {
 }
 
 }  // namespace cc
+
+namespace cc {
+
+// Z-block cover of a combine step (t'; a', p') in the K-colour universe
+// (see common.h).  Greedy: take the first uncovered output S in colex
+// order, extend it by the colour c that completes the most uncovered
+// outputs, and assign every uncovered S_z = Z \ {z} to that block.
+std::vector<uint16_t> zblock_table(int K, int ts, int as, int *n_blocks) {
+  const int zs = ts + 1, ps = ts - as;
+  const int64_t nS = binom(K, ts), na = binom(zs, as), nn = binom(zs, ps);
+  const int64_t ld = zblock_ld(ts, as);
+  std::vector<char> covered((size_t)nS, 0);
+  std::vector<uint16_t> out;
+  int nb = 0;
+  auto expand = [&](uint32_t Z, uint32_t local) {  // local subset of Z's positions -> global mask
+    uint32_t g = 0;
+    int pos = 0;
+    for (int c = 0; c < K; ++c)
+      if (Z >> c & 1u) {
+        if (local >> pos & 1u) g |= 1u << c;
+        ++pos;
+      }
+    return g;
+  };
+  for (int64_t r = 0; r < nS; ++r) {
+    if (covered[r]) continue;
+    const uint32_t S = colex_unrank(ts, r);
+    int best_c = -1, best = -1;
+    for (int c = 0; c < K; ++c) {
+      if (S >> c & 1u) continue;
+      const uint32_t Z = S | 1u << c;
+      int gain = 0;
+      for (int z = 0; z < K; ++z)
+        if (Z >> z & 1u) gain += !covered[colex_rank(Z & ~(1u << z))];
+      if (gain > best) {
+        best = gain;
+        best_c = c;
+      }
+    }
+    const uint32_t Z = S | 1u << best_c;
+    const size_t base = out.size();
+    out.resize(base + (size_t)ld, 0);
+    for (int64_t i = 0; i < na; ++i) out[base + i] = (uint16_t)colex_rank(expand(Z, colex_unrank(as, i)));
+    for (int64_t i = 0; i < nn; ++i) out[base + na + i] = (uint16_t)colex_rank(expand(Z, colex_unrank(ps, i)));
+    for (int zl = 0; zl < zs; ++zl) {  // output S_z = Z minus its zl-th element (local order)
+      const uint32_t Sz = expand(Z, ((1u << zs) - 1) & ~(1u << zl));
+      const int64_t rz = colex_rank(Sz);
+      out[base + na + nn + zl] = covered[rz] ? 0xFFFF : (uint16_t)rz;
+      covered[rz] = 1;
+    }
+    ++nb;
+  }
+  *n_blocks = nb;
+  return out;
+}
+
+int64_t zblock_ld(int ts, int as) {
+  const int zs = ts + 1;
+  return (binom(zs, as) + binom(zs, ts - as) + zs + 7) / 8 * 8;
+}
+
+}  // namespace cc

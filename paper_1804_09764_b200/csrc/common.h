@@ -43,6 +43,18 @@ uint32_t unsqueeze(uint32_t mask, int c);
 std::vector<uint16_t> gather_map(int k, int p);
 int64_t gather_map_ld(int k, int p);  // map row stride: C(k-1,p-1) rounded up to 8 (padding 0xFFFF)
 
+// Z-block cover of a combine step with outputs of size ts = t-1, actives of
+// size as = a-1 and passives of size ps = ts - as, in a K = k-1 colour
+// universe: every output set lies in some block Z of ts + 1 colours, and all
+// splits of all outputs inside Z use only the C(ts+1, as) active sets and
+// C(ts+1, ps) passive sets of Z (the combine keeps Z's passive values in
+// registers).  Per block, zblock_ld(ts, as) uint16 entries: the global colex
+// ranks of Z's active sets (local colex order), of its passive sets, and of
+// the output Z minus its z-th colour for each z (0xFFFF when another block
+// owns that output).  *n_blocks receives the block count.
+std::vector<uint16_t> zblock_table(int K, int ts, int as, int *n_blocks);
+int64_t zblock_ld(int ts, int as);
+
 // ---------------------------------------------------------------- plan.cpp
 // One DP step (t; a, p): T_out(v, S) = sum_{S1 u S2 = S} A(v, S1) N_P(v, S2),
 // N_P(v, S2) = sum_{u in N(v)} P(u, S2).  Table ids index Plan::tables;

@@ -96,6 +96,8 @@ struct cc_ctx {
   std::vector<int32_t> user_parent;  // the template as given (re-planned when the graph changes)
   cc::Plan plan;
   std::vector<uint32_t *> d_split;    // per step: split table (combine steps)
+  std::vector<uint16_t *> d_ztab;     // per step: Z-block cover table (nullptr if none)
+  std::vector<int> zblocks;
   std::vector<uint16_t *> d_map;      // per passive size p: gather map (p >= 2)
   uint16_t *d_comp = nullptr;         // root step complement table
   bool has_colors = false;

@@ -131,9 +131,12 @@ void replan(cc_ctx *c, bool fixed) {
 
 void upload_template(cc_ctx *c) {
   for (auto *p : c->d_split) c->pfree(p);
+  for (auto *p : c->d_ztab) c->pfree(p);
   for (auto *p : c->d_map) c->pfree(p);
   c->pfree(c->d_comp);
   c->d_split.assign(c->plan.steps.size(), nullptr);
+  c->d_ztab.assign(c->plan.steps.size(), nullptr);
+  c->zblocks.assign(c->plan.steps.size(), 0);
   c->d_map.assign(kMaxK + 1, nullptr);
   c->d_comp = nullptr;
   const int k = c->plan.k;
@@ -150,6 +153,12 @@ void upload_template(cc_ctx *c) {
       std::vector<uint32_t> pad((size_t)(nq * WOp), 0);
       for (int64_t q = 0; q < nq; ++q) std::copy(tab.begin() + q * WO, tab.begin() + (q + 1) * WO, pad.begin() + q * WOp);
       c->d_split[s] = c->pupload(pad);
+      if (dev::combine_z_supported(c->elem(), st.t - 1, st.a - 1)) {  // Z-block cover for the register-blocked combine
+        int nb = 0;
+        const std::vector<uint16_t> zt = zblock_table(k - 1, st.t - 1, st.a - 1, &nb);
+        c->d_ztab[s] = c->pupload(zt);
+        c->zblocks[s] = nb;
+      }
     }
     if (st.p > 1 && !c->d_map[st.p]) c->d_map[st.p] = c->pupload(gather_map(k, st.p));
   }
@@ -434,7 +443,9 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       cudaEvent_t b = c->begin(c->s_main);
       c->stats[3] += dev::launch_combine(elem, bufs.ptr(T[st.active]), c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, Wp,
                                          c->d_split[s], (int)binom(st.t - 1, st.a - 1), n, bufs.ptr(T[st.out]),
-                                         c->ld_of(Wt), Wt, c->num_sms, c->s_main);
+                                         c->ld_of(Wt), Wt, c->d_ztab[s], c->zblocks[s],
+                                         (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->num_sms,
+                                         c->s_main);
       c->check_launch();
       c->end(PH_COMBINE, c->s_main, b);
       c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;

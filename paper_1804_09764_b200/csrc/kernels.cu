@@ -248,6 +248,139 @@ __global__ void __launch_bounds__(512, 1) k_combine_lane(const T *__restrict__ A
   }
 }
 
+// Z-block combine.  For a block Z of t'+1 colours, every split (X, Y) of
+// every output S = Z \ {z} uses only the C(t'+1, a') active sets and the
+// C(t'+1, p') passive sets of Z.  A lane (one vertex, or V vertices) loads
+// Z's passive values into registers once, then streams Z's active values:
+// each active value X feeds the p'+1 outputs Z \ {z}, z not in X, with the
+// passive value Z \ X \ {z} -- register indices fixed at compile time by
+// ZTab.  Shared-memory reads per FMA drop from 2 to ~0.4 (config 3's
+// (9;6,3): 25 blocks cover its 165 outputs).
+constexpr int cbinom(int n, int r) {
+  if (r < 0 || r > n) return 0;
+  int c = 1;
+  for (int i = 1; i <= r; ++i) c = c * (n - r + i) / i;
+  return c;
+}
+constexpr int clocal_rank(unsigned m) {  // colex rank of a subset of {0..31}
+  int r = 0, i = 0;
+  for (int c = 0; c < 32; ++c)
+    if (m >> c & 1u) r += cbinom(c, ++i);
+  return r;
+}
+constexpr unsigned clocal_unrank(int s, int r) {
+  unsigned m = 0;
+  int hi = 31;
+  for (int i = s; i >= 1; --i) {
+    int c = i - 1;
+    while (c + 1 <= hi && cbinom(c + 1, i) <= r) ++c;
+    r -= cbinom(c, i);
+    m |= 1u << c;
+    hi = c - 1;
+  }
+  return m;
+}
+template <int ZS, int AS>
+struct ZTab {
+  static constexpr int PS = ZS - 1 - AS;
+  static constexpr int NA = cbinom(ZS, AS), NN = cbinom(ZS, PS);
+  int z[NA][PS + 1];  // outputs (local z) fed by active set a
+  int y[NA][PS + 1];  // the passive set's local index for that output
+  constexpr ZTab() : z(), y() {
+    for (int a = 0; a < NA; ++a) {
+      const unsigned X = clocal_unrank(AS, a);
+      int q = 0;
+      for (int zz = 0; zz < ZS; ++zz) {
+        if (X >> zz & 1u) continue;
+        z[a][q] = zz;
+        y[a][q] = clocal_rank(((1u << ZS) - 1) & ~X & ~(1u << zz));
+        ++q;
+      }
+    }
+  }
+};
+
+template <typename T, int ZS, int AS, int V>
+__global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, int64_t ldA, int WA,
+                                                      const T *__restrict__ N, int64_t ldN, int WN,
+                                                      const uint16_t *__restrict__ ztab, int nblocks, int zld, int64_t n,
+                                                      T *__restrict__ out, int64_t ldO, int nbuf) {
+  constexpr ZTab<ZS, AS> tab{};
+  constexpr int PS = ZS - 1 - AS, NA = ZTab<ZS, AS>::NA, NN = ZTab<ZS, AS>::NN;
+  constexpr int S = 33;
+  constexpr int TV = 32 * V;
+  using LV = typename LaneVec<T, V>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int W = WA + WN;
+  const size_t bstride = ((size_t)S * V * W * sizeof(T) + 15) / 16 * 16 / sizeof(T);
+  T *bufs = reinterpret_cast<T *>(smem_raw);
+  uint16_t *zs = reinterpret_cast<uint16_t *>(bufs + (size_t)nbuf * bstride);
+  for (int i = threadIdx.x; i < nblocks * zld; i += blockDim.x) zs[i] = ztab[i];
+  const int64_t ntiles = (n + TV - 1) / TV;
+  auto stage = [&](int64_t tile, T *b) {
+    const int64_t v0 = tile * TV;
+    for (int r = warp; r < TV; r += nwarp) {
+      const bool ok = v0 + r < n;
+      const int64_t vr = ok ? v0 + r : 0;
+      T *dst = b + (r / V) * V + (r % V);
+      for (int x = lane; x < WA; x += 32) cp_async_elem(dst + (size_t)x * S * V, A + vr * ldA + x, ok);
+      for (int y = lane; y < WN; y += 32) cp_async_elem(dst + (size_t)(WA + y) * S * V, N + vr * ldN + y, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) stage(tile, bufs);
+  __syncthreads();
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    T *cur = bufs + (size_t)(nbuf == 2 ? (it & 1) : 0) * bstride;
+    if (nbuf == 2) {
+      if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs + (size_t)((it + 1) & 1) * bstride);
+      else asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const char *Ab = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + lane);
+    const char *Nb = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + (size_t)WA * S + lane);
+    constexpr uint32_t CB = S * sizeof(LV);
+    const int64_t vb = tile * TV + (int64_t)lane * V;
+    for (int zb = warp; zb < nblocks; zb += nwarp) {
+      const uint16_t *e = zs + (size_t)zb * zld;
+      LV nv[NN];
+#pragma unroll
+      for (int j = 0; j < NN; ++j) nv[j] = *reinterpret_cast<const LV *>(Nb + (uint32_t)e[NA + j] * CB);
+      T acc[ZS][V];
+#pragma unroll
+      for (int zz = 0; zz < ZS; ++zz)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[zz][i] = (T)0;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        const LV av = *reinterpret_cast<const LV *>(Ab + (uint32_t)e[a] * CB);
+#pragma unroll
+        for (int q = 0; q <= PS; ++q)
+#pragma unroll
+          for (int i = 0; i < V; ++i)
+            acc[tab.z[a][q]][i] = fma(LaneVec<T, V>::at(av, i), LaneVec<T, V>::at(nv[tab.y[a][q]], i),
+                                      acc[tab.z[a][q]][i]);
+      }
+#pragma unroll
+      for (int zz = 0; zz < ZS; ++zz) {
+        const uint16_t oc = e[NA + NN + zz];
+        if (oc != 0xFFFF) {
+#pragma unroll
+          for (int i = 0; i < V; ++i)
+            if (vb + i < n) out[(vb + i) * ldO + oc] = acc[zz][i];
+        }
+      }
+    }
+    __syncthreads();
+    if (nbuf == 1 && tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs);
+  }
+}
+
 // ------------------------------------------------------------------ root
 template <typename T>
 __global__ void __launch_bounds__(256) k_root(const T *__restrict__ A, int64_t ldA, int WA, const T *__restrict__ N,
@@ -343,7 +476,7 @@ int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN
   // config 3 at 11.7 FMA/entry wins, config 2's (7;4,3) at 6.7 and (4;3,1)
   // at 2.1 lose)
   const double intensity = (double)WO * nq / (double)(WA + WN + WO);
-  const bool lane_ok = impl ? impl[0] != 't' : intensity >= 8.0;
+  const bool lane_ok = (impl && impl[0] != 'z') ? impl[0] != 't' : intensity >= 8.0;
   if (lane_ok && chunk > 0) {
     const int WOcp = (std::min(chunk, WO) + 7) & ~7;
     const size_t smem = nbuf * tile_bytes + (size_t)nq * WOcp * 4;
@@ -391,10 +524,44 @@ int launch_permute_colors(const uint8_t *by_orig, const int32_t *orig, int64_t n
   return 1;
 }
 
+bool combine_z_supported(int elem, int ts, int as) {
+  // instantiated shapes: (t'; a') = (8; 5) -- configs[3]'s (9;6,3) -- and
+  // (6; 3) -- configs[2] and [4]'s (7;4,3); fp64 only for (6; 3) (registers)
+  if (ts == 8 && as == 5) return elem == 4;
+  return ts == 6 && as == 3;
+}
+
+namespace {
+template <typename T, int ZS, int AS>
+int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint16_t *ztab, int nblocks,
+         int zld, int64_t n, void *out, int64_t ldO, int num_sms, cudaStream_t s) {
+  const size_t cap = 227 * 1024;
+  const size_t tile = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
+  const size_t zbytes = (size_t)nblocks * zld * 2;
+  if (tile + zbytes > cap) return 0;
+  const int nbuf = 2 * tile + zbytes <= cap ? 2 : 1;
+  const size_t smem = nbuf * tile + zbytes;
+  auto kern = k_combine_z<T, ZS, AS, 1>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, 512, smem, num_sms);
+  kern<<<grid, 512, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, ztab, nblocks,
+                               zld, n, static_cast<T *>(out), ldO, nbuf);
+  return 1;
+}
+}  // namespace
+
 int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
-                   const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms,
-                   cudaStream_t s) {
+                   const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
+                   int nblocks, int zld, int ts, int as, int num_sms, cudaStream_t s) {
   if (n == 0) return 0;
+  const char *impl = getenv("CC_COMBINE_IMPL");  // "z" / "lane" / "tile"; default: z when available
+  if (ztab && (!impl || impl[0] == 'z')) {
+    int l = 0;
+    if (elem == 4 && ts == 8 && as == 5) l = z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
+    else if (elem == 4 && ts == 6 && as == 3) l = z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
+    else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
+    if (l) return l;
+  }
   if (elem == 8) return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
   return combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
 }

@@ -98,9 +98,12 @@ int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t 
                 const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s);
 // The neighbour sum of a passive table of size p >= 2 (compressed).
 int launch_gather(int elem, const GatherArgs &a, int num_sms, cudaStream_t s);
+// Combine step; ztab (nullable) = its Z-block cover (zblock_table, nblocks
+// blocks of zld entries) for the register-blocked kernel when combine_z_supported.
 int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
-                   const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms,
-                   cudaStream_t s);
+                   const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
+                   int nblocks, int zld, int ts, int as, int num_sms, cudaStream_t s);
+bool combine_z_supported(int elem, int ts, int as);
 // Root step + deterministic reduction into result[0] (double).  A == nullptr
 // means a single-vertex active part: sum_v N''(v, [k-1]) (one column).
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN,

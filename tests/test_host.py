@@ -159,3 +159,39 @@ def test_median_of_means_and_niter_match_the_oracle(cc):
         cc.cc_median_of_means([1.0], 3, 1, 2)
     with pytest.raises(cc.CCError):
         cc.cc_niter(0.0, 0.1, 3)
+
+
+@pytest.mark.parametrize("K,ts,as_", [(11, 8, 5), (14, 6, 3), (9, 6, 3), (8, 5, 2)])
+def test_zblock_cover_computes_the_split_sum(cc, K, ts, as_):
+    """The Z-block cover (register-blocked combine) covers every output set
+    exactly once, and evaluating the combine through it (each block: its
+    active sets x its passive sets, outputs Z minus one colour) equals the
+    direct split sum of Eq. 1 over the split table, on random rows."""
+    ps = ts - as_
+    tab = cc.cc_zblock_table(K, ts, as_)
+    na, nn, zs = math.comb(ts + 1, as_), math.comb(ts + 1, ps), ts + 1
+    owned = tab[:, na + nn:na + nn + zs].ravel()
+    owned = owned[owned != 0xFFFF]
+    assert sorted(owned.tolist()) == list(range(math.comb(K, ts)))
+    rng = np.random.default_rng(5)
+    A = rng.random(math.comb(K, as_))
+    N = rng.random(math.comb(K, ps))
+    split = cc.cc_split_table(K, ts, as_)  # [q][r] = rank(X) | rank(Y) << 16
+    direct = np.sum(A[split & 0xFFFF] * N[split >> 16], axis=0)
+    local_sets = [c for c in itertools.combinations(range(zs), as_)]
+    local_sets.sort(key=lambda s: s[::-1])  # colex order
+    local_p = sorted(itertools.combinations(range(zs), ps), key=lambda s: s[::-1])
+    pidx = {s: i for i, s in enumerate(local_p)}
+    got = np.full(math.comb(K, ts), np.nan)
+    for row in tab:
+        acc = np.zeros(zs)
+        for a, X in enumerate(local_sets):
+            for z in range(zs):
+                if z in X:
+                    continue
+                Y = tuple(sorted(set(range(zs)) - set(X) - {z}))
+                acc[z] += A[row[a]] * N[row[na + pidx[Y]]]
+        for z in range(zs):
+            if row[na + nn + z] != 0xFFFF:
+                got[row[na + nn + z]] = acc[z]
+    assert np.allclose(got, direct, rtol=1e-12)
