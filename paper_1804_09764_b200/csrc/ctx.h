@@ -37,6 +37,7 @@ struct Pass {
   int32_t *seg_v = nullptr, *seg_hv = nullptr, *hv_first = nullptr, *hv_nseg = nullptr;
   int64_t *seg_b = nullptr, *seg_e = nullptr;
   int64_t n_light = 0, n_seg = 0, n_hv = 0;
+  int64_t small_from = 0;      // first item (segments first, then light) of the <= 8-neighbour tail
   int64_t nnz = 0;             // adjacency entries covered
   const int64_t *beg = nullptr, *end = nullptr;  // device
   uint16_t *goff = nullptr;    // n_items x 16 colour-group ends (per colouring)

@@ -48,6 +48,11 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
   }
   w.nnz = nnz;
   w.n_light = (int64_t)light.size();
+  {  // light items are in internal (degree-descending) order: the <= 8-neighbour tail
+    int64_t i = (int64_t)light.size();
+    while (i > 0 && end[light[i - 1]] - beg[light[i - 1]] <= 8) --i;
+    w.small_from = (int64_t)seg_v.size() + i;
+  }
   w.n_seg = (int64_t)seg_v.size();
   w.n_hv = (int64_t)hv_first.size();
   w.light = c->pupload(light);
@@ -376,7 +381,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     Pass &p = c->p_full;
     c->stats[3] += dev::launch_csort_hist(elem, p.beg, p.end, c->d_col, c->d_colors, p.view(), k, c->d_col_sorted,
                                           p.goff, p.desc, hist >= 0 ? bufs.ptr(hist) : nullptr, c->ld_of(k - 1), rows,
-                                          c->num_sms, c->s_main);
+                                          p.small_from, c->num_sms, c->s_main);
     c->check_launch();
     c->end(PH_CSORT, c->s_main, b);
     c->sorted_valid = true;

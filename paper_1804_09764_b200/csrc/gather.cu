@@ -229,6 +229,79 @@ __global__ void __launch_bounds__(256) k_csort2(const int64_t *__restrict__ beg,
   }
 }
 
+// The tail of light items with <= 8 neighbours (most items of an R-MAT
+// graph): 4 items per warp, 8 lanes per item, one neighbour per lane.
+// Colour groups via __match_any_sync on (group << 5 | colour); per-colour
+// counts and starts in shared memory; the same outputs as k_csort2.
+template <typename T>
+__global__ void __launch_bounds__(256) k_csort_small(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+                                                     const int32_t *__restrict__ col,
+                                                     const uint8_t *__restrict__ colors, AggWork work, int k,
+                                                     int64_t small_from, int32_t *__restrict__ col_out,
+                                                     uint16_t *__restrict__ goff, ItemDesc *__restrict__ desc,
+                                                     T *__restrict__ hist, int64_t ldh) {
+  __shared__ int cnt_all[8][4][16], st_all[8][4][16];
+  const int lane = threadIdx.x & 31, g = lane >> 3, sl = lane & 7;
+  const unsigned lt = (1u << lane) - 1u;
+  int *cs = cnt_all[threadIdx.x >> 5][g], *es = st_all[threadIdx.x >> 5][g];
+  const int64_t n_items = work.n_seg + work.n_light;
+  const int64_t nslots = (int64_t)gridDim.x * blockDim.x / 8;
+  for (int64_t base = small_from + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane) / 8;
+       base < n_items; base += nslots) {
+    const int64_t it = base + g;  // the 4 items of this warp are consecutive
+    const bool live = it < n_items;
+    const int32_t v = live ? work.light[it - work.n_seg] : 0;
+    const int64_t b = live ? beg[v] : 0;
+    const int d = live ? (int)(end[v] - b) : 0;
+    const int cv = live ? (int)colors[v] : 0;
+    const bool ok = sl < d;
+    const int32_t u = ok ? __ldg(col + b + sl) : 0;
+    const int c = ok ? (int)colors[u] : 16 + sl;
+    const unsigned m = __match_any_sync(0xffffffffu, (g << 5) | c);
+    const int rank = __popc(m & lt);
+    cs[sl] = 0;
+    cs[sl + 8] = 0;
+    __syncwarp();
+    if (ok && rank == 0) cs[c] = __popc(m);
+    __syncwarp();
+    const int a0 = cs[2 * sl], a1 = cs[2 * sl + 1];
+    int incl = a0 + a1;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o, 8);
+      if (sl >= o) incl += t;
+    }
+    const int e0 = incl - a0 - a1;
+    es[2 * sl] = e0;
+    es[2 * sl + 1] = e0 + a0;
+    if (live) {
+      uint32_t *gp = reinterpret_cast<uint32_t *>(goff + it * 16);
+      gp[sl] = (uint32_t)(e0 + a0) | ((uint32_t)incl << 16);  // group ends of colours 2 sl, 2 sl + 1
+      if (hist) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = 2 * sl + h;
+          if (j < k && j != cv) hist[(int64_t)v * ldh + (j < cv ? j : j - 1)] = (T)(h ? a1 : a0);
+        }
+      }
+    }
+    __syncwarp();
+    if (ok) col_out[b + es[c] + rank] = u;
+    if (live && sl == 0) {
+      ItemDesc dsc;
+      dsc.b = b;
+      dsc.v = v;
+      dsc.skip = cs[cv];
+      dsc.n_s = d - dsc.skip;
+      dsc.cv_lo = es[cv];
+      dsc.cv = cv;
+      dsc.heavy = 0;
+      desc[it] = dsc;
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------------ hist (p = 1)
 // Heavy segments add their counts atomically into a zeroed row: the values
 // are small integers, exact in fp32/fp64, so the result is order-independent.
@@ -788,9 +861,15 @@ int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, con
 
 int launch_csort_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                       const AggWork &work, int k, int32_t *col_out, uint16_t *goff, ItemDesc *desc, void *hist,
-                      int64_t ldh, int64_t hist_rows, int num_sms, cudaStream_t s) {
-  if (work.n_seg + work.n_light == 0) return 0;
+                      int64_t ldh, int64_t hist_rows, int64_t small_from, int num_sms, cudaStream_t s) {
+  const int64_t n_items = work.n_seg + work.n_light;
+  if (n_items == 0) return 0;
   int launches = 1;
+  // the items before small_from: one warp each (k_csort2 walks n_items on its
+  // own work view, so it gets a view truncated to small_from)
+  AggWork head = work;
+  const bool split = getenv("CC_CSORT_SMALL") == nullptr || getenv("CC_CSORT_SMALL")[0] != '0';
+  if (split && small_from < n_items) head.n_light = small_from - work.n_seg;
   if (hist && work.n_seg) {  // heavy rows accumulate segment counts atomically
     cudaMemsetAsync(hist, 0, (size_t)hist_rows * ldh * elem, s);
     ++launches;
@@ -798,13 +877,27 @@ int launch_csort_hist(int elem, const int64_t *beg, const int64_t *end, const in
   if (elem == 8) {
     static int grid = 0;
     if (!grid) grid = persistent_grid(k_csort2<double>, 256, 0, num_sms);
-    k_csort2<double><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, col_out, goff, desc,
+    k_csort2<double><<<grid, 256, 0, s>>>(beg, end, col, colors, head, k, col_out, goff, desc,
                                           static_cast<double *>(hist), ldh);
   } else {
     static int grid = 0;
     if (!grid) grid = persistent_grid(k_csort2<float>, 256, 0, num_sms);
-    k_csort2<float><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, col_out, goff, desc,
+    k_csort2<float><<<grid, 256, 0, s>>>(beg, end, col, colors, head, k, col_out, goff, desc,
                                          static_cast<float *>(hist), ldh);
+  }
+  if (split && small_from < n_items) {
+    ++launches;
+    if (elem == 8) {
+      static int grid = 0;
+      if (!grid) grid = persistent_grid(k_csort_small<double>, 256, 0, num_sms);
+      k_csort_small<double><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, small_from, col_out, goff, desc,
+                                                 static_cast<double *>(hist), ldh);
+    } else {
+      static int grid = 0;
+      if (!grid) grid = persistent_grid(k_csort_small<float>, 256, 0, num_sms);
+      k_csort_small<float><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, small_from, col_out, goff, desc,
+                                                static_cast<float *>(hist), ldh);
+    }
   }
   return launches;
 }

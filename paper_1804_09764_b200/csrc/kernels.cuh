@@ -92,7 +92,7 @@ int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, con
 // N''(v, {y}) into hist (rows x ldh, k-1 columns) unless hist is null.
 int launch_csort_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                       const AggWork &work, int k, int32_t *col_out, uint16_t *goff, ItemDesc *desc, void *hist,
-                      int64_t ldh, int64_t hist_rows, int num_sms, cudaStream_t s);
+                      int64_t ldh, int64_t hist_rows, int64_t small_from, int num_sms, cudaStream_t s);
 // N''(v, {y}) = #{u in N(v) : sq_{c_v}(col u) = y}, k-1 columns.
 int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                 const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s);
