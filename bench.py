@@ -313,6 +313,12 @@ def run_ours(args, cfg, rank, world, dist):
                         "d2h_bytes_per_step": 8, "ms_per_step": e2e_s * 1e3,
                         "api": "cc_set_colors(host colouring) + cc_count_colorful"},
                 "gpu_launches": launches * args.steps,
+                "nvlink": ({"halo_bytes_received_per_step_rank0": stats["halo_bytes"],
+                            "exchange_ms_per_step_rank0": last_prof["exchange"],
+                            "gbs_rank0": (stats["halo_bytes"] / (last_prof["exchange"] * 1e-3) / 1e9
+                                          if last_prof["exchange"] > 0 else None),
+                            "peak_gbs": 900.0, "peak_source": "nominal NVLink 5 per direction per GPU"}
+                           if world > 1 and not args.replicas else None),
                 "clocks": clk}
         if not args.no_cpu_baseline and world == 1:
             scale = args.cpu_scale or auto_cpu_scale(cfg)

@@ -219,7 +219,8 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * last count (0: none, 1: root dot with the active table, 2: self dot with
  * the lifted neighbour sum), out[6] / out[7] (cap >= 8) = algorithmic bytes
  * and device ms of the longest neighbour-sum launch, out[8] = number of
- * neighbour-sum launches.  cap >= 5. */
+ * neighbour-sum launches, out[9] = halo bytes received by this rank (1D
+ * partition).  cap >= 5. */
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
 
 /* ---- host-only introspection (no GPU needed; used by CPU tests) --------- */

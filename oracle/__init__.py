@@ -57,6 +57,8 @@ def _load():
         lib.or_combine_row.argtypes = [i32, i32, i32, vp, vp, vp]
         lib.or_dp_count.restype = ctypes.c_int
         lib.or_dp_count.argtypes = [i64, vp, vp, i32, vp, vp, i32, i32, vp, vp, vp, vp, vp]
+        lib.or_dp_count_kc.restype = ctypes.c_int
+        lib.or_dp_count_kc.argtypes = [i64, vp, vp, i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]
         lib.or_estimate.restype = ctypes.c_double
         lib.or_estimate.argtypes = [i32, vp, i32, u64]
         lib.or_mom.restype = ctypes.c_double
@@ -144,22 +146,26 @@ class DPResult:
         self.root = root        # np.ndarray n or None
 
 
-def dp_count(g, parent, colors, numtype=NUM_EXACT, keep_x=-1, want_root=False) -> DPResult:
-    """The fold-children DP of Eq. 1 with d = 1; returns X = sum_v D_root(v,[k])."""
+def dp_count(g, parent, colors, numtype=NUM_EXACT, keep_x=-1, want_root=False, colours=None) -> DPResult:
+    """The fold-children DP of Eq. 1 with d = 1; returns X = sum_v D_root(v,[k]).
+    colours (>= k, default k): a colouring with more colours than template
+    vertices: tables over the colours-universe, X sums the root
+    table over every colour set of size k."""
     par = _parent(parent)
     k = len(par)
+    kc = k if colours is None else int(colours)
     col = np.ascontiguousarray(colors, dtype=np.uint8)
     assert col.size == g.n
     table = None
     if keep_x >= 0:
         s = subtree_sizes(list(par))[keep_x]
-        table = np.zeros((g.n, math.comb(k, s)), dtype=np.float64)
+        table = np.zeros((g.n, math.comb(kc, s)), dtype=np.float64)
     root = np.zeros(g.n, dtype=np.float64) if want_root else None
     lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
     ld = ctypes.c_longdouble()
-    rc = _load().or_dp_count(g.n, _ptr(g.row_ptr), _ptr(g.col), k, par.ctypes.data, _ptr(col),
-                             numtype, keep_x, _ptr(table), _ptr(root), ctypes.byref(lo),
-                             ctypes.byref(hi), ctypes.byref(ld))
+    rc = _load().or_dp_count_kc(g.n, _ptr(g.row_ptr), _ptr(g.col), k, par.ctypes.data, _ptr(col), kc,
+                                numtype, keep_x, _ptr(table), _ptr(root), ctypes.byref(lo),
+                                ctypes.byref(hi), ctypes.byref(ld))
     if rc == 2:
         raise OverflowError("oracle DP overflowed the exact u128 type")
     if rc:

@@ -287,23 +287,26 @@ int or_combine_row(int32_t k, int32_t a, int32_t p, const double *A, const doubl
   return OR_OK;
 }
 
-/* numtype: 0 = exact u128 (OR_EOVERFLOW on overflow), 1 = long double, 2 = double.
+/* kc >= k colours (PAPER.md line 146 fixes kc = k): tables are
+ * indexed by colour sets of the kc-colour universe and the total sums the
+ * root table over every colour set of size k.
+ * numtype: 0 = exact u128 (OR_EOVERFLOW on overflow), 1 = long double, 2 = double.
  * keep_x: template vertex whose full-subtree table D_x(v, S) is written to
  *   out_table (n x C(k, size_x), colex order; as double), or -1.
  * out_root: if non-NULL, per-vertex D_root(v, [k]) as double (n entries).
  * Total X: exact in (out_lo, out_hi) for numtype 0; as long double in *out_ld. */
-int or_dp_count(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
-                const int32_t *parent, const uint8_t *colors, int32_t numtype,
-                int32_t keep_x, double *out_table, double *out_root,
-                uint64_t *out_lo, uint64_t *out_hi, long double *out_ld) {
+int or_dp_count_kc(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
+                   const int32_t *parent, const uint8_t *colors, int32_t kc, int32_t numtype,
+                   int32_t keep_x, double *out_table, double *out_root,
+                   uint64_t *out_lo, uint64_t *out_hi, long double *out_ld) {
   tmpl t;
   int rc = tmpl_init(&t, k, parent);
   if (rc) return rc;
-  if (keep_x >= k || keep_x < -1) return OR_EARG;
+  if (keep_x >= k || keep_x < -1 || kc < k || kc > 16) return OR_EARG;
   for (int64_t v = 0; v < n; ++v)
-    if (colors[v] >= k) return OR_EARG;
+    if (colors[v] >= kc) return OR_EARG;
   subsets ss;
-  if (subsets_init(&ss, k)) { subsets_free(&ss); return OR_ENOMEM; }
+  if (subsets_init(&ss, kc)) { subsets_free(&ss); return OR_ENOMEM; }
   switch (numtype) {
     case 0: {
       u128 tot = 0;
@@ -328,6 +331,14 @@ int or_dp_count(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
   }
   subsets_free(&ss);
   return rc;
+}
+
+int or_dp_count(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
+                const int32_t *parent, const uint8_t *colors, int32_t numtype,
+                int32_t keep_x, double *out_table, double *out_root,
+                uint64_t *out_lo, uint64_t *out_hi, long double *out_ld) {
+  return or_dp_count_kc(n, rp, col, k, parent, colors, k, numtype, keep_x, out_table, out_root, out_lo, out_hi,
+                        out_ld);
 }
 
 /* Median of means (Alg. 1 last line, lines 180-181). */

@@ -168,10 +168,11 @@ def cc_get_subtree_rows(ctx, x: int, vertices, k: int, s: int) -> np.ndarray:
 
 
 def cc_last_stats(ctx) -> dict:
-    buf = np.zeros(9, dtype=np.float64)
-    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 9))
+    buf = np.zeros(10, dtype=np.float64)
+    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 10))
     return dict(updates=buf[0], model_bytes=buf[1], agg_bytes=buf[2], launches=buf[3], peak_table_bytes=buf[4],
-                fused_root=int(buf[5]), top_gather_bytes=buf[6], top_gather_ms=buf[7], gather_launches=int(buf[8]))
+                fused_root=int(buf[5]), top_gather_bytes=buf[6], top_gather_ms=buf[7], gather_launches=int(buf[8]),
+                halo_bytes=buf[9])
 
 
 # ------------------------------------------------------------------ host-only

@@ -399,7 +399,7 @@ cc_status cc_last_profile(cc_ctx *c, double *ms, int32_t cap, int32_t *n) {
 
 cc_status cc_last_stats(cc_ctx *c, double *out, int32_t cap) {
   if (!c || !out || cap < 5) return CC_ERR_ARG;
-  for (int i = 0; i < std::min<int32_t>(cap, 9); ++i) out[i] = c->stats[i];
+  for (int i = 0; i < std::min<int32_t>(cap, 10); ++i) out[i] = c->stats[i];
   return CC_OK;
 }
 

@@ -112,7 +112,7 @@ struct cc_ctx {
 
   // profile / stats of the last count
   double prof[cc::PH_N + 1] = {0};
-  double stats[9] = {0};
+  double stats[10] = {0};
   std::vector<std::pair<size_t, double>> gather_log;  // (ev_log index, algorithmic bytes) per gather launch
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;
   std::vector<cudaEvent_t> ev_pool;

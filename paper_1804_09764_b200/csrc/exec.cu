@@ -304,6 +304,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
   gather_pass(c, c->p_remote, P, p, N, 1);
   c->stats[1] += (double)send_rows * ld * elem * 2;
+  c->stats[9] += (double)(R.recv_off[c->pworld()]) * ld * elem;  // halo bytes received
 }
 
 }  // namespace
@@ -312,7 +313,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
                const std::vector<int64_t> *dump_rows) {
   const Plan &pl = c->plan;
   const int k = pl.k, elem = c->elem();
-  std::fill(c->stats, c->stats + 9, 0.0);
+  std::fill(c->stats, c->stats + 10, 0.0);
   c->gather_log.clear();
   c->ev_used = 0;
   c->ev_log.clear();

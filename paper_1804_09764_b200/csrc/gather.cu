@@ -842,8 +842,6 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
     else ring_go<T, 8, 2, 4, 2>(a, num_sms, s);
   }
   else if (wvec <= 32) ring_go<T, 32, 1, 16, 2>(a, num_sms, s);
-  else if (wvec <= 48 && vr == 4) ring_go<T, 16, 3, 4, 2>(a, num_sms, s);
-  else if (wvec <= 64 && vr == 5) ring_go<T, 32, 2, 4, 2>(a, num_sms, s);
   else if (wvec <= 64) ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
   else if (vr == 1) ring_go<T, 32, 4, 5, 2>(a, num_sms, s);
   else ring_go<T, 32, 4, 4, 2>(a, num_sms, s);

@@ -227,6 +227,17 @@ def test_config2_full_fp32_two_colourings():
             assert rel_err(x, want) <= TOL_FP32, seed
 
 
+def test_config3_full_size_fp32_vs_oracle():
+    """configs[3] at full size (R-MAT scale 23, 507 M adjacency entries, the
+    bench workload) against the oracle's fold-children DP in double on the
+    host (~60 GB, a few minutes on 16 cores): final count within 1e-4."""
+    cfg = synth.CONFIGS[3]
+    g = cfg.graph()
+    x = count(g, cfg.parent, seed=cfg.color_seed, precision="fp32")
+    want = oracle.dp_count(g, cfg.parent, oracle.color(g.n, cfg.k, cfg.color_seed), oracle.NUM_DOUBLE).total
+    assert rel_err(x, want) <= TOL_FP32
+
+
 # ------------------------------------------------------------------ closed forms at any size
 def test_star_closed_form_full_config3_graph():
     """X(star with k-1 leaves) = (k-1)! sum_v prod_{j != c_v} cnt_j(v) (SURVEY 8(c) pins)."""

@@ -370,3 +370,40 @@ def test_median_of_means_spec_values():
     assert oracle.median_of_means([1, 2, 3, 4, 5, 6, 8], 3, 2, 3) == pytest.approx(4.5 * s3 / 2, rel=1e-15)
     with pytest.raises(oracle.OracleError):
         oracle.median_of_means([1.0], 3, 1, 2)
+
+
+def test_more_colours_than_vertices_dp_equals_brute_force():
+    """kc > k colours: the DP over the kc-colour universe, summed
+    over every colour set of size k at the root, still counts exactly the
+    colourful maps of the definition (distinct colours; PAPER.md lines
+    105-108), which the brute force enumerates without any colour sets."""
+    rng = np.random.default_rng(21)
+    for trial in range(24):
+        k = int(rng.integers(2, 6))
+        kc = int(rng.integers(k, min(k + 5, 16) + 1))
+        n = int(rng.integers(k, 14))
+        g = synth.gnp(n, float(rng.choice([0.3, 0.6])), int(rng.integers(1 << 30)))
+        parent = [-1] + [int(rng.integers(0, i)) for i in range(1, k)]
+        col = rng.integers(0, kc, n).astype(np.uint8)
+        want = oracle.brute_count(g, parent, col)
+        r = oracle.dp_count(g, parent, col, oracle.NUM_EXACT, want_root=True, colours=kc)
+        assert r.total == want, (k, kc, parent)
+        assert float(r.root.sum()) == float(want)
+    # kc = k is the plain DP
+    g = synth.gnp(10, 0.5, 3)
+    col = oracle.color(g.n, 4, 7)
+    assert oracle.dp_count(g, [-1, 0, 1, 1], col, colours=4).total == oracle.dp_count(g, [-1, 0, 1, 1], col).total
+
+
+def test_more_colours_sum_over_all_colourings():
+    """Summed over all kc^n colourings, X = kc!/(kc-k)! kc^(n-k) maps: each map
+    is colourful for kc (kc-1) ... (kc-k+1) colourings of its k image vertices
+    (the colourful probability of PAPER.md line 146 with kc colours)."""
+    g = synth.gnp(5, 0.7, 11)
+    parent = [-1, 0, 1]
+    k, kc = 3, 4
+    maps = oracle.brute_count(g, parent)
+    total = 0
+    for col in itertools.product(range(kc), repeat=g.n):
+        total += oracle.dp_count(g, parent, np.array(col, np.uint8), colours=kc).total
+    assert total == math.perm(kc, k) * kc ** (g.n - k) * maps
