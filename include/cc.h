@@ -146,6 +146,15 @@ cc_status cc_load_graph(cc_ctx *ctx, int64_t n, const int64_t *row_ptr, const in
  * parent array. */
 cc_status cc_set_template(cc_ctx *ctx, int32_t k, const int32_t *parent);
 
+/* cc_set_template with a colouring of `colours` >= k colours (the
+ * paper fixes colours = k): tables are indexed by colour
+ * sets of the colours-universe, X sums the root table over every colour set
+ * of size k, and the estimators divide by P(colourful) = colours! /
+ * ((colours - k)! colours^k).  cc_set_template(ctx, k, parent) is
+ * cc_set_template_colors(ctx, k, parent, k).  CC_ERR_ARG unless
+ * k <= colours <= 16. */
+cc_status cc_set_template_colors(cc_ctx *ctx, int32_t k, const int32_t *parent, int32_t colours);
+
 /* Colour every vertex uniformly at random with k colours (PAPER.md lines
  * 156-158), on the device, from the shared seed and the ORIGINAL vertex id:
  *   col(v) = ((mix(mix(seed) ^ v) >> 32) * k) >> 32,
@@ -167,6 +176,19 @@ cc_status cc_count_colorful(cc_ctx *ctx, double *colorful_maps);
  * `iterations` values X_j.  iterations >= 1. */
 cc_status cc_estimate(cc_ctx *ctx, int32_t iterations, uint64_t seed0, double *estimate,
                       double *per_iter);
+
+/* Several templates on the current colouring (graphlet frequencies,
+ * PAPER.md lines 46-50): X[i] = colourful maps of template i
+ * (sizes[i] vertices, its parent array at parents + sizes[0] + ... +
+ * sizes[i-1]) for the colouring set by cc_color / cc_set_colors, whose
+ * colours (cc_set_template_colors) must be >= every sizes[i].  Isomorphic
+ * rooted sub-templates are computed once across the templates (kept while
+ * they fit a quarter of the free device memory), and so are the colour sort
+ * and the leaf level; out[9] of cc_last_stats then gives the number of
+ * tables reused.  One GPU (or replica mode).  The context's own template is
+ * restored afterwards. */
+cc_status cc_count_colorful_multi(cc_ctx *ctx, int32_t n_templates, const int32_t *sizes, const int32_t *parents,
+                                  double *X);
 
 /* The paper's estimator (Alg. 1 last line, lines 180-181): run
  * `iterations` colourings with seeds seed0 + j, form C_j = X_j k^k/k!/|Aut(T)|,

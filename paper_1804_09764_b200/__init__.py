@@ -90,6 +90,11 @@ def cc_set_template(ctx, parent) -> None:
     _check(ctx, _lib.cc_set_template(ctx, len(par), _p(par)))
 
 
+def cc_set_template_colors(ctx, parent, colours: int) -> None:
+    par = np.ascontiguousarray(parent, dtype=np.int32)
+    _check(ctx, _lib.cc_set_template_colors(ctx, int(par.size), _p(par), int(colours)))
+
+
 def cc_color(ctx, seed: int) -> None:
     _check(ctx, _lib.cc_color(ctx, seed & 0xFFFFFFFFFFFFFFFF))
 
@@ -98,6 +103,15 @@ def cc_count_colorful(ctx) -> float:
     x = ctypes.c_double()
     _check(ctx, _lib.cc_count_colorful(ctx, ctypes.byref(x)))
     return x.value
+
+
+def cc_count_colorful_multi(ctx, parents) -> np.ndarray:
+    """Colourful maps of each template (list of parent arrays) for the current colouring."""
+    sizes = np.array([len(p) for p in parents], dtype=np.int32)
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(p, dtype=np.int32) for p in parents]), dtype=np.int32)
+    out = np.zeros(len(parents), dtype=np.float64)
+    _check(ctx, _lib.cc_count_colorful_multi(ctx, int(sizes.size), _p(sizes), _p(flat), _p(out)))
+    return out
 
 
 def cc_estimate(ctx, iterations: int, seed0: int, per_iter: bool = False):

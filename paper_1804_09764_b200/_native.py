@@ -41,8 +41,10 @@ SIGNATURES = {
     "cc_last_error": (ctypes.c_char_p, [vp]),
     "cc_load_graph": (c_i32, [vp, c_i64, vp, vp]),
     "cc_set_template": (c_i32, [vp, c_i32, vp]),
+    "cc_set_template_colors": (c_i32, [vp, c_i32, vp, c_i32]),
     "cc_color": (c_i32, [vp, c_u64]),
     "cc_count_colorful": (c_i32, [vp, vp]),
+    "cc_count_colorful_multi": (c_i32, [vp, c_i32, vp, vp, vp]),
     "cc_estimate": (c_i32, [vp, c_i32, c_u64, vp, vp]),
     "cc_set_colors": (c_i32, [vp, vp]),
     "cc_get_colors": (c_i32, [vp, vp]),

@@ -168,10 +168,14 @@ cc_status cc_load_graph(cc_ctx *c, int64_t n, const int64_t *row_ptr, const int3
   API_END(c)
 }
 
-cc_status cc_set_template(cc_ctx *c, int32_t k, const int32_t *parent) {
+cc_status cc_set_template(cc_ctx *c, int32_t k, const int32_t *parent) { return cc_set_template_colors(c, k, parent, k); }
+
+cc_status cc_set_template_colors(cc_ctx *c, int32_t k, const int32_t *parent, int32_t colours) {
   API_BEGIN(c)
   cc::make_plan(k, parent);  // validates (throws CC_ERR_TEMPLATE)
+  if (colours < k || colours > cc::kMaxK) throw Error(CC_ERR_ARG, "colours must be in [k, 16]");
   c->user_parent.assign(parent, parent + k);
+  c->user_kc = colours;
   c->has_colors = false;
   c->sorted_valid = false;
   cc::replan(c, false);
@@ -200,7 +204,8 @@ cc_status cc_set_colors(cc_ctx *c, const uint8_t *colors) {
   if (c->n_global) {
     CUDA_OK(cudaMemsetAsync(c->d_bad, 0, sizeof(unsigned), c->s_main));
     CUDA_OK(cudaMemcpyAsync(c->d_color_stage, colors, (size_t)c->n_global, cudaMemcpyHostToDevice, c->s_main));
-    cc::dev::launch_permute_colors(c->d_color_stage, c->d_orig, c->n_crow, c->plan.k, c->d_colors, c->d_bad, c->s_main);
+    cc::dev::launch_permute_colors(c->d_color_stage, c->d_orig, c->n_crow, c->plan.colours(), c->d_colors, c->d_bad,
+                                   c->s_main);
     c->check_launch();
     CUDA_OK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, c->s_main));
   }
@@ -231,6 +236,52 @@ cc_status cc_count_colorful(cc_ctx *c, double *X) {
   API_END(c)
 }
 
+cc_status cc_count_colorful_multi(cc_ctx *c, int32_t n_templates, const int32_t *sizes, const int32_t *parents,
+                                  double *X) {
+  API_BEGIN(c)
+  if (!c->has_graph || !c->has_template || !c->has_colors)
+    throw Error(CC_ERR_STATE, "cc_count_colorful_multi needs a graph, a template and a colouring");
+  if (c->pworld() != 1) throw Error(CC_ERR_STATE, "cc_count_colorful_multi needs the whole graph on this rank");
+  if (n_templates < 0 || (n_templates && (!sizes || !parents || !X))) throw Error(CC_ERR_ARG, "bad template list");
+  const int kc = c->plan.colours();
+  int64_t off = 0;
+  for (int i = 0; i < n_templates; ++i) {
+    if (sizes[i] < 1 || sizes[i] > kc) throw Error(CC_ERR_ARG, "template larger than the colouring's colours");
+    cc::make_plan(sizes[i], parents + off);  // validates (CC_ERR_TEMPLATE)
+    off += sizes[i];
+  }
+  const std::vector<int32_t> saved(c->user_parent);
+  const int saved_kc = c->user_kc;
+  struct Restore {
+    cc_ctx *c;
+    const std::vector<int32_t> &parent;
+    int kc;
+    cc::TableCache cache;
+    ~Restore() {
+      try {
+        cc::free_cache(c, cache);
+        c->user_parent = parent;
+        c->user_kc = kc;
+        cc::replan(c, false);
+      } catch (...) {
+      }
+    }
+  } restore{c, saved, saved_kc, {}};
+  size_t free_b = 0, total_b = 0;
+  CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+  restore.cache.budget = free_b / 4;  // shared tables kept while they fit a quarter of the free memory
+  c->user_kc = kc;
+  off = 0;
+  for (int i = 0; i < n_templates; ++i) {
+    c->user_parent.assign(parents + off, parents + off + sizes[i]);
+    off += sizes[i];
+    cc::replan(c, false);
+    cc::run_count(c, &X[i], -1, nullptr, nullptr, nullptr, &restore.cache);
+  }
+  c->stats[9] = (double)restore.cache.reused;  // (reported through cc_last_stats out[9] for this call)
+  API_END(c)
+}
+
 cc_status cc_estimate(cc_ctx *c, int32_t iterations, uint64_t seed0, double *estimate, double *per_iter) {
   API_BEGIN(c)
   if (iterations < 1 || !estimate) throw Error(CC_ERR_ARG, "iterations >= 1 and estimate != NULL required");
@@ -239,8 +290,9 @@ cc_status cc_estimate(cc_ctx *c, int32_t iterations, uint64_t seed0, double *est
   long double mean = 0;
   for (double x : xs) mean += x;
   mean /= iterations;
-  long double scale = 1;  // k^k / k!
-  for (int i = 1; i <= c->plan.k; ++i) scale *= (long double)c->plan.k / i;
+  // 1 / P(a map is colourful) = kc^k (kc-k)! / kc! (PAPER.md line 146 with kc colours)
+  long double scale = 1;
+  for (int i = 0; i < c->plan.k; ++i) scale *= (long double)c->plan.colours() / (c->plan.colours() - i);
   *estimate = (double)(mean * scale / (long double)c->plan.aut);
   if (per_iter) std::copy(xs.begin(), xs.end(), per_iter);
   API_END(c)
@@ -253,7 +305,15 @@ cc_status cc_estimate_mom(cc_ctx *c, int32_t iterations, uint64_t seed0, int32_t
     throw Error(CC_ERR_ARG, "need 1 <= groups <= iterations and estimate != NULL");
   if (!c->has_graph || !c->has_template) throw Error(CC_ERR_STATE, "cc_estimate_mom needs a graph and a template");
   const std::vector<double> xs = cc::run_iterations(c, iterations, seed0);
-  const cc_status st = cc_median_of_means(xs.data(), iterations, c->plan.k, c->plan.aut, groups, estimate);
+  // C_j = X_j / P(colourful) / |Aut|: rescale to the k = kc form cc_median_of_means uses
+  std::vector<double> ys(xs);
+  if (c->plan.colours() != c->plan.k) {
+    long double r = 1;  // [kc^k (kc-k)!/kc!] / [k^k/k!]
+    for (int i = 0; i < c->plan.k; ++i)
+      r *= ((long double)c->plan.colours() / (c->plan.colours() - i)) / ((long double)c->plan.k / (c->plan.k - i));
+    for (auto &y : ys) y = (double)((long double)y * r);
+  }
+  const cc_status st = cc_median_of_means(ys.data(), iterations, c->plan.k, c->plan.aut, groups, estimate);
   if (st != CC_OK) throw Error(st, "median of means");
   if (per_iter) std::copy(xs.begin(), xs.end(), per_iter);
   API_END(c)
@@ -287,14 +347,14 @@ cc_status cc_get_subtree_counts(cc_ctx *c, int32_t x, double *out) {
   cc::replan(c, true);
   const auto &pl = c->plan;
   const auto &R = c->part;
-  const int k = pl.k;
+  const int k = pl.colours();
   const int tid = pl.full_table[x];
   std::vector<uint8_t> col((size_t)c->n_crow);
   if (!col.empty()) CUDA_OK(cudaMemcpy(col.data(), c->d_colors, col.size(), cudaMemcpyDeviceToHost));
   double X = 0;
   if (tid == -2) {  // root: per-vertex C(v, T, [k])
     std::memset(out, 0, (size_t)c->n_global * sizeof(double));
-    if (k == 1) {
+    if (pl.k == 1) {
       for (int64_t v = 0; v < c->n_global; ++v) out[v] = 1.0;
     } else {
       std::vector<double> root;
@@ -342,7 +402,7 @@ cc_status cc_get_subtree_rows(cc_ctx *c, int32_t x, const int32_t *vertices, int
   cc::replan(c, true);
   const auto &pl = c->plan;
   const auto &R = c->part;
-  const int k = pl.k;
+  const int k = pl.colours();
   const int tid = pl.full_table[x];
   // original id -> internal row (owned rows only; isolated vertices: -1)
   std::vector<int64_t> inv((size_t)c->n_global, -1);
@@ -360,9 +420,9 @@ cc_status cc_get_subtree_rows(cc_ctx *c, int32_t x, const int32_t *vertices, int
   double X = 0;
   if (tid == -2) {  // root: per-vertex count, one column
     std::vector<double> root;
-    if (k > 1) cc::run_count(c, &X, -1, nullptr, &root);
+    if (pl.k > 1) cc::run_count(c, &X, -1, nullptr, &root);
     for (int32_t i = 0; i < nv; ++i)
-      out[i] = k == 1 ? 1.0 : (inv[vertices[i]] >= 0 ? root[inv[vertices[i]]] : 0.0);
+      out[i] = pl.k == 1 ? 1.0 : (inv[vertices[i]] >= 0 ? root[inv[vertices[i]]] : 0.0);
   } else if (tid == -1) {  // a leaf: the single-vertex table
     for (int32_t i = 0; i < nv; ++i)
       for (int j = 0; j < k; ++j) out[(size_t)i * k + j] = j == colour_of[vertices[i]] ? 1.0 : 0.0;

@@ -74,7 +74,9 @@ struct TableInfo {
 };
 
 struct Plan {
-  int k = 0;
+  int k = 0;           // template vertices
+  int kc = 0;          // colours (>= k); 0 = k
+  int colours() const { return kc ? kc : k; }
   int root = -1;       // root of the plan (chosen by the planner)
   int user_root = -1;  // the parent -1 vertex of the user's array
   std::vector<int> parent;
@@ -99,7 +101,9 @@ struct PlanOpts {
   bool auto_root = true;
   double avg_degree = 32.0;  // adjacency entries per stored vertex
   int elem = 4;              // table entry bytes
-  double fma_bytes = 0.25;   // weight of one combine FMA in bytes
+  double fma_bytes = 4.0;    // weight of one combine FMA in bytes (measured: the combine
+                             // kernels run ~1.5-4 TFMA/s against ~7 TB/s of gather bytes)
+  int kc = 0;                // colours (0 = template size)
 };
 Plan make_plan(int k, const int32_t *parent, const PlanOpts *opts = nullptr);  // throws Error(CC_ERR_TEMPLATE)
 double plan_cost(const Plan &P, const PlanOpts &o);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -65,6 +66,21 @@ struct Buf {
   void *p = nullptr;
   size_t bytes = 0;
   int refs = 0;
+  bool owned = true;  // false: owned by a TableCache (never freed by the executor)
+};
+
+// Tables of one colouring shared across the templates of
+// cc_count_colorful_multi: isomorphic rooted sub-templates
+// (same AHU code, Plan::tables[].code) have identical tables for the same
+// colouring and colour universe, so each is computed once.  The colour sort
+// and the leaf level are computed once as well.
+struct TableCache {
+  std::map<std::string, std::pair<void *, size_t>> tables;  // code -> device buffer, bytes
+  void *hist = nullptr;
+  size_t hist_bytes = 0;
+  bool sorted = false;
+  size_t bytes = 0, budget = 0;
+  int64_t reused = 0, stored = 0;
 };
 
 }  // namespace cc
@@ -95,6 +111,7 @@ struct cc_ctx {
   // template
   bool has_template = false;
   std::vector<int32_t> user_parent;  // the template as given (re-planned when the graph changes)
+  int user_kc = 0;                   // colours of the colouring (0 = template size)
   cc::Plan plan;
   std::vector<uint32_t *> d_split;    // per step: split table (combine steps)
   std::vector<uint16_t *> d_ztab;     // per step: Z-block cover table (nullptr if none)
@@ -210,7 +227,8 @@ void launch_colouring(cc_ctx *c, uint64_t seed);
 // only the internal rows listed in *dump_rows (copied right after the step
 // that produces the table; nothing else changes).
 void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out,
-               const std::vector<int64_t> *dump_rows = nullptr);
+               const std::vector<int64_t> *dump_rows = nullptr, TableCache *cache = nullptr);
+void free_cache(cc_ctx *c, TableCache &cache);
 // X_j for colourings seed0 + j, j < iterations (replica mode with world > 1:
 // iteration j on rank j mod world, then one all-reduce of the vector).
 std::vector<double> run_iterations(cc_ctx *c, int iterations, uint64_t seed0);

@@ -13,6 +13,7 @@
 //            T' = N'' itself (a = 1: no work in the compressed layout);
 //   X = sum_v of the root step (fp64), all-reduced over ranks (line 237).
 #include <cmath>
+#include <functional>
 #include <cstring>
 
 #include "ctx.h"
@@ -74,13 +75,17 @@ struct Bufs {
   std::vector<Buf> pool;
   explicit Bufs(cc_ctx *cx) : c(cx) { pool.reserve(256); }
   int make(size_t bytes) {
-    pool.push_back({c->amalloc(bytes, c->s_main), bytes, 1});
+    pool.push_back({c->amalloc(bytes, c->s_main), bytes, 1, true});
+    return (int)pool.size() - 1;
+  }
+  int alias(void *p, size_t bytes) {  // a buffer owned elsewhere (table cache)
+    pool.push_back({p, bytes, 1, false});
     return (int)pool.size() - 1;
   }
   void ref(int b) { pool[b].refs++; }
   void unref(int b) {
     if (b < 0) return;
-    if (--pool[b].refs == 0) c->afree(pool[b].p, pool[b].bytes, c->s_main);
+    if (--pool[b].refs == 0 && pool[b].owned) c->afree(pool[b].p, pool[b].bytes, c->s_main);
   }
   void *ptr(int b) const { return b < 0 ? nullptr : pool[b].p; }
 };
@@ -129,6 +134,7 @@ void replan(cc_ctx *c, bool fixed) {
   PlanOpts o;
   o.auto_root = !(fixed || c->opt.fixed_root);
   o.elem = c->elem();
+  o.kc = c->user_kc;
   if (c->has_graph && c->n_own > 0) o.avg_degree = (double)c->part.col.size() / (double)c->n_own;
   c->plan = make_plan((int)c->user_parent.size(), c->user_parent.data(), &o);
   if (c->has_graph) upload_template(c);
@@ -144,11 +150,13 @@ void upload_template(cc_ctx *c) {
   c->zblocks.assign(c->plan.steps.size(), 0);
   c->d_map.assign(kMaxK + 1, nullptr);
   c->d_comp = nullptr;
-  const int k = c->plan.k;
+  const int k = c->plan.colours();
   for (size_t s = 0; s < c->plan.steps.size(); ++s) {
     const Step &st = c->plan.steps[s];
-    // compressed universe: k-1 colours, sets of size t-1 split into (a-1, p)
-    if (st.out < 0) {
+    // compressed universe: k-1 colours, sets of size t-1 split into (a-1, p);
+    // the root of a template with as many vertices as colours pairs each
+    // active set with its complement, otherwise the root is a full combine
+    if (st.out < 0 && c->plan.k == k) {
       if (st.a > 1) c->d_comp = c->pupload(complement_table(k - 1, st.a - 1));
     } else if (st.a > 1) {
       // rows of the split table padded to a multiple of 8 outputs (16-byte
@@ -175,7 +183,7 @@ void launch_colouring(cc_ctx *c, uint64_t seed) {
     CUDA_OK(cudaEventCreate(&c->ev_color[1]));
   }
   CUDA_OK(cudaEventRecord(c->ev_color[0], c->s_main));
-  dev::launch_color(c->d_orig, c->n_crow, seed, c->plan.k, c->d_colors, c->s_main);
+  dev::launch_color(c->d_orig, c->n_crow, seed, c->plan.colours(), c->d_colors, c->s_main);
   c->check_launch();
   CUDA_OK(cudaEventRecord(c->ev_color[1], c->s_main));
   c->has_colors = true;
@@ -203,7 +211,7 @@ struct RootFuse {
 
 // N'' = neighbour sum of the passive table P' (size p >= 2) over one pass.
 void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, const RootFuse *rf = nullptr) {
-  const int k = c->plan.k, elem = c->elem();
+  const int k = c->plan.colours(), elem = c->elem();
   const int W_in = (int)binom(k - 1, p - 1), W_out = (int)binom(k - 1, p);
   dev::GatherArgs a;
   a.beg = w.beg;
@@ -271,7 +279,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   // world > 1: exchange the boundary rows of P' on the comm stream while the
   // local part runs; then add the remote part.
   auto &api = nccl();
-  const int k = c->plan.k, elem = c->elem();
+  const int k = c->plan.colours(), elem = c->elem();
   const int64_t ld = c->ld_of(binom(k - 1, p - 1));
   cudaEvent_t ready = c->ev(), recvd = c->ev();
   CUDA_OK(cudaEventRecord(ready, c->s_main));
@@ -309,17 +317,26 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
 
 }  // namespace
 
+void free_cache(cc_ctx *c, TableCache &cache) {
+  for (auto &t : cache.tables) c->afree(t.second.first, t.second.second, c->s_main);
+  cache.tables.clear();
+  if (cache.hist) c->afree(cache.hist, cache.hist_bytes, c->s_main);
+  cache.hist = nullptr;
+  cache.sorted = false;
+  cache.bytes = 0;
+}
+
 void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out,
-               const std::vector<int64_t> *dump_rows) {
+               const std::vector<int64_t> *dump_rows, TableCache *cache) {
   const Plan &pl = c->plan;
-  const int k = pl.k, elem = c->elem();
+  const int k = pl.colours(), elem = c->elem();
   std::fill(c->stats, c->stats + 10, 0.0);
   c->gather_log.clear();
   c->ev_used = 0;
   c->ev_log.clear();
   c->cur_bytes = c->peak_bytes = 0;
   std::fill(c->prof, c->prof + PH_N + 1, 0.0);
-  if (k == 1) {  // the single-vertex template maps onto every vertex
+  if (pl.k == 1) {  // the single-vertex template maps onto every vertex (any colouring)
     *X = (double)c->n_global;
     return;
   }
@@ -348,7 +365,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   {
     const Step &rs = pl.steps[sr];
     const char *f = getenv("CC_FUSED_ROOT");
-    if (c->pworld() == 1 && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
+    if (c->pworld() == 1 && pl.k == k && !cache && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') &&
+        rs.out < 0 && rs.p >= 2) {
       const int P = rs.passive;
       int s_l = -1, users = 0;
       for (int s = 0; s < sr; ++s) {
@@ -376,8 +394,19 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     if (pl.steps[s].p == 1) last_hist_use = s;
   double *per_vertex = nullptr;
   if (root_out || fuse) per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
-  if (c->pworld() == 1) {  // colour sort + leaf level N''(v, {y}) in one pass over the adjacency
-    if (last_hist_use >= 0) hist = bufs.make((size_t)rows * c->ld_of(k - 1) * elem);
+  if (cache && cache->sorted) {  // an earlier template of this colouring sorted and built the leaf level
+    if (last_hist_use >= 0) hist = bufs.alias(cache->hist, cache->hist_bytes);
+  } else if (c->pworld() == 1) {  // colour sort + leaf level N''(v, {y}) in one pass over the adjacency
+    if (last_hist_use >= 0) {
+      const size_t hb = (size_t)rows * c->ld_of(k - 1) * elem;
+      if (cache) {
+        cache->hist = c->amalloc(hb, c->s_main);
+        cache->hist_bytes = hb;
+        hist = bufs.alias(cache->hist, hb);
+      } else {
+        hist = bufs.make(hb);
+      }
+    }
     cudaEvent_t b = c->begin(c->s_main);
     Pass &p = c->p_full;
     c->stats[3] += dev::launch_csort_hist(elem, p.beg, p.end, c->d_col, c->d_colors, p.view(), k, c->d_col_sorted,
@@ -388,12 +417,49 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     c->sorted_valid = true;
     c->stats[1] += (double)p.nnz * 9.0 + (double)p.items() * 64.0 + (hist >= 0 ? (double)n * (k - 1) * elem : 0.0);
     if (hist >= 0) c->stats[0] += (double)c->part.col.size() * k;  // U counts C(k,1) = k colour sets per entry
+    if (cache) {
+      cache->sorted = true;
+      if (!cache->hist) {  // the first template needed no leaf level: build it with the next one that does
+        cache->sorted = false;
+      }
+    }
+  }
+  // with a cache: the tables this template still has to compute (those not
+  // cached, reachable from the root without passing through a cached one)
+  std::vector<char> need((size_t)pl.tables.size(), 1);
+  std::vector<int> producer((size_t)pl.tables.size(), -1);
+  if (cache) {
+    for (int s = 0; s < (int)pl.steps.size(); ++s)
+      if (pl.steps[s].out >= 0) producer[pl.steps[s].out] = s;
+    std::fill(need.begin(), need.end(), 0);
+    std::function<void(int)> mark = [&](int id) {
+      if (id < 0 || need[id]) return;
+      if (cache->tables.count(pl.tables[id].code)) {
+        need[id] = 2;  // cached
+        return;
+      }
+      need[id] = 1;
+      const Step &ps = pl.steps[producer[id]];
+      mark(ps.active);
+      mark(ps.passive);
+    };
+    mark(pl.steps.back().active);
+    mark(pl.steps.back().passive);
   }
 
   for (int s = 0; s < (int)pl.steps.size(); ++s) {
     const Step &st = pl.steps[s];
     const int Wa = (int)binom(k - 1, st.a - 1), Wp = (int)binom(k - 1, st.p), Wt = (int)binom(k - 1, st.t - 1);
     if (s == defer_lift) continue;  // T_out = N''(P) is evaluated inside the fused root
+    if (cache && st.out >= 0) {
+      if (!need[st.out]) continue;  // only feeds tables this template finds cached
+      if (need[st.out] == 2) {      // computed by an earlier template of this colouring
+        const auto &e = cache->tables[pl.tables[st.out].code];
+        T[st.out] = bufs.alias(e.first, e.second);
+        ++cache->reused;
+        continue;
+      }
+    }
     if (s == sr && fuse) {
       cc::RootFuse rf;
       rf.mode = fuse;
@@ -433,7 +499,27 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       nbuf = Nb[P];
     }
     const int64_t ldN = c->ld_of(Wp);
-    if (st.out < 0) {  // root step fused with the sum over v (Eq. 3)
+    if (st.out < 0 && pl.k < k) {  // fewer template vertices than colours: root table, then row sums (Eq. 3)
+      int rb = nbuf;  // a = 1: the root table is the neighbour sum itself
+      if (st.a > 1) {
+        rb = bufs.make((size_t)rows * c->ld_of(Wt) * elem);
+        cudaEvent_t b = c->begin(c->s_main);
+        c->stats[3] += dev::launch_combine(elem, bufs.ptr(T[st.active]), c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, Wp,
+                                           c->d_split[s], (int)binom(st.t - 1, st.a - 1), n, bufs.ptr(rb),
+                                           c->ld_of(Wt), Wt, c->d_ztab[s], c->zblocks[s],
+                                           (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->num_sms,
+                                           c->s_main);
+        c->check_launch();
+        c->end(PH_COMBINE, c->s_main, b);
+        c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;
+      }
+      cudaEvent_t b = c->begin(c->s_main);
+      c->stats[3] += dev::launch_rowsum(elem, bufs.ptr(rb), c->ld_of(Wt), Wt, n, c->d_partials, c->n_partials,
+                                        per_vertex, c->d_result, c->s_main);
+      c->check_launch();
+      c->end(PH_ROOT, c->s_main, b);
+      c->stats[1] += (double)n * Wt * elem;
+    } else if (st.out < 0) {  // root step fused with the sum over v (Eq. 3)
       cudaEvent_t b = c->begin(c->s_main);
       const void *A = st.a > 1 ? bufs.ptr(T[st.active]) : nullptr;
       c->stats[3] += dev::launch_root(elem, A, c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, c->d_comp, n, c->d_partials,
@@ -455,6 +541,15 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       c->check_launch();
       c->end(PH_COMBINE, c->s_main, b);
       c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;
+    }
+    if (cache && st.out >= 0 && T[st.out] >= 0 && bufs.pool[T[st.out]].owned &&
+        !cache->tables.count(pl.tables[st.out].code) &&
+        cache->bytes + bufs.pool[T[st.out]].bytes <= cache->budget) {  // keep it for the next templates
+      Buf &bb = bufs.pool[T[st.out]];
+      cache->tables[pl.tables[st.out].code] = {bb.p, bb.bytes};
+      cache->bytes += bb.bytes;
+      bb.owned = false;
+      ++cache->stored;
     }
     if (dump_rows && st.out == dump_table && st.out >= 0 && T[st.out] >= 0) {  // sampled rows of this table
       const int W = (int)binom(k - 1, pl.tables[dump_table].size - 1);
@@ -513,7 +608,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     if (n) CUDA_OK(cudaMemcpyAsync(root_out->data(), per_vertex, (size_t)n * 8, cudaMemcpyDeviceToHost, c->s_main));
   }
   for (auto &b : bufs.pool)
-    if (b.p) c->afree(b.p, b.bytes, c->s_main);
+    if (b.p && b.owned && b.refs > 0) c->afree(b.p, b.bytes, c->s_main);
   if (per_vertex) {
     void *pv = per_vertex;
     c->afree(pv, (size_t)std::max<int64_t>(n, 1) * 8, c->s_main);

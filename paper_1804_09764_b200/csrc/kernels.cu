@@ -415,6 +415,33 @@ __global__ void __launch_bounds__(256) k_root(const T *__restrict__ A, int64_t l
   }
 }
 
+// X_v = sum of the root table's row (templates with fewer vertices than colours)
+template <typename T>
+__global__ void __launch_bounds__(256) k_rowsum(const T *__restrict__ R, int64_t ld, int W, int64_t n,
+                                                double *__restrict__ partials, double *__restrict__ per_vertex) {
+  __shared__ double wsum_s[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  double wsum = 0.0;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; v < n; v += nwarps) {
+    double s = 0.0;
+    for (int x = lane; x < W; x += 32) s += (double)R[v * ld + x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (per_vertex) per_vertex[v] = s;
+      wsum += s;
+    }
+  }
+  if (lane == 0) wsum_s[warp] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) b += wsum_s[i];
+    partials[blockIdx.x] = b;
+  }
+}
+
 __global__ void k_reduce(const double *__restrict__ partials, int np, double *__restrict__ out) {
   const int lane = threadIdx.x;
   double s = 0.0;
@@ -574,6 +601,16 @@ int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int
   else
     k_root<float><<<n_partials, 256, 0, s>>>(static_cast<const float *>(A), ldA, WA, static_cast<const float *>(N),
                                               ldN, comp, n, partials, per_vertex);
+  k_reduce<<<1, 32, 0, s>>>(partials, n_partials, result);
+  return 2;
+}
+
+int launch_rowsum(int elem, const void *R, int64_t ld, int W, int64_t n, double *partials, int n_partials,
+                  double *per_vertex, double *result, cudaStream_t s) {
+  if (elem == 8)
+    k_rowsum<double><<<n_partials, 256, 0, s>>>(static_cast<const double *>(R), ld, W, n, partials, per_vertex);
+  else
+    k_rowsum<float><<<n_partials, 256, 0, s>>>(static_cast<const float *>(R), ld, W, n, partials, per_vertex);
   k_reduce<<<1, 32, 0, s>>>(partials, n_partials, result);
   return 2;
 }

@@ -109,6 +109,10 @@ bool combine_z_supported(int elem, int ts, int as);
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN,
                 const uint16_t *comp, int64_t n, double *partials, int n_partials, double *per_vertex,
                 double *result, cudaStream_t s);
+// X = sum_v sum_x R(v, x) for x < W (root of a template with fewer vertices
+// than colours), per-vertex sums into per_vertex (nullable), result[0].
+int launch_rowsum(int elem, const void *R, int64_t ld, int W, int64_t n, double *partials, int n_partials,
+                  double *per_vertex, double *result, cudaStream_t s);
 // Halo pack: out[i, :] = src[idx[i], :] for i < rows (whole padded rows).
 int launch_pack(int elem, const void *src, int64_t ld, const int32_t *idx, int64_t rows, void *out,
                 cudaStream_t s);

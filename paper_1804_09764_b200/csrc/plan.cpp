@@ -130,7 +130,7 @@ Plan plan_rooted(const Tree &T);
 // writes its rows and performs C(k-1,t-1) C(t-1,a-1) FMAs (weighted as
 // `fma_bytes` bytes each).
 double plan_cost(const Plan &P, const PlanOpts &o) {
-  const int k = P.k;
+  const int k = o.kc > 0 ? o.kc : P.k;  // colour universe
   const double e = o.elem, d = o.avg_degree;
   double c = 0;
   bool hist = false;
@@ -155,6 +155,7 @@ double plan_cost(const Plan &P, const PlanOpts &o) {
 Plan make_plan(int k, const int32_t *parent, const PlanOpts *opts) {
   Tree T0 = load_tree(k, parent);
   Plan base = plan_rooted(T0);
+  base.kc = opts && opts->kc > 0 ? opts->kc : k;
   if (!opts || !opts->auto_root || k <= 2) return base;
   Plan best = base;
   double best_cost = plan_cost(base, *opts);
@@ -173,6 +174,7 @@ Plan make_plan(int k, const int32_t *parent, const PlanOpts *opts) {
   best.memory = base.memory;
   best.computation = base.computation;
   best.user_root = base.root;
+  best.kc = base.kc;
   return best;
 }
 

@@ -101,6 +101,86 @@ def test_small_suite_every_table_exact():
             assert np.array_equal(got[x], ref[x]), (parent, x)
 
 
+def test_more_colours_than_vertices_every_table_exact():
+    """kc > k colours: every table, the root per-vertex counts and
+    the total against the oracle's kc-colour DP (itself pinned to brute
+    force), including heavy segments and fp32."""
+    cc = lib()
+    rng = np.random.default_rng(77)
+    for trial in range(12):
+        k = int(rng.integers(2, 8))
+        kc = int(rng.integers(k + 1, min(k + 6, 16) + 1))
+        n = int(rng.integers(k, 60))
+        g = synth.gnp(n, float(rng.choice([0.1, 0.3])), int(rng.integers(1 << 30)))
+        parent = [-1] + [int(rng.integers(0, i)) for i in range(1, k)]
+        col = rng.integers(0, kc, n).astype(np.uint8)
+        want = oracle.dp_count(g, parent, col, oracle.NUM_EXACT, want_root=True, colours=kc)
+        sizes = subtree_sizes(parent)
+        with context(g, parent, segment_len=3) as ctx:
+            cc.cc_set_template_colors(ctx, parent, kc)
+            cc.cc_set_colors(ctx, col)
+            assert cc.cc_count_colorful(ctx) == float(want.total), (k, kc, parent)
+            root = cc.cc_get_subtree_counts(ctx, parent.index(-1), g.n, kc, kc)
+            assert np.array_equal(root[:, 0], want.root), (k, kc)
+            for x in range(k):
+                if parent[x] < 0:
+                    continue
+                got = cc.cc_get_subtree_counts(ctx, x, g.n, kc, sizes[x])
+                ref = oracle.dp_count(g, parent, col, oracle.NUM_EXACT, keep_x=x, colours=kc).table
+                assert np.array_equal(got, ref), (k, kc, parent, x)
+        with context(g, parent, "fp32") as ctx:
+            cc.cc_set_template_colors(ctx, parent, kc)
+            cc.cc_set_colors(ctx, col)
+            assert rel_err(cc.cc_count_colorful(ctx), float(want.total)) <= TOL_FP32
+
+
+def test_more_colours_estimator_scaling():
+    """estimate = mean X_j kc^k (kc-k)! / kc! / |Aut(T)| for kc colours."""
+    cc = lib()
+    g = synth.gnp(40, 0.3, 3)
+    parent = [-1, 0, 1, 1]
+    k, kc = 4, 7
+    with context(g, parent) as ctx:
+        cc.cc_set_template_colors(ctx, parent, kc)
+        est, xs = cc.cc_estimate(ctx, 12, 300, per_iter=True)
+        est_m = cc.cc_estimate_mom(ctx, 12, 300, 3)
+    want_x = [oracle.dp_count(g, parent, oracle.color(g.n, kc, 300 + j), oracle.NUM_EXACT, colours=kc).total
+              for j in range(12)]
+    assert list(xs) == [float(v) for v in want_x]
+    scale = kc ** k * math.factorial(kc - k) / math.factorial(kc) / oracle.aut(parent)
+    assert est == pytest.approx(np.mean(want_x) * scale, rel=1e-13)
+    groups = [np.mean(want_x[0:4]), np.mean(want_x[4:8]), np.mean(want_x[8:12])]
+    assert est_m == pytest.approx(float(np.median(groups)) * scale, rel=1e-13)
+
+
+def test_multi_template_counts_share_tables():
+    """cc_count_colorful_multi: several templates on one colouring,
+    isomorphic sub-templates computed once -- every count equals the oracle's
+    single-template DP, for kc = k and kc > k, fp64 and fp32."""
+    cc = lib()
+    templates = [[-1, 0, 1, 2, 3, 4], [-1, 0, 0, 0, 0, 0], [-1, 0, 1, 2, 3, 2], [-1, 0, 1, 2, 2, 2],
+                 [-1, 0, 1, 1, 2, 2], [-1, 0, 0, 1, 1, 2], [-1, 0, 1], [-1, 0, 1, 2, 3, 4, 5, 6]]
+    for gi, g in enumerate((synth.gnp(70, 0.12, 5), synth.scaled_twin(synth.CONFIGS[3], 11, 16).graph())):
+        for kc in (8, 10):
+            col = oracle.color(g.n, kc, 31 + gi)
+            want = [oracle.dp_count(g, t, col, oracle.NUM_LONGDOUBLE, colours=kc).total for t in templates]
+            with context(g, templates[0]) as ctx:
+                cc.cc_set_template_colors(ctx, templates[0], kc)
+                cc.cc_set_colors(ctx, col)
+                got = cc.cc_count_colorful_multi(ctx, templates)
+                reused = cc.cc_last_stats(ctx)["halo_bytes"]  # out[9]: tables reused across templates
+                assert cc.cc_count_colorful(ctx) == got[0]  # the context's own template is restored
+            for i, t in enumerate(templates):
+                assert rel_err(got[i], want[i]) <= TOL_FP64, (gi, kc, t)
+            assert reused > 0
+            with context(g, templates[0], "fp32") as ctx:
+                cc.cc_set_template_colors(ctx, templates[0], kc)
+                cc.cc_set_colors(ctx, col)
+                got32 = cc.cc_count_colorful_multi(ctx, templates)
+            for i in range(len(templates)):
+                assert rel_err(got32[i], want[i]) <= TOL_FP32
+
+
 def test_small_suite_heavy_segments_and_chunks_do_not_change_results():
     for g, parent, col in _small_suite()[:10]:
         want = float(oracle.dp_count(g, parent, col, oracle.NUM_EXACT).total)
