@@ -101,11 +101,22 @@ typedef struct {
                             locally (no exchange), and cc_estimate /
                             cc_estimate_mom run iteration j on rank j mod world
                             and all-reduce the per-iteration counts */
+  void *loopback;        /* test hook, NULL for NCCL: a group from
+                            cc_loopback_create -- the ranks are threads of one
+                            process, possibly on one GPU; halo rows move with
+                            event-ordered device copies, reductions on the
+                            host (no kernel waits for another rank) */
 } cc_options;
 
 /* Fill *opt with defaults: CC_FP64, device 0, world 1, rank 0, auto sizes,
  * relabel_seed 0x5eed, planner-chosen root, 1D partition (replicas 0). */
 cc_status cc_default_options(cc_options *opt);
+
+/* Test hook: an in-process group of `world` ranks for cc_options.loopback
+ * (each rank a host thread with its own context); destroy after every
+ * context of the group. */
+cc_status cc_loopback_create(int32_t world, void **group);
+void cc_loopback_destroy(void *group);
 
 /* Rank 0 only: write a fresh 128-byte ncclUniqueId to out128 (host).
  * CC_ERR_NCCL if libnccl.so.2 cannot be loaded. */

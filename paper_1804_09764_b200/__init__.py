@@ -54,6 +54,17 @@ def cc_default_options(**kw) -> cc_options:
     return o
 
 
+def cc_loopback_create(world: int) -> ctypes.c_void_p:
+    """Test hook: an in-process transport group for `world` rank threads (cc_options.loopback)."""
+    h = ctypes.c_void_p()
+    _check(None, _lib.cc_loopback_create(world, ctypes.byref(h)))
+    return h
+
+
+def cc_loopback_destroy(group) -> None:
+    _lib.cc_loopback_destroy(group)
+
+
 def cc_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(None, _lib.cc_nccl_unique_id(buf))

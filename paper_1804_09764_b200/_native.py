@@ -23,7 +23,8 @@ c_i32, c_i64, c_u32, c_u64, c_dbl, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.
 class cc_options(ctypes.Structure):
     _fields_ = [("precision", c_i32), ("device", c_i32), ("world", c_i32), ("rank", c_i32),
                 ("nccl_id", vp), ("chunk_cols", c_i64), ("segment_len", c_i32),
-                ("use_graphs", c_i32), ("relabel_seed", c_u64), ("fixed_root", c_i32), ("replicas", c_i32)]
+                ("use_graphs", c_i32), ("relabel_seed", c_u64), ("fixed_root", c_i32), ("replicas", c_i32),
+                ("loopback", vp)]
 
 
 CC_OK, CC_ERR_ARG, CC_ERR_GRAPH, CC_ERR_TEMPLATE, CC_ERR_STATE, CC_ERR_OOM, CC_ERR_CUDA, \
@@ -36,6 +37,8 @@ STATUS_NAMES = ["CC_OK", "CC_ERR_ARG", "CC_ERR_GRAPH", "CC_ERR_TEMPLATE", "CC_ER
 SIGNATURES = {
     "cc_default_options": (c_i32, [vp]),
     "cc_nccl_unique_id": (c_i32, [vp]),
+    "cc_loopback_create": (c_i32, [c_i32, vp]),
+    "cc_loopback_destroy": (None, [vp]),
     "cc_create": (c_i32, [vp, vp]),
     "cc_destroy": (None, [vp]),
     "cc_last_error": (ctypes.c_char_p, [vp]),

@@ -89,6 +89,14 @@ cc_status cc_default_options(cc_options *opt) {
   return CC_OK;
 }
 
+cc_status cc_loopback_create(int32_t world, void **group) {
+  if (world < 1 || world > 64 || !group) return CC_ERR_ARG;
+  *group = new cc::LoopbackGroup(world);
+  return CC_OK;
+}
+
+void cc_loopback_destroy(void *group) { delete static_cast<cc::LoopbackGroup *>(group); }
+
 cc_status cc_nccl_unique_id(void *out128) {
   if (!out128) return CC_ERR_ARG;
   auto &api = cc::nccl();
@@ -104,7 +112,7 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   if (!opt || !out) return CC_ERR_ARG;
   if (opt->precision != CC_FP64 && opt->precision != CC_FP32) return CC_ERR_ARG;
   if (opt->world < 1 || opt->world > 64 || opt->rank < 0 || opt->rank >= opt->world) return CC_ERR_ARG;
-  if (opt->world > 1 && !opt->nccl_id) return CC_ERR_ARG;
+  if (opt->world > 1 && !opt->nccl_id && !opt->loopback) return CC_ERR_ARG;
   if (opt->chunk_cols != 0 || opt->segment_len < 0 || opt->use_graphs < 0 || opt->use_graphs > 1) return CC_ERR_ARG;
   if (opt->replicas < 0 || opt->replicas > 1) return CC_ERR_ARG;
   std::unique_ptr<cc_ctx> c(new cc_ctx());
@@ -123,7 +131,10 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
     uint64_t thr = UINT64_MAX;
     CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     alloc_scratch(c.get());
-    if (opt->world > 1) {
+    if (opt->world > 1 && opt->loopback) {
+      c->loop = static_cast<cc::LoopbackGroup *>(opt->loopback);
+      if (c->loop->world != opt->world) throw Error(CC_ERR_ARG, "loopback group size != world");
+    } else if (opt->world > 1) {
       auto &api = cc::nccl();
       if (!api.ok) throw Error(CC_ERR_NCCL, api.why);
       ncclUniqueId id;

@@ -10,6 +10,7 @@
 
 #include "common.h"
 #include "kernels.cuh"
+#include "loopback.h"
 #include "nccl_dl.h"
 
 #define CUDA_OK(expr)                                                                                  \
@@ -93,6 +94,7 @@ struct cc_ctx {
   int64_t l2_bytes = 126LL << 20;
   cudaStream_t s_main = nullptr, s_comm = nullptr;
   ncclComm_t comm = nullptr;
+  cc::LoopbackGroup *loop = nullptr;  // in-process transport instead of NCCL (test hook)
   std::vector<void *> persistent;  // cudaMalloc'd: graph, plan tables (freed on reload / destroy)
 
   // graph

@@ -12,6 +12,7 @@
 //     T'  <- split-sum combine of the active table with N'' (a >= 2), or
 //            T' = N'' itself (a = 1: no work in the compressed layout);
 //   X = sum_v of the root step (fp64), all-reduced over ranks (line 237).
+#include <chrono>
 #include <cmath>
 #include <functional>
 #include <cstring>
@@ -271,6 +272,52 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   c->stats[2] += bytes;
 }
 
+// Loopback transport (cc_options.loopback): the halo rows of this rank come
+// from the peers' send buffers by device copies ordered by the peers' pack
+// events; this rank's send buffer is released only after every peer's copy.
+void loopback_exchange(cc_ctx *c, void *sendbuf, void *P, int64_t ld, int elem) {
+  LoopbackGroup &G = *c->loop;
+  const auto &R = c->part;
+  const int me = c->opt.rank;
+  cudaEvent_t packed = c->ev(), copied = c->ev();
+  CUDA_OK(cudaEventRecord(packed, c->s_comm));
+  G.ptr[me] = sendbuf;
+  G.offs[me] = R.send_off.data();
+  G.ev[me] = packed;
+  G.rendezvous();
+  for (int q = 0; q < G.world; ++q) {
+    if (q == me) continue;
+    const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
+    if (!nr) continue;
+    CUDA_OK(cudaStreamWaitEvent(c->s_comm, G.ev[q], 0));
+    CUDA_OK(cudaMemcpyAsync(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[q]) * ld * elem,
+                            static_cast<const char *>(G.ptr[q]) + (size_t)G.offs[q][me] * ld * elem,
+                            (size_t)nr * ld * elem, cudaMemcpyDeviceToDevice, c->s_comm));
+  }
+  CUDA_OK(cudaEventRecord(copied, c->s_comm));
+  G.ev2[me] = copied;
+  G.rendezvous();
+  for (int q = 0; q < G.world; ++q)
+    if (q != me) CUDA_OK(cudaStreamWaitEvent(c->s_comm, G.ev2[q], 0));
+  G.rendezvous();  // every rank has read the slots before they are reused
+}
+
+void loopback_allreduce(cc_ctx *c, double *d, size_t count, cudaStream_t s) {
+  LoopbackGroup &G = *c->loop;
+  const int me = c->opt.rank;
+  std::vector<double> h(count);
+  CUDA_OK(cudaMemcpyAsync(h.data(), d, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  G.vec[me] = h;
+  G.rendezvous();
+  std::vector<double> sum(count, 0.0);
+  for (int r = 0; r < G.world; ++r)  // rank order: the same sum on every rank
+    for (size_t i = 0; i < count; ++i) sum[i] += G.vec[r][i];
+  G.rendezvous();
+  CUDA_OK(cudaMemcpyAsync(d, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+}
+
 void aggregate(cc_ctx *c, void *P, int p, void *N) {
   if (c->pworld() == 1) {
     gather_pass(c, c->p_full, P, p, N, 0);
@@ -292,6 +339,9 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   c->stats[3] += dev::launch_pack(elem, P, ld, c->d_send_idx, send_rows, sendbuf, c->s_comm);
   c->check_launch();
   const ncclDataType_t dt = elem == 8 ? ncclFloat64 : ncclFloat32;
+  if (c->loop) {
+    loopback_exchange(c, sendbuf, P, ld, elem);
+  } else {
   NCCL_OK(api.GroupStart());
   for (int q = 0; q < c->pworld(); ++q) {
     if (q == c->opt.rank) continue;
@@ -305,6 +355,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
                        q, c->comm, c->s_comm));
   }
   NCCL_OK(api.GroupEnd());
+  }
   c->end(PH_EXCHANGE, c->s_comm, xb);
   if (sendbuf) c->afree(sendbuf, sbytes, c->s_comm);
   CUDA_OK(cudaEventRecord(recvd, c->s_comm));
@@ -316,6 +367,19 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
 }
 
 }  // namespace
+
+void LoopbackGroup::rendezvous() {
+  std::unique_lock<std::mutex> lk(mu);
+  const int64_t gen = generation;
+  if (++arrived == world) {
+    arrived = 0;
+    ++generation;
+    cv.notify_all();
+    return;
+  }
+  if (!cv.wait_for(lk, std::chrono::seconds(300), [&] { return generation != gen; }))
+    throw Error(CC_ERR_NCCL, "loopback rendezvous timed out (a rank failed or diverged)");
+}
 
 void free_cache(cc_ctx *c, TableCache &cache) {
   for (auto &t : cache.tables) c->afree(t.second.first, t.second.second, c->s_main);
@@ -583,7 +647,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   }
   if (c->pworld() > 1) {
     cudaEvent_t b = c->begin(c->s_main);
-    NCCL_OK(nccl().AllReduce(c->d_result, c->d_result, 1, ncclFloat64, ncclSum, c->comm, c->s_main));
+    if (c->loop) loopback_allreduce(c, c->d_result, 1, c->s_main);
+    else NCCL_OK(nccl().AllReduce(c->d_result, c->d_result, 1, ncclFloat64, ncclSum, c->comm, c->s_main));
     c->end(PH_EXCHANGE, c->s_main, b);
   }
   CUDA_OK(cudaEventRecord(t1, c->s_main));
@@ -651,7 +716,8 @@ std::vector<double> run_iterations(cc_ctx *c, int iterations, uint64_t seed0) {
   if (rep) {  // every rank ends with every X_j (the others' entries are 0 here)
     double *d = static_cast<double *>(c->amalloc((size_t)iterations * 8, c->s_main));
     CUDA_OK(cudaMemcpyAsync(d, xs.data(), (size_t)iterations * 8, cudaMemcpyHostToDevice, c->s_main));
-    NCCL_OK(nccl().AllReduce(d, d, (size_t)iterations, ncclFloat64, ncclSum, c->comm, c->s_main));
+    if (c->loop) loopback_allreduce(c, d, (size_t)iterations, c->s_main);
+    else NCCL_OK(nccl().AllReduce(d, d, (size_t)iterations, ncclFloat64, ncclSum, c->comm, c->s_main));
     CUDA_OK(cudaMemcpyAsync(xs.data(), d, (size_t)iterations * 8, cudaMemcpyDeviceToHost, c->s_main));
     c->afree(reinterpret_cast<void *&>(d), (size_t)iterations * 8, c->s_main);
     CUDA_OK(cudaStreamSynchronize(c->s_main));

@@ -1,0 +1,110 @@
+"""-m gpu: the multi-rank device path (1D vertex partition, Alg. 2 of the
+paper; and colouring replicas) with several ranks on
+ONE GPU through the in-process loopback transport (cc_options.loopback): each
+rank is a host thread with its own context and partition; halo rows move by
+event-ordered device copies and the final reductions on the host, so no
+kernel waits for another rank.  Everything but NCCL itself runs: the
+partition, the per-rank colour sort of the local / remote neighbour ranges,
+the leaf level over the full ranges, the pack kernel, the halo placement, the
+local gather and the accumulating remote gather, and the cross-rank sums.
+The results must equal the single-rank run and the oracle."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import count, lib, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def run_ranks(g, parent, world, colors=None, seed=None, precision="fp64", replicas=0, estimate=None, **kw):
+    cc = lib()
+    group = cc.cc_loopback_create(world)
+    out = [None] * world
+    stats = [None] * world
+    errors = []
+
+    def worker(r):
+        ctx = None
+        try:
+            opt = cc.cc_default_options(world=world, rank=r, device=0, replicas=replicas,
+                                        precision=cc.CC_FP64 if precision == "fp64" else cc.CC_FP32, **kw)
+            opt.loopback = group
+            ctx = cc.cc_create(opt)
+            cc.cc_load_graph(ctx, g.n, g.row_ptr, g.col)
+            cc.cc_set_template(ctx, parent)
+            if estimate:
+                out[r] = cc.cc_estimate(ctx, estimate[0], estimate[1], per_iter=True)
+            else:
+                if colors is not None:
+                    cc.cc_set_colors(ctx, colors)
+                else:
+                    cc.cc_color(ctx, seed)
+                out[r] = cc.cc_count_colorful(ctx)
+                stats[r] = cc.cc_last_stats(ctx)
+        except Exception as e:  # noqa: BLE001
+            errors.append((r, e))
+        finally:
+            if ctx is not None:
+                cc.cc_destroy(ctx)
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=900)
+    cc.cc_loopback_destroy(group)
+    assert not errors, errors
+    return out, stats
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_partitioned_counts_equal_single_rank_exact(world):
+    rng = np.random.default_rng(world)
+    cases = [(synth.CONFIGS[0].graph(), synth.CONFIGS[0].parent, 5),
+             (synth.gnp(300, 0.05, 9), [-1, 0, 1, 1, 0, 4], 6),
+             (synth.scaled_twin(synth.CONFIGS[3], 11, 16).graph(), synth.CONFIGS[3].parent, 12)]
+    for g, parent, k in cases:
+        col = rng.integers(0, k, g.n).astype(np.uint8)
+        want = oracle.dp_count(g, parent, col, oracle.NUM_LONGDOUBLE).total
+        single = count(g, parent, colors=col)
+        for seg in (0, 3):
+            xs, st = run_ranks(g, parent, world, colors=col, segment_len=seg)
+            assert len(set(xs)) == 1, xs  # every rank returns the all-reduced count
+            assert rel_err(xs[0], want) <= 1e-12 and rel_err(xs[0], single) <= 1e-12, (world, k, seg)
+            if g.nnz > 1000:
+                assert all(s["halo_bytes"] > 0 for s in st)  # rows really crossed between ranks
+
+
+def test_partitioned_fp32_config1_and_twin_of_config4():
+    for cfg, g in ((synth.CONFIGS[1], synth.CONFIGS[1].graph()),
+                   (synth.CONFIGS[4], synth.scaled_twin(synth.CONFIGS[4], 11, 32).graph())):
+        col = oracle.color(g.n, cfg.k, cfg.color_seed)
+        want = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE).total
+        xs, _ = run_ranks(g, cfg.parent, 2, seed=cfg.color_seed, precision="fp32")
+        assert rel_err(xs[0], want) <= 1e-4 and len(set(xs)) == 1
+        xs, _ = run_ranks(g, cfg.parent, 2, seed=cfg.color_seed, precision="fp64")
+        assert rel_err(xs[0], want) <= 1e-12
+
+
+def test_colouring_replicas_split_the_iterations():
+    """Replicas: every rank the whole graph, iteration j on rank
+    j mod world, one all-reduce of the per-iteration counts."""
+    g = synth.gnp(80, 0.1, 4)
+    parent = [-1, 0, 1, 1]
+    want_x = [oracle.dp_count(g, parent, oracle.color(g.n, 4, 70 + j), oracle.NUM_EXACT).total for j in range(9)]
+    out, _ = run_ranks(g, parent, 3, replicas=1, estimate=(9, 70))
+    for est, xs in out:
+        assert list(xs) == [float(v) for v in want_x]
+        assert est == pytest.approx(oracle.estimate(want_x, 4, oracle.aut(parent)), rel=1e-14)
