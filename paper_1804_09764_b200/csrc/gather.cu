@@ -635,8 +635,8 @@ __device__ __forceinline__ void load_desc(const GatherArgs &a, int64_t it, int l
   go = lane < 16 ? (int)__ldg(a.goff + it * 16 + lane) : 0;
 }
 
-template <typename T, int NV, int U, typename AccT = double>
-__global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
+template <typename T, int NV, int U, typename AccT = double, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = 32 * NV * VW;  // columns per pass
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(256, 2) k_gather_ldg(GatherArgs a, int nch) {
   }
 }
 
-template <typename T, int NV, int U>
+template <typename T, int NV, int U, int MINB = 2>
 void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = 32 * NV * VW;
@@ -773,7 +773,7 @@ void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   // 3432) keep the shared-memory row in fp32 so that 16 warps fit per SM
   // (each entry adds at most k-1 colour-group block sums; C-6)
   const bool acc32 = sizeof(T) == 4 && a.W_out > 1600;
-  auto kern = acc32 ? k_gather_ldg<T, NV, U, float> : k_gather_ldg<T, NV, U, double>;
+  auto kern = acc32 ? k_gather_ldg<T, NV, U, float, MINB> : k_gather_ldg<T, NV, U, double, MINB>;
   const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
@@ -818,9 +818,13 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
       else ldg_go<T, 1, 8>(a, num_sms, s);
     } else if (wvec <= 64) {
       if (lv == 1) ldg_go<T, 2, 4>(a, num_sms, s);
+      else if (lv == 2) ldg_go<T, 2, 4, 3>(a, num_sms, s);
+      else if (lv == 3) ldg_go<T, 2, 6, 3>(a, num_sms, s);
       else ldg_go<T, 2, 8>(a, num_sms, s);
     } else if (wvec <= 96) {
       if (lv == 1) ldg_go<T, 3, 2>(a, num_sms, s);
+      else if (lv == 2) ldg_go<T, 3, 2, 3>(a, num_sms, s);
+      else if (lv == 3) ldg_go<T, 3, 3, 3>(a, num_sms, s);
       else ldg_go<T, 3, 4>(a, num_sms, s);
     } else {
       if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);

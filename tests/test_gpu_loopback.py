@@ -108,3 +108,16 @@ def test_colouring_replicas_split_the_iterations():
     for est, xs in out:
         assert list(xs) == [float(v) for v in want_x]
         assert est == pytest.approx(oracle.estimate(want_x, 4, oracle.aut(parent)), rel=1e-14)
+
+
+def test_partitioned_config3_full_size_two_ranks():
+    """configs[3] at full size split over 2 ranks (loopback, one GPU): the
+    same count as the single-rank run (fp32 tables, different summation
+    order: within 1e-6), with ~40% of the rows crossing as halos."""
+    cfg = synth.CONFIGS[3]
+    g = cfg.graph()
+    single = count(g, cfg.parent, seed=cfg.color_seed, precision="fp32")
+    xs, st = run_ranks(g, cfg.parent, 2, seed=cfg.color_seed, precision="fp32")
+    assert len(set(xs)) == 1
+    assert rel_err(xs[0], single) <= 1e-6
+    assert all(s["halo_bytes"] > 0 for s in st)
