@@ -818,13 +818,9 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
       else ldg_go<T, 1, 8>(a, num_sms, s);
     } else if (wvec <= 64) {
       if (lv == 1) ldg_go<T, 2, 4>(a, num_sms, s);
-      else if (lv == 2) ldg_go<T, 2, 4, 3>(a, num_sms, s);
-      else if (lv == 3) ldg_go<T, 2, 6, 3>(a, num_sms, s);
       else ldg_go<T, 2, 8>(a, num_sms, s);
     } else if (wvec <= 96) {
       if (lv == 1) ldg_go<T, 3, 2>(a, num_sms, s);
-      else if (lv == 2) ldg_go<T, 3, 2, 3>(a, num_sms, s);
-      else if (lv == 3) ldg_go<T, 3, 3, 3>(a, num_sms, s);
       else ldg_go<T, 3, 4>(a, num_sms, s);
     } else {
       if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);
