@@ -1,11 +1,16 @@
 // gather.cu -- the neighbour-sum kernels of the DP (sm_100a).
 //
-//   k_csort        per colouring: stable sort of every work item's neighbour
-//                  range by neighbour colour, recording the 16 colour-group
-//                  ends (neighbours whose compressed rows share an index space
+//   k_csort2       per colouring (one GPU): stable sort of every work item's
+//                  neighbour range by neighbour colour (match_any groups),
+//                  the 16 colour-group ends, the item descriptor, and the
+//                  leaf level N''(v, {y}) in the same pass;
+//   k_csort_small  the same for the <= 8-neighbour tail, 4 items per warp;
+//   k_csort        the sort alone for the multi-rank local / remote passes
+//                  (neighbours whose compressed rows share an index space
 //                  become contiguous)
 //   k_hist         N''(v, {y}): neighbour counts per colour -- the neighbour
-//                  sum of the single-vertex table (passive part of size 1)
+//                  sum of the single-vertex table (passive part of size 1),
+//                  multi-rank path
 //   k_gather_ring  N''(v, Y'') = sum_{u in N(v)} P(u, Y): the inner sum over
 //                  u of Eq. 1, SpMM-shaped.  Rows of the
 //                  compressed passive table are fetched with cp.async into a
@@ -15,7 +20,8 @@
 //                  Heavy neighbour lists are split into segments (Alg. 4,
 //                  PAPER.md lines 494-523) whose partial rows the last
 //                  arriving segment sums in segment order (deterministic).
-//   k_gather_ldg   the same sum for rows of > 8 vectors: one warp per item,
+//                  Used for rows of <= 16 vectors (4 / 8 lanes per item).
+//   k_gather_ldg   the same sum for rows of > 16 vectors: one warp per item,
 //                  plain LDG.128 rows, U rows in flight, ~20 instructions per
 //                  row (the ring's per-row bookkeeping made it issue-bound);
 //                  optionally evaluates the root step in its epilogue.
