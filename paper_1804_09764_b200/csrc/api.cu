@@ -59,7 +59,8 @@ void free_persistent(cc_ctx *c) {
   c->d_arrive = nullptr;
   c->arrive_cap = 0;
   c->max_hv = c->max_seg = 0;
-  c->has_graph = c->has_colors = c->sorted_valid = false;
+  c->has_graph = c->has_colors = c->sorted_valid = c->full_sorted_valid = false;
+  c->d_col_sorted_full = nullptr;
 }
 
 void alloc_scratch(cc_ctx *c) {
@@ -188,7 +189,7 @@ cc_status cc_set_template_colors(cc_ctx *c, int32_t k, const int32_t *parent, in
   c->user_parent.assign(parent, parent + k);
   c->user_kc = colours;
   c->has_colors = false;
-  c->sorted_valid = false;
+  c->sorted_valid = c->full_sorted_valid = false;
   cc::replan(c, false);
   c->has_template = true;
   API_END(c)
@@ -223,7 +224,7 @@ cc_status cc_set_colors(cc_ctx *c, const uint8_t *colors) {
   CUDA_OK(cudaStreamSynchronize(c->s_main));
   if (bad) throw Error(CC_ERR_ARG, "colour out of [0, k)");
   c->has_colors = true;
-  c->sorted_valid = false;
+  c->sorted_valid = c->full_sorted_valid = false;
   API_END(c)
 }
 

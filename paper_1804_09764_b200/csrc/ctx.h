@@ -44,6 +44,7 @@ struct Pass {
   const int64_t *beg = nullptr, *end = nullptr;  // device
   uint16_t *goff = nullptr;    // n_items x 16 colour-group ends (per colouring)
   dev::ItemDesc *desc = nullptr;  // n_items descriptors (per colouring)
+  int32_t *col_sorted = nullptr;   // the colour-sorted neighbour ids this pass reads
   int64_t items() const { return n_seg + n_light; }
   dev::AggWork view() const {
     dev::AggWork w;
@@ -122,6 +123,8 @@ struct cc_ctx {
   uint16_t *d_comp = nullptr;         // root step complement table
   bool has_colors = false;
   bool sorted_valid = false;          // colour-sorted adjacency matches the colouring
+  bool full_sorted_valid = false;     // world > 1: the full ranges' sort (fused root) matches it
+  int32_t *d_col_sorted_full = nullptr;
 
   // scratch
   double *d_partials = nullptr, *d_result = nullptr;

@@ -115,6 +115,7 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
   build_pass(c, beg, end, false, c->p_full);
   c->p_full.beg = c->d_rp;
   c->p_full.end = c->d_rp + 1;
+  c->p_full.col_sorted = c->d_col_sorted;  // world > 1: its own buffer, allocated for the fused root
   if (c->pworld() > 1) {
     c->d_mid = c->pupload(R.mid);
     c->d_send_idx = c->pupload(R.send_idx);
@@ -124,11 +125,14 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
     c->p_local.end = c->d_mid;
     c->p_remote.beg = c->d_mid;
     c->p_remote.end = c->d_rp + 1;
+    c->p_local.col_sorted = c->p_remote.col_sorted = c->d_col_sorted;
+    c->p_full.col_sorted = nullptr;
+    c->d_col_sorted_full = nullptr;
   }
   c->d_arrive = c->pmalloc<unsigned int>((size_t)std::max<int64_t>(c->max_hv, 1));
   c->arrive_cap = std::max<int64_t>(c->max_hv, 1);
   c->has_graph = true;
-  c->sorted_valid = false;
+  c->sorted_valid = c->full_sorted_valid = false;
 }
 
 void replan(cc_ctx *c, bool fixed) {
@@ -188,13 +192,13 @@ void launch_colouring(cc_ctx *c, uint64_t seed) {
   c->check_launch();
   CUDA_OK(cudaEventRecord(c->ev_color[1], c->s_main));
   c->has_colors = true;
-  c->sorted_valid = false;
+  c->sorted_valid = c->full_sorted_valid = false;
 }
 
 namespace {
 
 void csort(cc_ctx *c, Pass &p) {
-  c->stats[3] += dev::launch_csort(p.beg, p.end, c->d_col, c->d_colors, p.view(), c->d_col_sorted, p.goff,
+  c->stats[3] += dev::launch_csort(p.beg, p.end, c->d_col, c->d_colors, p.view(), p.col_sorted, p.goff,
                                    p.desc, c->num_sms, c->s_main);
   c->check_launch();
   c->stats[1] += (double)p.nnz * 14.0 + (double)p.items() * 64.0;
@@ -217,7 +221,7 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   dev::GatherArgs a;
   a.beg = w.beg;
   a.end = w.end;
-  a.col = c->d_col_sorted;
+  a.col = w.col_sorted;
   a.goff = w.goff;
   a.desc = w.desc;
   a.colors = c->d_colors;
@@ -318,13 +322,10 @@ void loopback_allreduce(cc_ctx *c, double *d, size_t count, cudaStream_t s) {
   CUDA_OK(cudaStreamSynchronize(s));
 }
 
-void aggregate(cc_ctx *c, void *P, int p, void *N) {
-  if (c->pworld() == 1) {
-    gather_pass(c, c->p_full, P, p, N, 0);
-    return;
-  }
-  // world > 1: exchange the boundary rows of P' on the comm stream while the
-  // local part runs; then add the remote part (PAPER.md lines 326-341).
+// world > 1: send this rank's boundary rows of P' to the peers that need
+// them and receive the halo rows (after the owned rows of P') on the comm
+// stream; returns an event recorded when the halo rows have arrived.
+cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p) {
   auto &api = nccl();
   const int k = c->plan.colours(), elem = c->elem();
   const int64_t ld = c->ld_of(binom(k - 1, p - 1));
@@ -359,11 +360,22 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   c->end(PH_EXCHANGE, c->s_comm, xb);
   if (sendbuf) c->afree(sendbuf, sbytes, c->s_comm);
   CUDA_OK(cudaEventRecord(recvd, c->s_comm));
+  c->stats[1] += (double)send_rows * ld * elem * 2;
+  c->stats[9] += (double)(R.recv_off[c->pworld()]) * ld * elem;  // halo bytes received
+  return recvd;
+}
+
+void aggregate(cc_ctx *c, void *P, int p, void *N) {
+  if (c->pworld() == 1) {
+    gather_pass(c, c->p_full, P, p, N, 0);
+    return;
+  }
+  // world > 1: exchange the boundary rows of P' on the comm stream while the
+  // local part runs; then add the remote part (PAPER.md lines 326-341).
+  cudaEvent_t recvd = exchange_halo(c, P, p);
   gather_pass(c, c->p_local, P, p, N, 0);
   CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
   gather_pass(c, c->p_remote, P, p, N, 1);
-  c->stats[1] += (double)send_rows * ld * elem * 2;
-  c->stats[9] += (double)(R.recv_off[c->pworld()]) * ld * elem;  // halo bytes received
 }
 
 }  // namespace
@@ -429,8 +441,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   {
     const Step &rs = pl.steps[sr];
     const char *f = getenv("CC_FUSED_ROOT");
-    if (c->pworld() == 1 && pl.k == k && !cache && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') &&
-        rs.out < 0 && rs.p >= 2) {
+    if (pl.k == k && !cache && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
       const int P = rs.passive;
       int s_l = -1, users = 0;
       for (int s = 0; s < sr; ++s) {
@@ -531,6 +542,21 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       rf.ldA = c->ld_of(Wa);
       rf.WA = Wa;
       rf.per_vertex = per_vertex;
+      if (c->pworld() > 1) {
+        // partitioned: the fused root needs whole neighbour ranges, so the
+        // halo rows of the passive table arrive first and the full ranges
+        // are colour-sorted once per colouring (their own buffer)
+        if (!c->full_sorted_valid) {
+          if (!c->d_col_sorted_full) c->d_col_sorted_full = c->pmalloc<int32_t>(std::max<size_t>(c->part.col.size(), 1));
+          c->p_full.col_sorted = c->d_col_sorted_full;
+          cudaEvent_t b = c->begin(c->s_main);
+          csort(c, c->p_full);
+          c->end(PH_CSORT, c->s_main, b);
+          c->full_sorted_valid = true;
+        }
+        cudaEvent_t recvd = exchange_halo(c, bufs.ptr(T[st.passive]), st.p);
+        CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
+      }
       gather_pass(c, c->p_full, bufs.ptr(T[st.passive]), st.p, nullptr, 0, &rf);
       cudaEvent_t b = c->begin(c->s_main);
       c->stats[3] += dev::launch_root(8, nullptr, 0, 0, per_vertex, 1, nullptr, n, c->d_partials, c->n_partials,

@@ -560,7 +560,6 @@ bool combine_z_supported(int elem, int ts, int as) {
   // instantiated shapes: (t'; a') = (8; 5) -- configs[3]'s (9;6,3) -- and
   // (6; 3) -- configs[2] and [4]'s (7;4,3); fp64 only for (6; 3) (registers)
   if (ts == 8 && as == 5) return elem == 4;
-  if (getenv("CC_COMBINE_Z_SMALL") && ((ts == 3 && as == 2) || (ts == 2 && as == 1))) return true;  // experiment
   return ts == 6 && as == 3;
 }
 
@@ -593,8 +592,6 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
     if (elem == 4 && ts == 8 && as == 5) l = z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     else if (elem == 4 && ts == 6 && as == 3) l = z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
-    else if (elem == 4 && ts == 3 && as == 2) l = z_go<float, 4, 2>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
-    else if (elem == 4 && ts == 2 && as == 1) l = z_go<float, 3, 1>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     if (l) return l;
   }
   if (elem == 8) return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);

@@ -98,6 +98,26 @@ def test_partitioned_fp32_config1_and_twin_of_config4():
         assert rel_err(xs[0], want) <= 1e-12
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_fused_root(world):
+    """The fused root (reading C-15) in the partitioned path: the halo rows of
+    the root's passive table arrive first and the full neighbour ranges are
+    colour-sorted, so configs[4]'s N7 never reaches HBM on any rank (what
+    lets configs[4] fit at P = 2).  Self dot (mode 2) and dot with the active
+    table (mode 1), heavy segments, fp64 and fp32."""
+    cases = [(synth.scaled_twin(synth.CONFIGS[4], 11, 32).graph(), synth.CONFIGS[4].parent, 2),
+             (synth.gnp(200, 0.06, 8), [-1, 0, 0, 2], 1),
+             (synth.gnp(200, 0.06, 9), [-1, 0, 0, 1, 1, 2, 2], 2)]
+    for g, parent, mode in cases:
+        k = len(parent)
+        col = oracle.color(g.n, k, 12)
+        want = oracle.dp_count(g, parent, col, oracle.NUM_LONGDOUBLE).total
+        for prec, tol in (("fp64", 1e-12), ("fp32", 1e-4)):
+            xs, st = run_ranks(g, parent, world, colors=col, precision=prec, segment_len=5, fixed_root=1)
+            assert len(set(xs)) == 1 and rel_err(xs[0], want) <= tol, (parent, prec)
+            assert all(s["fused_root"] == mode for s in st)
+
+
 def test_colouring_replicas_split_the_iterations():
     """Replicas: every rank the whole graph, iteration j on rank
     j mod world, one all-reduce of the per-iteration counts."""
