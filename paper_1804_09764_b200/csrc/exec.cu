@@ -25,8 +25,24 @@ namespace {
 
 void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<int64_t> &end, bool skip_empty,
                 Pass &w) {
-  // segment length s of Alg. 4; colour-group offsets are stored as uint16
-  const int64_t L = std::min<int64_t>(c->opt.segment_len > 0 ? c->opt.segment_len : 4096, 65535);
+  // segment length s of Alg. 4; colour-group offsets are stored as uint16.
+  // Auto: with W adjacency entries per resident warp (16 per SM), s ~
+  // sqrt(20 W) rounded to a power of two in [64, 4096], and 4096 once W >=
+  // 100K (measured optimum: configs[1] 128, [2] 512, [3] 4096 -- a long
+  // hub list on one warp is the tail of small graphs, partial-row traffic
+  // the cost of short segments on big ones)
+  int64_t L = c->opt.segment_len;
+  if (L <= 0) {
+    int64_t nnz_all = 0;
+    for (int64_t v = 0; v < (int64_t)beg.size(); ++v) nnz_all += end[v] - beg[v];
+    const double W = (double)nnz_all / (double)(std::max(c->num_sms, 1) * 16);
+    L = 4096;
+    if (W < 100000.0) {
+      L = 64;
+      while (L < 4096 && (double)(2 * L) <= std::sqrt(20.0 * W) * 1.414) L *= 2;
+    }
+  }
+  L = std::min<int64_t>(L, 65535);
   std::vector<int32_t> light, seg_v, seg_hv, hv_first, hv_nseg;
   std::vector<int64_t> seg_b, seg_e;
   int64_t nnz = 0;
