@@ -203,12 +203,15 @@ struct cc_ctx {
     }
     return ev_pool[ev_used++];
   }
+  bool phase_events = true;  // per-kernel event pairs for cc_last_profile (CC_PHASE_EVENTS=0: off)
   cudaEvent_t begin(cudaStream_t s) {
+    if (!phase_events) return nullptr;
     cudaEvent_t b = ev();
     CUDA_OK(cudaEventRecord(b, s));
     return b;
   }
   void end(int ph, cudaStream_t s, cudaEvent_t b) {
+    if (!phase_events || !b) return;
     cudaEvent_t e = ev();
     CUDA_OK(cudaEventRecord(e, s));
     ev_log.push_back({ph, {b, e}});

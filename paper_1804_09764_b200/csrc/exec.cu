@@ -423,6 +423,10 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   const Plan &pl = c->plan;
   const int k = pl.colours(), elem = c->elem();
   std::fill(c->stats, c->stats + 10, 0.0);
+  {
+    const char *pe = getenv("CC_PHASE_EVENTS");
+    c->phase_events = !(pe && pe[0] == '0');
+  }
   c->gather_log.clear();
   c->ev_used = 0;
   c->ev_log.clear();

@@ -354,6 +354,26 @@ def test_clique_every_entry_closed_form():
             assert_close_entries(got[xv][v], want, 1e-12, f"clique x={xv} v={v}")
 
 
+def test_maximum_template_size_k16():
+    """k = 16 (the library's maximum): P_16 on a long cycle with col = v mod 16
+    (every window rainbow: X = 2n exactly), and a 16-vertex tree on an R-MAT
+    graph against the oracle, fp64 per entry of the root counts."""
+    n = 160_000
+    assert count(synth.cycle(n), [-1] + list(range(15)), colors=(np.arange(n) % 16).astype(np.uint8)) == 2 * n
+    parent = [-1] + [(i - 1) // 2 for i in range(1, 15)] + [14]  # binary tree of 15 plus a leaf under a leaf
+    g = synth.rmat(9, 8, seed=3)
+    col = oracle.color(g.n, 16, 5)
+    want = oracle.dp_count(g, parent, col, oracle.NUM_LONGDOUBLE, want_root=True)
+    for prec, tol in (("fp64", TOL_FP64), ("fp32", TOL_FP32)):
+        with context(g, parent, prec) as ctx:
+            cc = lib()
+            cc.cc_set_colors(ctx, col)
+            assert rel_err(cc.cc_count_colorful(ctx), want.total) <= tol
+            if prec == "fp64":
+                root = cc.cc_get_subtree_counts(ctx, 0, g.n, 16, 16)
+                assert_close_entries(root[:, 0], want.root, TOL_FP64, "k=16 root")
+
+
 def test_path_on_long_cycle():
     # P_k on C_n with col = v mod k, k | n: every window is rainbow, X = 2n (SURVEY 8(c) pins)
     n, k = 200_004, 6
