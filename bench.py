@@ -315,6 +315,7 @@ def run_ours(args, cfg, rank, world, dist):
                 "gpu_launches": launches * args.steps,
                 "nvlink": ({"halo_bytes_received_per_step_rank0": stats["halo_bytes"],
                             "exchange_ms_per_step_rank0": last_prof["exchange"],
+                            "exposed_exchange_ms_per_step_rank0": last_prof.get("exposed_exchange"),
                             "gbs_rank0": (stats["halo_bytes"] / (last_prof["exchange"] * 1e-3) / 1e9
                                           if last_prof["exchange"] > 0 else None),
                             "peak_gbs": 900.0, "peak_source": "nominal NVLink 5 per direction per GPU"}

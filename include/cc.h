@@ -241,7 +241,9 @@ cc_status cc_get_subtree_counts(cc_ctx *ctx, int32_t x, double *out);
 cc_status cc_get_subtree_rows(cc_ctx *ctx, int32_t x, const int32_t *vertices, int32_t nv, double *out);
 
 /* Timing of the last cc_count_colorful, in ms, per phase (device events):
- * out[0] = total, then per DP step.  *n receives the number written. */
+ * out[0] = total, then colour, colour sort, leaf level, gathers, combines,
+ * root, exchange (comm stream), exposed exchange (main-stream wait for halo
+ * rows).  *n receives the number written. */
 cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
 
 /* Stats of the last cc_count_colorful: out[0] = U = sum over aggregations of

@@ -24,7 +24,7 @@ _lib = _native.lib
 LIB_PATH = _native.LIB_PATH
 
 # Phases reported by cc_last_profile (ms), in order.
-PROFILE_FIELDS = ["total", "color", "csort", "hist", "gather", "combine", "root", "exchange"]
+PROFILE_FIELDS = ["total", "color", "csort", "hist", "gather", "combine", "root", "exchange", "exposed_exchange"]
 
 
 class CCError(RuntimeError):

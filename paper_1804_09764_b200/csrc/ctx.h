@@ -31,7 +31,7 @@
 namespace cc {
 
 // Phases reported by cc_last_profile after "total": PROFILE order.
-enum Phase { PH_COLOR = 0, PH_CSORT, PH_HIST, PH_GATHER, PH_COMBINE, PH_ROOT, PH_EXCHANGE, PH_N };
+enum Phase { PH_COLOR = 0, PH_CSORT, PH_HIST, PH_GATHER, PH_COMBINE, PH_ROOT, PH_EXCHANGE, PH_EXPOSED, PH_N };
 
 // One aggregation pass over a range [beg[v], end[v]) of every owned row.
 struct Pass {

@@ -390,7 +390,9 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   // local part runs; then add the remote part.
   cudaEvent_t recvd = exchange_halo(c, P, p);
   gather_pass(c, c->p_local, P, p, N, 0);
+  cudaEvent_t wb = c->begin(c->s_main);  // exposed exchange: s_main idles until the halo rows are in
   CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
+  c->end(PH_EXPOSED, c->s_main, wb);
   gather_pass(c, c->p_remote, P, p, N, 1);
 }
 

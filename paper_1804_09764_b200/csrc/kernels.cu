@@ -353,9 +353,17 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
     const int64_t vb = tile * TV + (int64_t)lane * V;
     for (int zb = warp; zb < nblocks; zb += nwarp) {
       const uint16_t *e = zs + (size_t)zb * zld;
+      // block entries read 4 at a time (one 8-byte broadcast load per 4
+      // column indices instead of one 2-byte load each)
+      const uint2 *e4 = reinterpret_cast<const uint2 *>(e);
+      auto idx = [&](int i) -> uint32_t {
+        const uint2 w = e4[i >> 2];
+        const uint32_t h = (i & 2) ? w.y : w.x;
+        return (i & 1) ? h >> 16 : h & 0xFFFFu;
+      };
       LV nv[NN];
 #pragma unroll
-      for (int j = 0; j < NN; ++j) nv[j] = *reinterpret_cast<const LV *>(Nb + (uint32_t)e[NA + j] * CB);
+      for (int j = 0; j < NN; ++j) nv[j] = *reinterpret_cast<const LV *>(Nb + idx(NA + j) * CB);
       T acc[ZS][V];
 #pragma unroll
       for (int zz = 0; zz < ZS; ++zz)
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
         for (int i = 0; i < V; ++i) acc[zz][i] = (T)0;
 #pragma unroll
       for (int a = 0; a < NA; ++a) {
-        const LV av = *reinterpret_cast<const LV *>(Ab + (uint32_t)e[a] * CB);
+        const LV av = *reinterpret_cast<const LV *>(Ab + idx(a) * CB);
 #pragma unroll
         for (int q = 0; q <= PS; ++q)
 #pragma unroll
