@@ -111,7 +111,8 @@ RankPart partition_graph(const HostGraph &g, int world, int rank, uint64_t relab
     while (r < world) bound[r++] = nn;
   }
   // hubs first within each range; ties by original id (measured: keeping the
-  // generator's id order instead makes the gathers 20% slower on config 3)
+  // generator's id order makes the gathers 20% slower on config 3, a BFS
+  // (Cuthill-McKee) order from the hubs 27% slower)
   for (int r = 0; r < world; ++r)
     std::sort(nz.begin() + bound[r], nz.begin() + bound[r + 1], [&](int32_t a, int32_t b) {
       int64_t da = deg(a), db = deg(b);
