@@ -156,6 +156,10 @@ def cc_get_subtree_counts(ctx, x: int, n: int, k: int, size: int) -> np.ndarray:
     return out
 
 
+def cc_set_profiling(ctx, on: bool) -> None:
+    _check(ctx, _lib.cc_set_profiling(ctx, 1 if on else 0))
+
+
 def cc_last_profile(ctx) -> dict:
     buf = np.zeros(16, dtype=np.float64)
     n = ctypes.c_int32()

@@ -460,6 +460,12 @@ cc_status cc_get_subtree_rows(cc_ctx *c, int32_t x, const int32_t *vertices, int
   API_END(c)
 }
 
+cc_status cc_set_profiling(cc_ctx *c, int32_t on) {
+  if (!c) return CC_ERR_ARG;
+  c->profiling = on != 0;
+  return CC_OK;
+}
+
 cc_status cc_last_profile(cc_ctx *c, double *ms, int32_t cap, int32_t *n) {
   if (!c || !ms) return CC_ERR_ARG;
   const int m = std::min<int>(cap, cc::PH_N + 1);

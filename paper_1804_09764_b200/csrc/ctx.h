@@ -203,6 +203,7 @@ struct cc_ctx {
     }
     return ev_pool[ev_used++];
   }
+  bool profiling = true;     // cc_set_profiling
   bool phase_events = true;  // per-kernel event pairs for cc_last_profile (CC_PHASE_EVENTS=0: off)
   cudaEvent_t begin(cudaStream_t s) {
     if (!phase_events) return nullptr;

@@ -427,7 +427,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   std::fill(c->stats, c->stats + 10, 0.0);
   {
     const char *pe = getenv("CC_PHASE_EVENTS");
-    c->phase_events = !(pe && pe[0] == '0');
+    c->phase_events = c->profiling && !(pe && pe[0] == '0');
   }
   c->gather_log.clear();
   c->ev_used = 0;
