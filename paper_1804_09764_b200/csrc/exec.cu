@@ -529,7 +529,12 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     for (int s = 0; s < (int)pl.steps.size(); ++s)
       if (pl.steps[s].out >= 0) producer[pl.steps[s].out] = s;
     std::fill(need.begin(), need.end(), 0);
-    std::function<void(int)> mark = [&](int id) {
+    std::function<void(int)> mark;
+    // a passive table is needed only when its neighbour sum is not cached
+    auto mark_passive = [&](int id) {
+      if (id >= 0 && !cache->tables.count("N" + pl.tables[id].code)) mark(id);
+    };
+    mark = [&](int id) {
       if (id < 0 || need[id]) return;
       if (cache->tables.count(pl.tables[id].code)) {
         need[id] = 2;  // cached
@@ -538,10 +543,10 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       need[id] = 1;
       const Step &ps = pl.steps[producer[id]];
       mark(ps.active);
-      mark(ps.passive);
+      mark_passive(ps.passive);
     };
     mark(pl.steps.back().active);
-    mark(pl.steps.back().passive);
+    mark_passive(pl.steps.back().passive);
   }
 
   for (int s = 0; s < (int)pl.steps.size(); ++s) {
@@ -605,8 +610,22 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     } else {
       const int P = st.passive;
       if (Nb[P] < 0) {
-        Nb[P] = bufs.make((size_t)rows * c->ld_of(Wp) * elem);
-        aggregate(c, bufs.ptr(T[P]), st.p, bufs.ptr(Nb[P]));
+        const std::string nkey = cache ? "N" + pl.tables[P].code : std::string();
+        if (cache && cache->tables.count(nkey)) {  // neighbour sum of an earlier template
+          const auto &e = cache->tables[nkey];
+          Nb[P] = bufs.alias(e.first, e.second);
+          ++cache->reused;
+        } else {
+          Nb[P] = bufs.make((size_t)rows * c->ld_of(Wp) * elem);
+          aggregate(c, bufs.ptr(T[P]), st.p, bufs.ptr(Nb[P]));
+          Buf &bb = bufs.pool[Nb[P]];
+          if (cache && cache->bytes + bb.bytes <= cache->budget) {
+            cache->tables[nkey] = {bb.p, bb.bytes};
+            cache->bytes += bb.bytes;
+            bb.owned = false;
+            ++cache->stored;
+          }
+        }
       }
       nbuf = Nb[P];
     }
