@@ -193,10 +193,10 @@ cc_status cc_estimate(cc_ctx *ctx, int32_t iterations, uint64_t seed0, double *e
  * (sizes[i] vertices, its parent array at parents + sizes[0] + ... +
  * sizes[i-1]) for the colouring set by cc_color / cc_set_colors, whose
  * colours (cc_set_template_colors) must be >= every sizes[i].  Isomorphic
- * rooted sub-templates are computed once across the templates (kept while
- * they fit a quarter of the free device memory), and so are the colour sort
- * and the leaf level; out[9] of cc_last_stats then gives the number of
- * tables reused.  One GPU (or replica mode).  The context's own template is
+ * rooted sub-templates are computed once across the templates, and so are
+ * the neighbour sums of such passive parts (both kept while they fit a
+ * quarter of the free device memory), the colour sort and the leaf level;
+ * out[9] of cc_last_stats then gives the number of tables and sums reused.  One GPU (or replica mode).  The context's own template is
  * restored afterwards. */
 cc_status cc_count_colorful_multi(cc_ctx *ctx, int32_t n_templates, const int32_t *sizes, const int32_t *parents,
                                   double *X);
