@@ -316,6 +316,10 @@ def run_ours(args, cfg, rank, world, dist):
                 "nvlink": ({"halo_bytes_received_per_step_rank0": stats["halo_bytes"],
                             "exchange_ms_per_step_rank0": last_prof["exchange"],
                             "exposed_exchange_ms_per_step_rank0": last_prof.get("exposed_exchange"),
+                            # overlap ratio: share of the exchange hidden behind
+                            # the local gathers on rank 0
+                            "overlap_ratio_rank0": (1.0 - last_prof.get("exposed_exchange", 0.0) / last_prof["exchange"]
+                                                    if last_prof["exchange"] > 0 else None),
                             "gbs_rank0": (stats["halo_bytes"] / (last_prof["exchange"] * 1e-3) / 1e9
                                           if last_prof["exchange"] > 0 else None),
                             "peak_gbs": 900.0, "peak_source": "nominal NVLink 5 per direction per GPU"}
