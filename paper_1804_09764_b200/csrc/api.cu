@@ -54,6 +54,8 @@ void free_persistent(cc_ctx *c) {
   c->d_ztab.clear();
   c->zblocks.clear();
   c->d_map.clear();
+  c->d_skip.clear();
+  c->skip_words.clear();
   c->d_comp = nullptr;
   c->d_partials = c->d_result = nullptr;
   c->d_arrive = nullptr;

@@ -167,3 +167,28 @@ int64_t zblock_ld(int ts, int as) {
 }
 
 }  // namespace cc
+
+namespace cc {
+
+std::vector<uint32_t> skip_table(int k, int p, int elem, int *words) {
+  const int K = k - 1, s = p - 1;
+  const int64_t W = binom(K, s);
+  const int vw = 16 / elem, se = 32 / elem;  // entries per 16-byte vector / 32-byte sector
+  const int64_t nvec = (W + vw - 1) / vw;
+  const int nw = (int)((nvec + 31) / 32) + 4;  // + slack: the kernel may address (pass, j) words past the row
+  std::vector<uint32_t> out((size_t)K * nw, 0);
+  std::vector<uint32_t> sets((size_t)W);
+  for (int64_t r = 0; r < W; ++r) sets[r] = colex_unrank(s, r);
+  for (int c = 0; c < K; ++c)
+    for (int64_t vi = 0; vi < nvec; ++vi) {
+      const int64_t s0 = vi * vw / se * se;
+      bool useless = true;
+      for (int64_t e = s0; e < s0 + se && useless; ++e)
+        if (e < W && !(sets[e] >> c & 1u)) useless = false;
+      if (useless) out[(size_t)c * nw + vi / 32] |= 1u << (vi % 32);
+    }
+  *words = nw;
+  return out;
+}
+
+}  // namespace cc

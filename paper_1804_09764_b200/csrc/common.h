@@ -41,6 +41,12 @@ uint32_t unsqueeze(uint32_t mask, int c);
 // (k-1)-universe of cu), out[(cu*k + cv) * C(k-1,p-1) + r] = rank of
 // sq_cv({cu} u us_cu(Y')) in C(k-1, p), or 0xFFFF if that set contains cv.
 std::vector<uint16_t> gather_map(int k, int p);
+// Sector-skip table of a passive part of size p (rows of C(k-1, p-1) entries
+// of elem bytes): for each colour c' of the (k-1)-universe, bit (vi mod 32)
+// of word (vi / 32) marks 16-byte vector vi of a row whose whole 32-byte
+// sector holds only sets containing c' (or padding) -- entries no
+// destination of that colour can use.  *words receives the words per colour.
+std::vector<uint32_t> skip_table(int k, int p, int elem, int *words);
 int64_t gather_map_ld(int k, int p);  // map row stride: C(k-1,p-1) rounded up to 8 (padding 0xFFFF)
 
 // Z-block cover of a combine step with outputs of size ts = t-1, actives of

@@ -120,6 +120,8 @@ struct cc_ctx {
   std::vector<uint16_t *> d_ztab;     // per step: Z-block cover table (nullptr if none)
   std::vector<int> zblocks;
   std::vector<uint16_t *> d_map;      // per passive size p: gather map (p >= 2)
+  std::vector<uint32_t *> d_skip;     // per passive size p: sector-skip table
+  std::vector<int> skip_words;
   uint16_t *d_comp = nullptr;         // root step complement table
   bool has_colors = false;
   bool sorted_valid = false;          // colour-sorted adjacency matches the colouring

@@ -165,11 +165,14 @@ void upload_template(cc_ctx *c) {
   for (auto *p : c->d_split) c->pfree(p);
   for (auto *p : c->d_ztab) c->pfree(p);
   for (auto *p : c->d_map) c->pfree(p);
+  for (auto *p : c->d_skip) c->pfree(p);
   c->pfree(c->d_comp);
   c->d_split.assign(c->plan.steps.size(), nullptr);
   c->d_ztab.assign(c->plan.steps.size(), nullptr);
   c->zblocks.assign(c->plan.steps.size(), 0);
   c->d_map.assign(kMaxK + 1, nullptr);
+  c->d_skip.assign(kMaxK + 1, nullptr);
+  c->skip_words.assign(kMaxK + 1, 0);
   c->d_comp = nullptr;
   const int k = c->plan.colours();
   for (size_t s = 0; s < c->plan.steps.size(); ++s) {
@@ -194,7 +197,13 @@ void upload_template(cc_ctx *c) {
         c->zblocks[s] = nb;
       }
     }
-    if (st.p > 1 && !c->d_map[st.p]) c->d_map[st.p] = c->pupload(gather_map(k, st.p));
+    if (st.p > 1 && !c->d_map[st.p]) {
+      c->d_map[st.p] = c->pupload(gather_map(k, st.p));
+      int nw = 0;
+      const std::vector<uint32_t> sk = skip_table(k, st.p, c->elem(), &nw);
+      c->d_skip[st.p] = c->pupload(sk);
+      c->skip_words[st.p] = nw;
+    }
   }
 }
 
@@ -246,6 +255,13 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   a.W_in = W_in;
   a.map = c->d_map[p];
   a.map_ld = gather_map_ld(k, p);
+  {
+    const char *sk = getenv("CC_SECTOR_SKIP");
+    if (!(sk && sk[0] == '0')) {
+      a.skip = c->d_skip[p];
+      a.skip_words = c->skip_words[p];
+    }
+  }
   {  // hub rows kept in L2: a fraction of the L2 (rows are degree-ordered, hubs first)
     const char *f = getenv("CC_HUB_L2_FRAC");
     const double frac = f ? atof(f) : 0.5;

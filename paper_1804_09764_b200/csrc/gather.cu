@@ -686,6 +686,18 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
         const int cu = __ffs(g) - 1;
         const int lo = cu == 0 ? 0 : __shfl_sync(0xffffffffu, hi_l, cu - 1);
         const int hi = __shfl_sync(0xffffffffu, hi_l, cu);
+        // the lane's vectors whose whole 32-byte sector holds only colour sets
+        // that contain v's colour (in u's universe): never used by v, not read
+        bool use[NV];
+        {
+          const int cvu = cv < cu ? cv : cv - 1;  // sq_{c_u}(c_v)
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            use[j] = valid[j];
+            if (a.skip && valid[j])
+              use[j] = !((__ldg(a.skip + (int64_t)cvu * a.skip_words + ch * NV + j) >> lane) & 1u);
+          }
+        }
         // colour-pair map of this group, for the lane's columns
         uint16_t m[NV][VW];
         const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
@@ -729,7 +741,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
               const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
 #pragma unroll
               for (int j = 0; j < NV; ++j)
-                if (valid[j]) x[uu][j] = __ldg(row + 32 * j);
+                if (use[j]) x[uu][j] = __ldg(row + 32 * j);
             }
 #pragma unroll
             for (int uu = 0; uu < U; ++uu)
@@ -743,7 +755,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
               const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
 #pragma unroll
               for (int j = 0; j < NV; ++j) {
-                if (r + uu < cnt && valid[j]) x[uu][j] = __ldg(row + 32 * j);
+                if (r + uu < cnt && use[j]) x[uu][j] = __ldg(row + 32 * j);
                 else zero_vec(x[uu][j]);
               }
             }

@@ -58,6 +58,8 @@ struct GatherArgs {
   int W_in;
   const uint16_t *map;    // [c_u][c_v][map_ld] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
   int64_t map_ld;         // map row stride (multiple of 8 entries, padding = 0xFFFF)
+  const uint32_t *skip = nullptr;  // [k-1][skip_words]: bit v of word w set = 16-byte vector 32 w + v of a
+  int skip_words = 0;               // row lies in a 32-byte sector of sets that all contain that colour
   int64_t hub_rows;       // rows [0, hub_rows) of src are gathered with an L2 evict-last policy
   void *dst;              // N'' (rows x ld_dst), W_out = C(k-1, p)
   int64_t ld_dst;
