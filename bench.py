@@ -46,6 +46,8 @@ def parse():
                     help="N > 1: colouring replicas (each GPU the whole graph, different colourings; SURVEY F1) "
                          "instead of the 1D vertex partition")
     ap.add_argument("--segment-len", type=int, default=0)
+    ap.add_argument("--exchange", default="auto", choices=["auto", "grouped", "ring"],
+                    help="halo-exchange schedule of the 1D partition (PAPER.md Alg. 3)")
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-scale", type=int, default=0, help="R-MAT scale of the oracle sample (0 = auto)")
@@ -202,6 +204,8 @@ def run_ours(args, cfg, rank, world, dist):
     torch.cuda.set_device(local)
     g = cfg.graph()
     kw = dict(precision=cc.CC_FP64 if precision == "fp64" else cc.CC_FP32, segment_len=args.segment_len,
+              exchange={"auto": cc.CC_EXCHANGE_AUTO, "grouped": cc.CC_EXCHANGE_GROUPED,
+                        "ring": cc.CC_EXCHANGE_RING}[args.exchange],
               replicas=1 if (args.replicas and world > 1) else 0)
     if world > 1:
         opt, _idbuf = cc.distributed_options(**kw)
@@ -313,7 +317,8 @@ def run_ours(args, cfg, rank, world, dist):
                         "d2h_bytes_per_step": 8, "ms_per_step": e2e_s * 1e3,
                         "api": "cc_set_colors(host colouring) + cc_count_colorful"},
                 "gpu_launches": launches * args.steps,
-                "nvlink": ({"halo_bytes_received_per_step_rank0": stats["halo_bytes"],
+                "nvlink": ({"schedule": {1: "grouped", 2: "ring"}.get(stats["exchange"]),
+                            "halo_bytes_received_per_step_rank0": stats["halo_bytes"],
                             "exchange_ms_per_step_rank0": last_prof["exchange"],
                             "exposed_exchange_ms_per_step_rank0": last_prof.get("exposed_exchange"),
                             # overlap ratio: share of the exchange hidden behind

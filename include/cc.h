@@ -67,6 +67,20 @@ enum {
                   fp64 root products and fp64 final reduction */
 };
 
+/* Halo-exchange schedule of the 1D partition (cc_options.exchange; PAPER.md
+ * Alg. 3 "Adaptive-Group", lines 275-341). */
+enum {
+  CC_EXCHANGE_AUTO = 0,    /* pick by the pipeline cost model (cc_exchange_model),
+                              the maximum over ranks, the same on every rank */
+  CC_EXCHANGE_GROUPED = 1, /* one grouped send/recv with every peer (the
+                              all-to-all branch, Alg. 3 line 15), overlapped with
+                              the local neighbour sum, then one remote pass */
+  CC_EXCHANGE_RING = 2     /* world - 1 steps: step r sends to rank + r and
+                              receives from rank - r (Alg. 3 lines 2-6), the
+                              remote neighbour sum over step r's rows runs while
+                              step r + 1 transfers (the pipeline, lines 326-341) */
+};
+
 typedef struct {
   int32_t precision;     /* CC_FP64 or CC_FP32 */
   int32_t device;        /* CUDA device ordinal for this rank */
@@ -106,6 +120,7 @@ typedef struct {
                             process, possibly on one GPU; halo rows move with
                             event-ordered device copies, reductions on the
                             host (no kernel waits for another rank) */
+  int32_t exchange;      /* CC_EXCHANGE_*; world > 1, replicas = 0 only */
 } cc_options;
 
 /* Fill *opt with defaults: CC_FP64, device 0, world 1, rank 0, auto sizes,
@@ -261,7 +276,9 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * the lifted neighbour sum), out[6] / out[7] (cap >= 8) = algorithmic bytes
  * and device ms of the longest neighbour-sum launch, out[8] = number of
  * neighbour-sum launches, out[9] = halo bytes received by this rank (1D
- * partition).  cap >= 5. */
+ * partition), out[10] (cap >= 11) = the exchange schedule in use
+ * (0: none -- one rank or replicas, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING).
+ * cap >= 5. */
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
 
 /* ---- host-only introspection (no GPU needed; used by CPU tests) --------- */
@@ -334,6 +351,16 @@ cc_status cc_partition_plan(int64_t n, const int64_t *row_ptr, const int32_t *co
                             int32_t rank, uint64_t relabel_seed, int64_t *sizes_out,
                             int32_t *own_orig, int32_t *halo_orig, int64_t *recv_off,
                             int64_t *send_off, int32_t *send_idx, int64_t *rp, int32_t *lcol);
+
+/* The exchange cost model behind CC_EXCHANGE_AUTO for rank `rank` of `world`
+ * (host only; the partition as cc_partition_plan): out[0] = modelled seconds
+ * of one neighbour sum of a table with `row_bytes`-byte rows under the
+ * grouped schedule, out[1] = under the ring pipeline, out[2] / out[3] = the
+ * link and gather rates assumed (bytes/s).  cc_load_graph takes the maximum
+ * of each over the ranks and runs the ring when it is below the grouped
+ * figure. */
+cc_status cc_exchange_model(int64_t n, const int64_t *row_ptr, const int32_t *col, int32_t world, int32_t rank,
+                            uint64_t relabel_seed, double row_bytes, double *out);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,8 @@ import numpy as np
 
 from . import _native
 from ._native import (CC_ERR_ARG, CC_ERR_CUDA, CC_ERR_GRAPH, CC_ERR_NCCL, CC_ERR_NONFINITE,  # noqa: F401
-                      CC_ERR_OOM, CC_ERR_STATE, CC_ERR_TEMPLATE, CC_FP32, CC_FP64, CC_OK, STATUS_NAMES,
+                      CC_ERR_OOM, CC_ERR_STATE, CC_ERR_TEMPLATE, CC_EXCHANGE_AUTO, CC_EXCHANGE_GROUPED,
+                      CC_EXCHANGE_RING, CC_FP32, CC_FP64, CC_OK, STATUS_NAMES,
                       cc_options)
 
 _lib = _native.lib
@@ -197,11 +198,11 @@ def cc_get_subtree_rows(ctx, x: int, vertices, k: int, s: int) -> np.ndarray:
 
 
 def cc_last_stats(ctx) -> dict:
-    buf = np.zeros(10, dtype=np.float64)
-    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 10))
+    buf = np.zeros(11, dtype=np.float64)
+    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 11))
     return dict(updates=buf[0], model_bytes=buf[1], agg_bytes=buf[2], launches=buf[3], peak_table_bytes=buf[4],
                 fused_root=int(buf[5]), top_gather_bytes=buf[6], top_gather_ms=buf[7], gather_launches=int(buf[8]),
-                halo_bytes=buf[9])
+                halo_bytes=buf[9], exchange=int(buf[10]))
 
 
 # ------------------------------------------------------------------ host-only
@@ -266,6 +267,16 @@ def cc_partition_plan(n: int, row_ptr, col, world: int, rank: int, relabel_seed:
                                         _p(send_idx), _p(lrp), _p(lcol)))
     return dict(own_orig=own, halo_orig=halo, recv_off=recv_off, send_off=send_off, send_idx=send_idx,
                 rp=lrp, col=lcol)
+
+
+def cc_exchange_model(n: int, row_ptr, col, world: int, rank: int, row_bytes: float = 1024.0,
+                      relabel_seed: int = 0x5eed) -> dict:
+    """The cost model behind CC_EXCHANGE_AUTO for one rank (host only)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cl = np.ascontiguousarray(col, dtype=np.int32)
+    out = np.zeros(4, dtype=np.float64)
+    _check(None, _lib.cc_exchange_model(n, _p(rp), _p(cl), world, rank, relabel_seed, float(row_bytes), _p(out)))
+    return dict(grouped_s=out[0], ring_s=out[1], link_bps=out[2], gather_bps=out[3])
 
 
 # ------------------------------------------------------------------ torch.distributed plumbing

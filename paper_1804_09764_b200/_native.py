@@ -24,12 +24,13 @@ class cc_options(ctypes.Structure):
     _fields_ = [("precision", c_i32), ("device", c_i32), ("world", c_i32), ("rank", c_i32),
                 ("nccl_id", vp), ("chunk_cols", c_i64), ("segment_len", c_i32),
                 ("use_graphs", c_i32), ("relabel_seed", c_u64), ("fixed_root", c_i32), ("replicas", c_i32),
-                ("loopback", vp)]
+                ("loopback", vp), ("exchange", c_i32)]
 
 
 CC_OK, CC_ERR_ARG, CC_ERR_GRAPH, CC_ERR_TEMPLATE, CC_ERR_STATE, CC_ERR_OOM, CC_ERR_CUDA, \
     CC_ERR_NCCL, CC_ERR_NONFINITE = range(9)
 CC_FP64, CC_FP32 = 0, 1
+CC_EXCHANGE_AUTO, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING = 0, 1, 2
 STATUS_NAMES = ["CC_OK", "CC_ERR_ARG", "CC_ERR_GRAPH", "CC_ERR_TEMPLATE", "CC_ERR_STATE", "CC_ERR_OOM",
                 "CC_ERR_CUDA", "CC_ERR_NCCL", "CC_ERR_NONFINITE"]
 
@@ -67,6 +68,7 @@ SIGNATURES = {
     "cc_plan_template": (c_i32, [c_i32, vp, vp, c_i32, vp, vp, vp, vp, vp]),
     "cc_plan_template_auto": (c_i32, [c_i32, vp, c_dbl, c_i32, vp, c_i32, vp, vp, vp]),
     "cc_partition_plan":(c_i32, [c_i64, vp, vp, c_i32, c_i32, c_u64, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "cc_exchange_model": (c_i32, [c_i64, vp, vp, c_i32, c_i32, c_u64, c_dbl, vp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

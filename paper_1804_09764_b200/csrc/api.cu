@@ -50,6 +50,8 @@ void free_persistent(cc_ctx *c) {
   c->d_col = c->d_col_sorted = c->d_orig = c->d_send_idx = nullptr;
   c->d_colors = nullptr;
   c->p_full = c->p_local = c->p_remote = cc::Pass();
+  c->p_peer.clear();
+  c->xmode = 0;
   c->d_split.clear();
   c->d_ztab.clear();
   c->zblocks.clear();
@@ -118,6 +120,7 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   if (opt->world > 1 && !opt->nccl_id && !opt->loopback) return CC_ERR_ARG;
   if (opt->chunk_cols != 0 || opt->segment_len < 0 || opt->use_graphs < 0 || opt->use_graphs > 1) return CC_ERR_ARG;
   if (opt->replicas < 0 || opt->replicas > 1) return CC_ERR_ARG;
+  if (opt->exchange < CC_EXCHANGE_AUTO || opt->exchange > CC_EXCHANGE_RING) return CC_ERR_ARG;
   std::unique_ptr<cc_ctx> c(new cc_ctx());
   c->opt = *opt;
   c->opt.nccl_id = nullptr;
@@ -479,7 +482,7 @@ cc_status cc_last_profile(cc_ctx *c, double *ms, int32_t cap, int32_t *n) {
 
 cc_status cc_last_stats(cc_ctx *c, double *out, int32_t cap) {
   if (!c || !out || cap < 5) return CC_ERR_ARG;
-  for (int i = 0; i < std::min<int32_t>(cap, 10); ++i) out[i] = c->stats[i];
+  for (int i = 0; i < std::min<int32_t>(cap, 11); ++i) out[i] = c->stats[i];
   return CC_OK;
 }
 
@@ -616,6 +619,23 @@ cc_status cc_partition_plan(int64_t n, const int64_t *row_ptr, const int32_t *co
     if (send_idx) std::copy(R.send_idx.begin(), R.send_idx.end(), send_idx);
     if (rp) std::copy(R.rp.begin(), R.rp.end(), rp);
     if (lcol) std::copy(R.col.begin(), R.col.end(), lcol);
+  } catch (const Error &e) {
+    return e.status;
+  }
+  return CC_OK;
+}
+
+cc_status cc_exchange_model(int64_t n, const int64_t *row_ptr, const int32_t *col, int32_t world, int32_t rank,
+                            uint64_t relabel_seed, double row_bytes, double *out) {
+  try {
+    if (!out || world < 2 || rank < 0 || rank >= world || !(row_bytes > 0)) return CC_ERR_ARG;
+    cc::HostGraph g = cc::validate_graph(n, row_ptr, col);
+    cc::RankPart R = cc::partition_graph(g, world, rank, relabel_seed);
+    const cc::ExchangeModel m = cc::model_exchange(R, cc::peer_bounds(R), row_bytes);
+    out[0] = m.grouped_s;
+    out[1] = m.ring_s;
+    out[2] = m.link_bps;
+    out[3] = m.gather_bps;
   } catch (const Error &e) {
     return e.status;
   }

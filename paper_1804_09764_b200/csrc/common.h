@@ -141,4 +141,22 @@ struct RankPart {
 };
 RankPart partition_graph(const HostGraph &g, int world, int rank, uint64_t relabel_seed);
 
+// Per-peer split of every owned row's halo range: the neighbours of row i
+// owned by peer q (Alg. 3's per-step set N_{r,w}(v))
+// are positions [b[q * n_own + i], b[(q + 1) * n_own + i]) of the local CSR;
+// q = world is rp[i + 1].  (world + 1) x n_own entries.
+std::vector<int64_t> peer_bounds(const RankPart &R);
+
+// Modelled time of one neighbour sum of a table with `row_bytes`-byte rows
+// on this rank under the two exchange schedules (Alg. 3 and the
+// pipeline analysis, lines 326-341, 420-441): grouped = one all-to-all of
+// the halo rows overlapped with the local part, then one remote pass;
+// ring = P - 1 steps (send to rank + r, receive from rank - r), the remote
+// pass of step r overlapping the transfer of step r + 1.
+struct ExchangeModel {
+  double grouped_s = 0, ring_s = 0;
+  double link_bps = 0, gather_bps = 0;
+};
+ExchangeModel model_exchange(const RankPart &R, const std::vector<int64_t> &bounds, double row_bytes);
+
 }  // namespace cc

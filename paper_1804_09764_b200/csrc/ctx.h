@@ -109,6 +109,9 @@ struct cc_ctx {
   uint8_t *d_color_stage = nullptr;  // n_global bytes: a caller's colouring in original order
   unsigned *d_bad = nullptr;
   cc::Pass p_full, p_local, p_remote;  // world 1: p_full; world > 1: p_local + p_remote (+ p_full for hist)
+  std::vector<cc::Pass> p_peer;        // ring exchange: the remote pass per source peer (replaces p_remote)
+  int xmode = 0;                       // exchange schedule in use: 0 none, CC_EXCHANGE_GROUPED / _RING
+  double xmodel[2] = {0, 0};           // modelled grouped / ring seconds (max over ranks)
   int64_t max_seg = 0, max_hv = 0;
 
   // template
@@ -136,7 +139,7 @@ struct cc_ctx {
 
   // profile / stats of the last count
   double prof[cc::PH_N + 1] = {0};
-  double stats[10] = {0};
+  double stats[11] = {0};
   std::vector<std::pair<size_t, double>> gather_log;  // (ev_log index, algorithmic bytes) per gather launch
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;
   std::vector<cudaEvent_t> ev_pool;

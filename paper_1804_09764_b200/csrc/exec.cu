@@ -109,6 +109,8 @@ struct Bufs {
 
 }  // namespace
 
+void allreduce_host(cc_ctx *c, std::vector<double> &v);
+
 void load_graph(cc_ctx *c, const HostGraph &g) {
   c->part = partition_graph(g, c->pworld(), c->pworld() == 1 ? 0 : c->opt.rank, c->opt.relabel_seed);
   const auto &R = c->part;
@@ -133,15 +135,52 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
   c->p_full.end = c->d_rp + 1;
   c->p_full.col_sorted = c->d_col_sorted;  // world > 1: its own buffer, allocated for the fused root
   if (c->pworld() > 1) {
+    const int W = c->pworld(), me = c->opt.rank;
     c->d_mid = c->pupload(R.mid);
     c->d_send_idx = c->pupload(R.send_idx);
     build_pass(c, beg, R.mid, false, c->p_local);
-    build_pass(c, R.mid, end, true, c->p_remote);
     c->p_local.beg = c->d_rp;
     c->p_local.end = c->d_mid;
-    c->p_remote.beg = c->d_mid;
-    c->p_remote.end = c->d_rp + 1;
-    c->p_local.col_sorted = c->p_remote.col_sorted = c->d_col_sorted;
+    c->p_local.col_sorted = c->d_col_sorted;
+    // exchange schedule (Alg. 3 "Adaptive-Group"): the same on every rank --
+    // the cost model's maximum over the ranks when auto
+    const std::vector<int64_t> bnd = peer_bounds(R);
+    {
+      const ExchangeModel m = model_exchange(R, bnd, 1024.0);
+      std::vector<double> v(2 * (size_t)W, 0.0);
+      v[2 * me] = m.grouped_s;
+      v[2 * me + 1] = m.ring_s;
+      allreduce_host(c, v);
+      c->xmodel[0] = c->xmodel[1] = 0;
+      for (int q = 0; q < W; ++q) {
+        c->xmodel[0] = std::max(c->xmodel[0], v[2 * q]);
+        c->xmodel[1] = std::max(c->xmodel[1], v[2 * q + 1]);
+      }
+    }
+    c->xmode = c->opt.exchange != CC_EXCHANGE_AUTO ? c->opt.exchange
+               : c->xmodel[1] < c->xmodel[0]        ? CC_EXCHANGE_RING
+                                                    : CC_EXCHANGE_GROUPED;
+    if (c->xmode == CC_EXCHANGE_RING) {
+      // one remote pass per source peer: its neighbours of each owned row
+      const int64_t n = R.n_own;
+      int64_t *d_b = c->pupload(bnd);
+      c->p_peer.assign(W, Pass());
+      for (int q = 0; q < W; ++q) {
+        if (q == me || R.recv_off[q + 1] == R.recv_off[q]) continue;
+        std::vector<int64_t> b0(bnd.begin() + (size_t)q * n, bnd.begin() + (size_t)(q + 1) * n),
+            b1(bnd.begin() + (size_t)(q + 1) * n, bnd.begin() + (size_t)(q + 2) * n);
+        Pass &w = c->p_peer[q];
+        build_pass(c, b0, b1, true, w);
+        w.beg = d_b + (size_t)q * n;
+        w.end = d_b + (size_t)(q + 1) * n;
+        w.col_sorted = c->d_col_sorted;
+      }
+    } else {
+      build_pass(c, R.mid, end, true, c->p_remote);
+      c->p_remote.beg = c->d_mid;
+      c->p_remote.end = c->d_rp + 1;
+      c->p_remote.col_sorted = c->d_col_sorted;
+    }
     c->p_full.col_sorted = nullptr;
     c->d_col_sorted_full = nullptr;
   }
@@ -311,24 +350,32 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
 // Loopback transport (cc_options.loopback): the halo rows of this rank come
 // from the peers' send buffers by device copies ordered by the peers' pack
 // events; this rank's send buffer is released only after every peer's copy.
-void loopback_exchange(cc_ctx *c, void *sendbuf, void *P, int64_t ld, int elem) {
+void loopback_exchange(cc_ctx *c, void *sendbuf, void *P, int64_t ld, int elem,
+                       std::vector<std::pair<int, cudaEvent_t>> *steps) {
   LoopbackGroup &G = *c->loop;
   const auto &R = c->part;
-  const int me = c->opt.rank;
+  const int me = c->opt.rank, W = G.world;
+  const bool ring = c->xmode == CC_EXCHANGE_RING;
   cudaEvent_t packed = c->ev(), copied = c->ev();
   CUDA_OK(cudaEventRecord(packed, c->s_comm));
   G.ptr[me] = sendbuf;
   G.offs[me] = R.send_off.data();
   G.ev[me] = packed;
   G.rendezvous();
-  for (int q = 0; q < G.world; ++q) {
-    if (q == me) continue;
+  for (int r = 1; r < W; ++r) {
+    const int q = ring ? (me - r + W) % W : (me + r) % W;  // ring: step r receives from rank - r
     const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
-    if (!nr) continue;
-    CUDA_OK(cudaStreamWaitEvent(c->s_comm, G.ev[q], 0));
-    CUDA_OK(cudaMemcpyAsync(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[q]) * ld * elem,
-                            static_cast<const char *>(G.ptr[q]) + (size_t)G.offs[q][me] * ld * elem,
-                            (size_t)nr * ld * elem, cudaMemcpyDeviceToDevice, c->s_comm));
+    if (nr) {
+      CUDA_OK(cudaStreamWaitEvent(c->s_comm, G.ev[q], 0));
+      CUDA_OK(cudaMemcpyAsync(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[q]) * ld * elem,
+                              static_cast<const char *>(G.ptr[q]) + (size_t)G.offs[q][me] * ld * elem,
+                              (size_t)nr * ld * elem, cudaMemcpyDeviceToDevice, c->s_comm));
+    }
+    if (ring && steps) {
+      cudaEvent_t e = c->ev();
+      CUDA_OK(cudaEventRecord(e, c->s_comm));
+      steps->push_back({q, e});
+    }
   }
   CUDA_OK(cudaEventRecord(copied, c->s_comm));
   G.ev2[me] = copied;
@@ -357,7 +404,9 @@ void loopback_allreduce(cc_ctx *c, double *d, size_t count, cudaStream_t s) {
 // world > 1: send this rank's boundary rows of P' to the peers that need
 // them and receive the halo rows (after the owned rows of P') on the comm
 // stream; returns an event recorded when the halo rows have arrived.
-cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p) {
+// ring schedule: *steps (nullable) receives (source peer, event recorded
+// when that peer's rows have arrived) in step order.
+cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p, std::vector<std::pair<int, cudaEvent_t>> *steps = nullptr) {
   auto &api = nccl();
   const int k = c->plan.colours(), elem = c->elem();
   const int64_t ld = c->ld_of(binom(k - 1, p - 1));
@@ -373,7 +422,28 @@ cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p) {
   c->check_launch();
   const ncclDataType_t dt = elem == 8 ? ncclFloat64 : ncclFloat32;
   if (c->loop) {
-    loopback_exchange(c, sendbuf, P, ld, elem);
+    loopback_exchange(c, sendbuf, P, ld, elem, steps);
+  } else if (c->xmode == CC_EXCHANGE_RING) {
+    // Alg. 3 lines 2-6: step r sends to rank + r and receives from rank - r
+    const int W = c->pworld(), me = c->opt.rank;
+    for (int r = 1; r < W; ++r) {
+      const int dst = (me + r) % W, src = (me - r + W) % W;
+      const int64_t ns = R.send_off[dst + 1] - R.send_off[dst];
+      const int64_t nr = R.recv_off[src + 1] - R.recv_off[src];
+      NCCL_OK(api.GroupStart());
+      if (ns)
+        NCCL_OK(api.Send(static_cast<char *>(sendbuf) + (size_t)R.send_off[dst] * ld * elem, (size_t)(ns * ld), dt,
+                         dst, c->comm, c->s_comm));
+      if (nr)
+        NCCL_OK(api.Recv(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[src]) * ld * elem,
+                         (size_t)(nr * ld), dt, src, c->comm, c->s_comm));
+      NCCL_OK(api.GroupEnd());
+      if (steps) {
+        cudaEvent_t e = c->ev();
+        CUDA_OK(cudaEventRecord(e, c->s_comm));
+        steps->push_back({src, e});
+      }
+    }
   } else {
   NCCL_OK(api.GroupStart());
   for (int q = 0; q < c->pworld(); ++q) {
@@ -403,16 +473,40 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
     return;
   }
   // world > 1: exchange the boundary rows of P' on the comm stream while the
-  // local part runs; then add the remote part.
-  cudaEvent_t recvd = exchange_halo(c, P, p);
+  // local part runs; then add the remote part --
+  // grouped: one pass once every halo row is in; ring: one pass per step,
+  // each as soon as its peer's rows have arrived (the next step transfers
+  // meanwhile)
+  std::vector<std::pair<int, cudaEvent_t>> steps;
+  const bool ring = c->xmode == CC_EXCHANGE_RING;
+  cudaEvent_t recvd = exchange_halo(c, P, p, ring ? &steps : nullptr);
   gather_pass(c, c->p_local, P, p, N, 0);
-  cudaEvent_t wb = c->begin(c->s_main);  // exposed exchange: s_main idles until the halo rows are in
-  CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
-  c->end(PH_EXPOSED, c->s_main, wb);
-  gather_pass(c, c->p_remote, P, p, N, 1);
+  if (!ring) steps.push_back({-1, recvd});
+  for (const auto &st : steps) {
+    Pass &w = st.first < 0 ? c->p_remote : c->p_peer[st.first];
+    if (!w.items()) continue;
+    cudaEvent_t wb = c->begin(c->s_main);  // exposed exchange: s_main idles until the rows are in
+    CUDA_OK(cudaStreamWaitEvent(c->s_main, st.second, 0));
+    c->end(PH_EXPOSED, c->s_main, wb);
+    gather_pass(c, w, P, p, N, 1);
+  }
+  CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));  // the send buffer's release is ordered after every step
 }
 
 }  // namespace
+
+// Sum of a small host vector over the ranks (setup only, e.g. the exchange
+// model at load time): NCCL all-reduce, or the loopback group's host sum.
+void allreduce_host(cc_ctx *c, std::vector<double> &v) {
+  void *buf = c->amalloc(v.size() * sizeof(double), c->s_main);
+  double *d = static_cast<double *>(buf);
+  CUDA_OK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c->s_main));
+  if (c->loop) loopback_allreduce(c, d, v.size(), c->s_main);
+  else NCCL_OK(nccl().AllReduce(d, d, v.size(), ncclFloat64, ncclSum, c->comm, c->s_main));
+  CUDA_OK(cudaMemcpyAsync(v.data(), d, v.size() * sizeof(double), cudaMemcpyDeviceToHost, c->s_main));
+  CUDA_OK(cudaStreamSynchronize(c->s_main));
+  c->afree(buf, v.size() * sizeof(double), c->s_main);
+}
 
 void LoopbackGroup::rendezvous() {
   std::unique_lock<std::mutex> lk(mu);
@@ -440,7 +534,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
                const std::vector<int64_t> *dump_rows, TableCache *cache) {
   const Plan &pl = c->plan;
   const int k = pl.colours(), elem = c->elem();
-  std::fill(c->stats, c->stats + 10, 0.0);
+  std::fill(c->stats, c->stats + 11, 0.0);
+  c->stats[10] = c->xmode;
   {
     const char *pe = getenv("CC_PHASE_EVENTS");
     c->phase_events = c->profiling && !(pe && pe[0] == '0');
@@ -463,7 +558,12 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   if (c->pworld() > 1 && !c->sorted_valid) {
     cudaEvent_t b = c->begin(c->s_main);
     csort(c, c->p_local);
-    csort(c, c->p_remote);
+    if (c->xmode == CC_EXCHANGE_RING) {
+      for (Pass &w : c->p_peer)
+        if (w.items()) csort(c, w);
+    } else {
+      csort(c, c->p_remote);
+    }
     c->end(PH_CSORT, c->s_main, b);
     c->sorted_valid = true;
   }

@@ -186,4 +186,63 @@ RankPart partition_graph(const HostGraph &g, int world, int rank, uint64_t relab
   return R;
 }
 
+std::vector<int64_t> peer_bounds(const RankPart &R) {
+  const int W = R.world;
+  const int64_t n = R.n_own;
+  std::vector<int64_t> b((size_t)(W + 1) * n);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t *row = R.col.data();
+    for (int q = 0; q <= W; ++q) {
+      const int64_t lo = R.mid[i], hi = R.rp[i + 1];
+      b[(size_t)q * n + i] =
+          q == W ? hi : std::lower_bound(row + lo, row + hi, (int32_t)(R.n_own + R.recv_off[q])) - row;
+    }
+  }
+  return b;
+}
+
+ExchangeModel model_exchange(const RankPart &R, const std::vector<int64_t> &b, double w) {
+  // Rates (reading): NVLink 5 through NVSwitch, 900 GB/s
+  // per direction, ~700 GB/s achieved by one peer-to-peer stream; the
+  // neighbour-sum gathers move ~7 TB/s of algorithmic bytes on config 3
+  // (profiles/r1); a ring step costs ~20 us of NCCL group launch.
+  ExchangeModel m;
+  m.link_bps = 700e9;
+  m.gather_bps = 7e12;
+  const double step_s = 20e-6;
+  const int W = R.world, me = R.rank;
+  const int64_t n = R.n_own;
+  std::vector<double> nnz(W, 0.0), items(W, 0.0);
+  double local = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    local += (double)(R.mid[i] - R.rp[i]);
+    for (int q = 0; q < W; ++q) {
+      const int64_t d = b[(size_t)(q + 1) * n + i] - b[(size_t)q * n + i];
+      nnz[q] += (double)d;
+      items[q] += d > 0;
+    }
+  }
+  double items_remote = 0;
+  for (int64_t i = 0; i < n; ++i) items_remote += R.rp[i + 1] > R.mid[i];
+  auto gather_s = [&](double entries, double touched) {  // index + rows read, N'' rows read and written
+    return (entries * (4.0 + w) + touched * 2.0 * w) / m.gather_bps;
+  };
+  const double t_local = gather_s(local, 0.0);
+  double halo = 0, remote = 0;
+  for (int q = 0; q < W; ++q) {
+    halo += (double)(R.recv_off[q + 1] - R.recv_off[q]) * w / m.link_bps;
+    remote += nnz[q];
+  }
+  m.grouped_s = std::max(halo + step_s, t_local) + gather_s(remote, items_remote);
+  double comm = 0, t = t_local;
+  for (int r = 1; r < W; ++r) {
+    const int src = (me - r + W) % W;
+    comm += step_s + (double)(R.recv_off[src + 1] - R.recv_off[src]) * w / m.link_bps;
+    t = std::max(t, comm) + gather_s(nnz[src], items[src]);
+  }
+  m.ring_s = t;
+  return m;
+}
+
 }  // namespace cc

@@ -141,3 +141,28 @@ def test_partitioned_config3_full_size_two_ranks():
     assert len(set(xs)) == 1
     assert rel_err(xs[0], single) <= 1e-6
     assert all(s["halo_bytes"] > 0 for s in st)
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_ring_and_grouped_exchange_schedules_agree(world):
+    """SURVEY F2 / PAPER.md Alg. 3: the ring pipeline (step r sends to rank +
+    r, receives from rank - r, the remote pass over that peer's rows while the
+    next step transfers) and the grouped all-to-all give the oracle's count on
+    every rank; the schedule in use is reported; auto picks the same one on
+    every rank.  Heavy segments (segment_len 3) inside the per-peer passes,
+    the fused root (whole ranges after the last step), fp64 and fp32."""
+    cases = [(synth.scaled_twin(synth.CONFIGS[3], 11, 16).graph(), synth.CONFIGS[3].parent),
+             (synth.scaled_twin(synth.CONFIGS[4], 11, 32).graph(), synth.CONFIGS[4].parent),
+             (synth.gnp(300, 0.05, 9), [-1, 0, 1, 1, 0, 4])]
+    for g, parent in cases:
+        k = len(parent)
+        col = oracle.color(g.n, k, 21)
+        want = oracle.dp_count(g, parent, col, oracle.NUM_LONGDOUBLE).total
+        for mode in (lib().CC_EXCHANGE_GROUPED, lib().CC_EXCHANGE_RING):
+            for prec, tol, seg in (("fp64", 1e-12, 3), ("fp32", 1e-4, 0)):
+                xs, st = run_ranks(g, parent, world, colors=col, precision=prec, segment_len=seg, exchange=mode)
+                assert len(set(xs)) == 1 and rel_err(xs[0], want) <= tol, (parent, mode, prec)
+                assert all(s["exchange"] == mode for s in st)
+        xs, st = run_ranks(g, parent, world, colors=col)
+        assert rel_err(xs[0], want) <= 1e-12
+        assert len({s["exchange"] for s in st}) == 1 and st[0]["exchange"] in (1, 2)

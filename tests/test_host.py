@@ -195,3 +195,51 @@ def test_zblock_cover_computes_the_split_sum(cc, K, ts, as_):
             if row[na + nn + z] != 0xFFFF:
                 got[row[na + nn + z]] = acc[z]
     assert np.allclose(got, direct, rtol=1e-12)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_exchange_model(cc, world):
+    """The cost model behind CC_EXCHANGE_AUTO (Alg. 3 and the
+    pipeline analysis, lines 326-341, 420-441), recomputed here from the
+    partition plan: grouped = max(all halo rows over the link, local part) +
+    one remote pass; ring = world - 1 steps in the order rank - 1, rank - 2,
+    ..., each remote pass starting once its rows are in and the previous
+    pass is done.  With two ranks the schedules coincide."""
+    g = synth.rmat(12, 16, seed=2)
+    w = 512.0
+    for r in range(world):
+        m = cc.cc_exchange_model(g.n, g.row_ptr, g.col, world, r, row_bytes=w)
+        p = cc.cc_partition_plan(g.n, g.row_ptr, g.col, world, r)
+        link, gbps, step = m["link_bps"], m["gather_bps"], 20e-6
+        n_own = len(p["own_orig"])
+        rp, col = p["rp"], p["col"]
+        # owner of each halo row from recv_off
+        halo_owner = np.repeat(np.arange(world), np.diff(p["recv_off"]))
+        nnz = np.zeros(world)
+        items = np.zeros(world)
+        local = 0
+        items_remote = 0
+        for i in range(n_own):
+            nb = col[rp[i]:rp[i + 1]]
+            local += int((nb < n_own).sum())
+            rem = nb[nb >= n_own] - n_own
+            items_remote += len(rem) > 0
+            cnt = np.bincount(halo_owner[rem], minlength=world)
+            nnz += cnt
+            items += cnt > 0
+
+        def gather(e, t):
+            return (e * (4 + w) + t * 2 * w) / gbps
+        halo = np.diff(p["recv_off"]) * w / link
+        grouped = max(halo.sum() + step, gather(local, 0)) + gather(nnz.sum(), items_remote)
+        t, comm = gather(local, 0), 0.0
+        for s in range(1, world):
+            src = (r - s) % world
+            comm += step + halo[src]
+            t = max(t, comm) + gather(nnz[src], items[src])
+        assert m["grouped_s"] == pytest.approx(grouped, rel=1e-9)
+        assert m["ring_s"] == pytest.approx(t, rel=1e-9)
+        if world == 2:
+            assert m["ring_s"] == pytest.approx(m["grouped_s"], rel=1e-12)
+    with pytest.raises(cc.CCError):
+        cc.cc_exchange_model(g.n, g.row_ptr, g.col, 1, 0)
