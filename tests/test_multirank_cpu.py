@@ -1,4 +1,4 @@
-"""-m "not gpu": the N > 1 host path on CPU with world-size-2 gloo.
+"""-m "not gpu": the N > 1 host path on CPU with gloo (world 2 grouped, world 3 ring).
 
 Each rank takes its 1D-partition plan from the product library
 (`cc_partition_plan`, the same host code `cc_load_graph` runs), exchanges the
@@ -24,7 +24,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, scale, W, errq):
+def _worker(rank, world, port, scale, W, errq, schedule="grouped"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -39,6 +39,35 @@ def _worker(rank, world, port, scale, W, errq):
         n_halo = len(plan["halo_orig"])
         local = np.zeros((n_own + n_halo, W))
         local[:n_own] = P[plan["own_orig"]]
+        rp, col = plan["rp"], plan["col"]
+        if schedule == "ring":
+            # Alg. 3 ring (CC_EXCHANGE_RING): step r sends to rank + r and
+            # receives from rank - r; the remote sum over that peer's rows
+            # (each row's halo range split at the peer's recv_off boundary)
+            # accumulates as soon as they are in
+            N = np.zeros((n_own, W))
+            for i in range(n_own):
+                nb = col[rp[i]:rp[i + 1]]
+                nb = nb[nb < n_own]
+                N[i] = local[nb].sum(axis=0)
+            for r in range(1, world):
+                dst, src = (rank + r) % world, (rank - r) % world
+                s0, s1 = plan["send_off"][dst], plan["send_off"][dst + 1]
+                req = dist.isend(torch.from_numpy(np.ascontiguousarray(local[plan["send_idx"][s0:s1]])), dst)
+                r0, r1 = plan["recv_off"][src], plan["recv_off"][src + 1]
+                buf = torch.zeros((r1 - r0, W), dtype=torch.float64)
+                dist.recv(buf, src)
+                req.wait()
+                local[n_own + r0:n_own + r1] = buf.numpy()
+                for i in range(n_own):
+                    nb = col[rp[i]:rp[i + 1]]
+                    lo = np.searchsorted(nb, n_own + r0)
+                    hi = np.searchsorted(nb, n_own + r1)
+                    N[i] += local[nb[lo:hi]].sum(axis=0)
+            src_ = np.repeat(np.arange(g.n), g.degrees())
+            NG = np.zeros((g.n, W))
+            np.add.at(NG, src_, P[g.col])
+            assert np.allclose(N, NG[plan["own_orig"]], rtol=1e-12, atol=0)
         # grouped send/recv with every peer (the NCCL step)
         reqs = []
         for q in range(world):
@@ -77,14 +106,14 @@ def _worker(rank, world, port, scale, W, errq):
         raise
 
 
-@pytest.mark.parametrize("world", [2])
-def test_halo_exchange_gloo_world2(world):
+@pytest.mark.parametrize("world,schedule", [(2, "grouped"), (3, "ring")])
+def test_halo_exchange_gloo(world, schedule):
     import __graft_entry__
     __graft_entry__._product_build()
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 11, 6, errq)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 11, 6, errq, schedule)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
