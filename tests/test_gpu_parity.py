@@ -485,19 +485,24 @@ def test_options_and_hooks_are_validated():
     with pytest.raises(cc.CCError) as e:
         cc.cc_create(device=0, replicas=2)
     assert e.value.status == cc.CC_ERR_ARG
+    with pytest.raises(cc.CCError) as e:
+        cc.cc_create(device=0, exchange=3)  # CC_EXCHANGE_AUTO / _GROUPED / _RING only
+    assert e.value.status == cc.CC_ERR_ARG
     g = synth.gnp(50, 0.2, 1)
-    with context(g, [-1, 0, 1]) as ctx:
+    with context(g, [-1, 0, 1, 2]) as ctx:  # P4: a p = 2 neighbour sum under every root
         with pytest.raises(cc.CCError) as e:
-            cc.cc_set_template_colors(ctx, [-1, 0, 1], 2)  # fewer colours than vertices
+            cc.cc_set_template_colors(ctx, [-1, 0, 1, 2], 3)  # fewer colours than vertices
         assert e.value.status == cc.CC_ERR_ARG
         cc.cc_color(ctx, 3)
         x = cc.cc_count_colorful(ctx)
         cc.cc_set_profiling(ctx, False)
         assert cc.cc_count_colorful(ctx) == x
         prof = cc.cc_last_profile(ctx)
-        assert prof["total"] > 0 and prof["gather"] == 0.0  # no per-kernel events
+        assert prof["total"] > 0 and prof["gather"] == 0.0 and prof["csort"] == 0.0  # no per-kernel events
         cc.cc_set_profiling(ctx, True)
-        assert cc.cc_count_colorful(ctx) == x and cc.cc_last_profile(ctx)["gather"] > 0
+        assert cc.cc_count_colorful(ctx) == x
+        prof = cc.cc_last_profile(ctx)
+        assert prof["gather"] > 0 and prof["csort"] > 0
         with pytest.raises(cc.CCError) as e:
             cc.cc_set_colors(ctx, np.full(g.n, 7, np.uint8))  # colour out of range
         assert e.value.status == cc.CC_ERR_ARG
