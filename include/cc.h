@@ -273,7 +273,8 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * of the aggregation kernels alone, out[3] = number of kernel launches,
  * out[4] = peak table bytes, out[5] (cap >= 6) = fused-root mode of the
  * last count (0: none, 1: root dot with the active table, 2: self dot with
- * the lifted neighbour sum), out[6] / out[7] (cap >= 8) = algorithmic bytes
+ * the lifted neighbour sum -- both in the last gather's epilogue; 3: root dot
+ * in the epilogue of the combine that produces the root's active table), out[6] / out[7] (cap >= 8) = algorithmic bytes
  * and device ms of the longest neighbour-sum launch, out[8] = number of
  * neighbour-sum launches, out[9] = halo bytes received by this rank (1D
  * partition), out[10] (cap >= 11) = the exchange schedule in use

@@ -597,6 +597,27 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     }
   }
 
+  // Fused combine + root (fuse = 3): the root's active table is the output
+  // of a combine over the SAME passive (configs[2] and [3]: the legs or
+  // subtrees under the root are isomorphic), whose neighbour sum that
+  // combine stages anyway -- the root is evaluated in the combine's
+  // epilogue and the active table never reaches HBM.
+  int fuse_cr = -1;
+  bool cr_done = false;
+  {
+    const Step &rs = pl.steps[sr];
+    const char *f = getenv("CC_FUSED_ROOT");
+    if (!fuse && pl.k == k && !cache && !(f && f[0] == '0') && rs.out < 0 && rs.a > 1 && rs.p >= 2 &&
+        (dump_table < 0 || (dump_rows && dump_table != rs.active)) && pl.table_last_use[rs.active] == sr) {
+      for (int s = 0; s < sr; ++s) {
+        const Step &cs = pl.steps[s];
+        if (cs.out == rs.active && cs.a >= 2 && cs.passive == rs.passive && c->d_ztab[s] &&
+            dev::combine_z_supported(elem, cs.t - 1, cs.a - 1))
+          fuse_cr = s;
+      }
+    }
+  }
+
   c->stats[5] = fuse;
   Bufs bufs(c);
   const int nt = (int)pl.tables.size();
@@ -606,7 +627,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   for (int s = 0; s < (int)pl.steps.size(); ++s)
     if (pl.steps[s].p == 1) last_hist_use = s;
   double *per_vertex = nullptr;
-  if (root_out || fuse) per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
+  if (root_out || fuse || fuse_cr >= 0)
+    per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
   if (cache && cache->sorted) {  // an earlier template of this colouring sorted and built the leaf level
     if (last_hist_use >= 0) hist = bufs.alias(cache->hist, cache->hist_bytes);
   } else if (c->pworld() == 1) {  // colour sort + leaf level N''(v, {y}) in one pass over the adjacency
@@ -766,6 +788,13 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       c->check_launch();
       c->end(PH_ROOT, c->s_main, b);
       c->stats[1] += (double)n * Wt * elem;
+    } else if (st.out < 0 && cr_done) {  // X_v came from the last combine's epilogue: sum over v
+      cudaEvent_t b = c->begin(c->s_main);
+      c->stats[3] += dev::launch_root(8, nullptr, 0, 0, per_vertex, 1, nullptr, n, c->d_partials, c->n_partials,
+                                      nullptr, c->d_result, c->s_main);
+      c->check_launch();
+      c->end(PH_ROOT, c->s_main, b);
+      c->stats[1] += (double)n * 8.0;
     } else if (st.out < 0) {  // root step fused with the sum over v (Eq. 3)
       cudaEvent_t b = c->begin(c->s_main);
       const void *A = st.a > 1 ? bufs.ptr(T[st.active]) : nullptr;
@@ -777,6 +806,22 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     } else if (st.a == 1) {  // T'(v, .) = N''(v, .): alias, no kernel
       T[st.out] = nbuf;
       bufs.ref(nbuf);
+    } else if (s == fuse_cr &&
+               [&] {
+                 cudaEvent_t b = c->begin(c->s_main);
+                 const int l = dev::launch_combine_root(
+                     elem, bufs.ptr(T[st.active]), c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, Wp, c->d_ztab[s],
+                     c->zblocks[s], (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->d_comp, n, per_vertex,
+                     c->num_sms, c->s_main);
+                 if (!l) return false;
+                 c->check_launch();
+                 c->end(PH_COMBINE, c->s_main, b);
+                 c->stats[3] += l;
+                 c->stats[1] += (double)n * (Wa + Wp + 1.0) * elem;
+                 return true;
+               }()) {
+      cr_done = true;  // the active table of the root is never stored
+      c->stats[5] = 3;
     } else {
       T[st.out] = bufs.make((size_t)rows * c->ld_of(Wt) * elem);
       cudaEvent_t b = c->begin(c->s_main);

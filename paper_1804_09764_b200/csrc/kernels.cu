@@ -309,7 +309,8 @@ template <typename T, int ZS, int AS, int V>
 __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, int64_t ldA, int WA,
                                                       const T *__restrict__ N, int64_t ldN, int WN,
                                                       const uint16_t *__restrict__ ztab, int nblocks, int zld, int64_t n,
-                                                      T *__restrict__ out, int64_t ldO, int nbuf) {
+                                                      T *__restrict__ out, int64_t ldO, int nbuf,
+                                                      const uint16_t *__restrict__ comp, double *__restrict__ per_vertex) {
   constexpr ZTab<ZS, AS> tab{};
   constexpr int PS = ZS - 1 - AS, NA = ZTab<ZS, AS>::NA, NN = ZTab<ZS, AS>::NN;
   constexpr int S = 33;
@@ -322,6 +323,12 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
   T *bufs = reinterpret_cast<T *>(smem_raw);
   uint16_t *zs = reinterpret_cast<uint16_t *>(bufs + (size_t)nbuf * bstride);
   for (int i = threadIdx.x; i < nblocks * zld; i += blockDim.x) zs[i] = ztab[i];
+  // fused root (per_vertex != nullptr): the outputs are not stored; each
+  // output T'(v, X') (rounded to the storage type, as the stored table would
+  // be) is multiplied in fp64 by the staged N''(v, comp X') -- the root step
+  // (Eq. 2 at the root) shares this step's passive -- and the per-warp sums
+  // are added in warp order into X_v (Eq. 3's summand)
+  double *red = reinterpret_cast<double *>(smem_raw + ((size_t)nbuf * bstride * sizeof(T) + (size_t)nblocks * zld * 2 + 7) / 8 * 8);
   const int64_t ntiles = (n + TV - 1) / TV;
   auto stage = [&](int64_t tile, T *b) {
     const int64_t v0 = tile * TV;
@@ -351,6 +358,9 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
     const char *Nb = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + (size_t)WA * S + lane);
     constexpr uint32_t CB = S * sizeof(LV);
     const int64_t vb = tile * TV + (int64_t)lane * V;
+    double rsum[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) rsum[i] = 0.0;
     for (int zb = warp; zb < nblocks; zb += nwarp) {
       const uint16_t *e = zs + (size_t)zb * zld;
       // block entries read 4 at a time (one 8-byte broadcast load per 4
@@ -383,13 +393,30 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
       for (int zz = 0; zz < ZS; ++zz) {
         const uint16_t oc = e[NA + NN + zz];
         if (oc != 0xFFFF) {
+          if (per_vertex) {
+            const LV ny = *reinterpret_cast<const LV *>(Nb + (uint32_t)__ldg(comp + oc) * CB);
 #pragma unroll
-          for (int i = 0; i < V; ++i)
-            if (vb + i < n) out[(vb + i) * ldO + oc] = acc[zz][i];
+            for (int i = 0; i < V; ++i) rsum[i] += (double)acc[zz][i] * (double)LaneVec<T, V>::at(ny, i);
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i)
+              if (vb + i < n) out[(vb + i) * ldO + oc] = acc[zz][i];
+          }
         }
       }
     }
+    if (per_vertex) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) red[warp * TV + lane * V + i] = rsum[i];
+    }
     __syncthreads();
+    if (per_vertex) {
+      for (int r = threadIdx.x; r < TV; r += blockDim.x) {
+        double x = 0.0;
+        for (int w = 0; w < nwarp; ++w) x += red[w * TV + r];
+        if (tile * TV + r < n) per_vertex[tile * TV + r] = x;
+      }
+    }
     if (nbuf == 1 && tile + gridDim.x < ntiles) stage(tile + gridDim.x, bufs);
   }
 }
@@ -420,6 +447,30 @@ __global__ void __launch_bounds__(256) k_root(const T *__restrict__ A, int64_t l
     }
   }
   if (lane == 0) wsum_s[warp] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) b += wsum_s[i];
+    partials[blockIdx.x] = b;
+  }
+}
+
+// A single column (A' = the root vertex alone, or X_v formed in an
+// epilogue): thread per vertex, then a fixed-order block reduction.
+template <typename T>
+__global__ void __launch_bounds__(256) k_vsum(const T *__restrict__ N, int64_t ldN, int64_t n,
+                                              double *__restrict__ partials, double *__restrict__ per_vertex) {
+  __shared__ double wsum_s[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double s = 0.0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const double x = (double)N[v * ldN];
+    if (per_vertex) per_vertex[v] = x;
+    s += x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) wsum_s[warp] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
     double b = 0.0;
@@ -574,10 +625,12 @@ bool combine_z_supported(int elem, int ts, int as) {
 namespace {
 template <typename T, int ZS, int AS>
 int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint16_t *ztab, int nblocks,
-         int zld, int64_t n, void *out, int64_t ldO, int num_sms, cudaStream_t s) {
+         int zld, int64_t n, void *out, int64_t ldO, int num_sms, cudaStream_t s, const uint16_t *comp = nullptr,
+         double *per_vertex = nullptr) {
   const size_t cap = 227 * 1024;
   const size_t tile = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
-  const size_t zbytes = (size_t)nblocks * zld * 2;
+  // (+ the fused root's per-warp vertex sums: 16 warps x 32 doubles)
+  const size_t zbytes = ((size_t)nblocks * zld * 2 + 7) / 8 * 8 + (per_vertex ? 16 * 32 * 8 : 0);
   if (tile + zbytes > cap) return 0;
   // two single-buffered CTAs of 8 warps per SM when they fit (one computes
   // while the other stages or waits at its barrier; measured 5% faster on
@@ -594,10 +647,25 @@ int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = persistent_grid(kern, threads, smem, num_sms);
   kern<<<grid, threads, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, ztab,
-                                   nblocks, zld, n, static_cast<T *>(out), ldO, nbuf);
+                                   nblocks, zld, n, static_cast<T *>(out), ldO, nbuf, comp, per_vertex);
   return 1;
 }
 }  // namespace
+
+int launch_combine_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
+                        const uint16_t *ztab, int nblocks, int zld, int ts, int as, const uint16_t *comp, int64_t n,
+                        double *per_vertex, int num_sms, cudaStream_t s) {
+  if (n == 0 || !ztab || !comp || !per_vertex) return 0;
+  const char *impl = getenv("CC_COMBINE_IMPL");
+  if (impl && impl[0] != 'z') return 0;
+  if (elem == 4 && ts == 8 && as == 5)
+    return z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
+  if (elem == 4 && ts == 6 && as == 3)
+    return z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
+  if (elem == 8 && ts == 6 && as == 3)
+    return z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
+  return 0;
+}
 
 int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
@@ -617,7 +685,11 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
 
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, const uint16_t *comp,
                 int64_t n, double *partials, int n_partials, double *per_vertex, double *result, cudaStream_t s) {
-  if (elem == 8)
+  if (!A && elem == 8)
+    k_vsum<double><<<n_partials, 256, 0, s>>>(static_cast<const double *>(N), ldN, n, partials, per_vertex);
+  else if (!A)
+    k_vsum<float><<<n_partials, 256, 0, s>>>(static_cast<const float *>(N), ldN, n, partials, per_vertex);
+  else if (elem == 8)
     k_root<double><<<n_partials, 256, 0, s>>>(static_cast<const double *>(A), ldA, WA, static_cast<const double *>(N),
                                                ldN, comp, n, partials, per_vertex);
   else

@@ -106,6 +106,14 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
                    int nblocks, int zld, int ts, int as, int num_sms, cudaStream_t s);
 bool combine_z_supported(int elem, int ts, int as);
+// The last combine fused with the root step that shares its passive table:
+// X_v = sum_{X'} T'(v, X') N''(v, comp X') into per_vertex[v] (fp64), T'
+// never stored.  Returns 0 (nothing launched) when the shape has no
+// register-blocked kernel or its tile does not fit; the caller then runs the
+// combine and launch_root.
+int launch_combine_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
+                        const uint16_t *ztab, int nblocks, int zld, int ts, int as, const uint16_t *comp, int64_t n,
+                        double *per_vertex, int num_sms, cudaStream_t s);
 // Root step + deterministic reduction into result[0] (double).  A == nullptr
 // means a single-vertex active part: sum_v N''(v, [k-1]) (one column).
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN,

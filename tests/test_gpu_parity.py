@@ -226,6 +226,38 @@ def test_fused_root_exact(parent, mode, monkeypatch):
             assert rel_err(cc.cc_count_colorful(ctx), float(want.total)) <= TOL_FP32
 
 
+@pytest.mark.parametrize("ci", [2, 3])
+def test_fused_combine_root(ci, monkeypatch):
+    """Fused combine + root (fused_root mode 3): configs[2]'s and [3]'s root
+    step takes its active table from a register-blocked combine over the
+    same passive neighbour sum, so X_v is formed in that combine's epilogue
+    and the active table is never stored.  Against the oracle (count and
+    every X_v) and the unfused run; fp64 where the Z-block kernel exists in
+    fp64 (configs[2]'s (7;4,3)), fp32 for both."""
+    cc = lib()
+    cfg = synth.CONFIGS[ci]
+    parent, k = cfg.parent, cfg.k
+    graphs = [synth.gnp(70, 0.2, 5), synth.scaled_twin(cfg, 10, 16).graph()]
+    precs = [("fp32", TOL_FP32)] + ([("fp64", TOL_FP64)] if ci == 2 else [])
+    for gi, g in enumerate(graphs):
+        col = oracle.color(g.n, k, 60 + gi)
+        want = oracle.dp_count(g, parent, col, oracle.NUM_LONGDOUBLE, want_root=True)
+        for prec, tol in precs:
+            for seg in (0, 3):
+                with context(g, parent, prec, segment_len=seg) as ctx:
+                    cc.cc_set_colors(ctx, col)
+                    x = cc.cc_count_colorful(ctx)
+                    assert cc.cc_last_stats(ctx)["fused_root"] == 3, (ci, prec)
+                    root = cc.cc_get_subtree_counts(ctx, parent.index(-1), g.n, k, k)
+                    monkeypatch.setenv("CC_FUSED_ROOT", "0")
+                    x_unfused = cc.cc_count_colorful(ctx)
+                    assert cc.cc_last_stats(ctx)["fused_root"] == 0
+                    monkeypatch.delenv("CC_FUSED_ROOT")
+                assert rel_err(x, float(want.total)) <= tol, (ci, gi, prec, seg)
+                assert rel_err(x_unfused, x) <= tol
+                assert_close_entries(root, want.root.reshape(-1, 1), tol, f"fused combine root X_v config {ci}")
+
+
 def test_subtree_rows_match_the_full_dump_and_the_oracle():
     """cc_get_subtree_rows (the sampled-row hook used at configs[4] scale)
     returns the same rows as the full-table dump and the oracle, including
