@@ -303,6 +303,9 @@ def run_ours(args, cfg, rank, world, dist):
                              "kernel": "k_gather_ldg: the longest neighbour-sum (SpMM gather) launch of the step",
                              "algorithmic_bytes_per_launch": top_bytes, "ms_per_launch": top_ms,
                              "peak_source": peak_src, "traffic_source": traffic_src,
+                             # the same launch judged by its DRAM bytes (ncu) over its live duration
+                             "dram_achieved": traffic / (top_ms * 1e-3) / 1e9 if traffic and top_ms else None,
+                             "dram_frac": traffic / (top_ms * 1e-3) / 1e9 / peak if traffic and top_ms else None,
                              "note": "algorithmic bytes include L2 hits on hub rows, so frac can exceed 1; "
                                      "traffic = ncu DRAM read+write bytes of the same launch"},
                 "gather_family": {"launches_per_step": stats["gather_launches"],
