@@ -282,6 +282,12 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * cap >= 5. */
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
 
+/* Test hook: a one-rank NCCL communicator on `device` runs the calls the
+ * partitioned path uses -- a grouped ncclSend/ncclRecv (to itself) and an
+ * fp64 ncclAllReduce -- and checks the values moved.  CC_ERR_NCCL when NCCL
+ * cannot be loaded or a value is wrong, CC_ERR_CUDA on a device error. */
+cc_status cc_nccl_selftest(int32_t device);
+
 /* ---- host-only introspection (no GPU needed; used by CPU tests) --------- */
 
 /* Median of means of n colourful counts X (as cc_estimate_mom, no GPU). */

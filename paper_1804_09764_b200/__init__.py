@@ -55,6 +55,11 @@ def cc_default_options(**kw) -> cc_options:
     return o
 
 
+def cc_nccl_selftest(device: int = 0) -> None:
+    """Test hook: one-rank NCCL grouped send/recv + all-reduce on `device`."""
+    _check(None, _lib.cc_nccl_selftest(device))
+
+
 def cc_loopback_create(world: int) -> ctypes.c_void_p:
     """Test hook: an in-process transport group for `world` rank threads (cc_options.loopback)."""
     h = ctypes.c_void_p()

@@ -38,6 +38,7 @@ STATUS_NAMES = ["CC_OK", "CC_ERR_ARG", "CC_ERR_GRAPH", "CC_ERR_TEMPLATE", "CC_ER
 SIGNATURES = {
     "cc_default_options": (c_i32, [vp]),
     "cc_nccl_unique_id": (c_i32, [vp]),
+    "cc_nccl_selftest": (c_i32, [c_i32]),
     "cc_loopback_create": (c_i32, [c_i32, vp]),
     "cc_loopback_destroy": (None, [vp]),
     "cc_create": (c_i32, [vp, vp]),

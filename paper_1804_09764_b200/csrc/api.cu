@@ -113,6 +113,42 @@ cc_status cc_nccl_unique_id(void *out128) {
   return CC_OK;
 }
 
+cc_status cc_nccl_selftest(int32_t device) {
+  auto &api = cc::nccl();
+  if (!api.ok) return CC_ERR_NCCL;
+  ncclComm_t comm = nullptr;
+  cudaStream_t s = nullptr;
+  double *d = nullptr;
+  cc_status st = CC_OK;
+  try {
+    CUDA_OK(cudaSetDevice(device));
+    ncclUniqueId id;
+    NCCL_OK(api.GetUniqueId(&id));
+    NCCL_OK(api.CommInitRank(&comm, 1, id, 0));
+    CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CUDA_OK(cudaMalloc(&d, 4 * sizeof(double)));
+    const double h0[4] = {1.5, 0.0, 0.0, -2.25};
+    CUDA_OK(cudaMemcpyAsync(d, h0, sizeof(h0), cudaMemcpyHostToDevice, s));
+    // the calls of the halo exchange (a grouped send/recv, here to itself)
+    // and of the final reduction, with the same argument types
+    NCCL_OK(api.GroupStart());
+    NCCL_OK(api.Send(d, 1, ncclFloat64, 0, comm, s));
+    NCCL_OK(api.Recv(d + 1, 1, ncclFloat64, 0, comm, s));
+    NCCL_OK(api.GroupEnd());
+    NCCL_OK(api.AllReduce(d + 3, d + 2, 1, ncclFloat64, ncclSum, comm, s));
+    double h[4];
+    CUDA_OK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    if (h[1] != 1.5 || h[2] != -2.25) st = CC_ERR_NCCL;
+  } catch (const Error &e) {
+    st = e.status;
+  }
+  if (d) cudaFree(d);
+  if (s) cudaStreamDestroy(s);
+  if (comm) api.CommDestroy(comm);
+  return st;
+}
+
 cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   if (!opt || !out) return CC_ERR_ARG;
   if (opt->precision != CC_FP64 && opt->precision != CC_FP32) return CC_ERR_ARG;

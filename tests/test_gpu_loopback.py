@@ -166,3 +166,11 @@ def test_ring_and_grouped_exchange_schedules_agree(world):
         xs, st = run_ranks(g, parent, world, colors=col)
         assert rel_err(xs[0], want) <= 1e-12
         assert len({s["exchange"] for s in st}) == 1 and st[0]["exchange"] in (1, 2)
+
+
+def test_nccl_calls_on_one_rank():
+    """The NCCL half of the partitioned path that one GPU can run: the
+    library loads NCCL at run time, builds a communicator and moves fp64
+    values with the same grouped ncclSend/ncclRecv and ncclAllReduce calls
+    (and argument types) the halo exchange and the final reduction use."""
+    lib().cc_nccl_selftest(0)
