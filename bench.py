@@ -165,6 +165,25 @@ def oracle_sample(cfg, scale: int, seed: int, reps: int = 1):
     return u / best / 1e9, best * 1e3, desc
 
 
+def host_info() -> dict:
+    """CPU model and host RAM of the box the oracle ran on."""
+    info = {"cpu_model": None, "host_ram_gb": None}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    info["host_ram_gb"] = round(int(line.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return info
+
+
 def auto_cpu_scale(cfg):
     return {0: 0, 1: 16, 2: 18, 3: 19, 4: 13}[cfg.idx]
 
@@ -186,7 +205,8 @@ def run_reference(args, cfg, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"configs[{cfg.idx}] {cfg.name}", "sample_scale": scale},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             **host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -337,7 +357,7 @@ def run_ours(args, cfg, rank, world, dist):
             scale = args.cpu_scale or auto_cpu_scale(cfg)
             v, ms, desc = oracle_sample(cfg, scale, args.seed)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                                    "sample": desc, "ms": ms}
+                                    "sample": desc, "ms": ms, **host_info()}
         print(json.dumps(line), flush=True)
     cc.cc_destroy(ctx)
 
