@@ -459,6 +459,33 @@ def test_determinism_bitwise():
     assert len(xs) == 1
 
 
+def test_invariances():
+    """SURVEY 8(c) invariants on the CUDA path, exact in fp64 (integer
+    counts below 2^53): the count does not depend on the root and cut order
+    (reading C-4: planner's choice vs the parent -1 vertex), on the internal
+    vertex relabelling, on a permutation of the colour names, or on the
+    heavy-vertex segment length; and equals the oracle's (exact below 2^53,
+    else within the fp64 bar)."""
+    rng = np.random.default_rng(8)
+    cases = [(synth.scaled_twin(synth.CONFIGS[3], 10, 16).graph(), synth.CONFIGS[3].parent),
+             (synth.scaled_twin(synth.CONFIGS[2], 10, 16).graph(), synth.CONFIGS[2].parent),
+             (synth.gnp(120, 0.08, 6), [-1, 0, 1, 2, 2, 0, 5])]
+    for g, parent in cases:
+        k = len(parent)
+        col = oracle.color(g.n, k, 77)
+        want = float(oracle.dp_count(g, parent, col, oracle.NUM_EXACT).total)
+        perm = rng.permutation(k).astype(np.uint8)
+        runs = [count(g, parent, colors=col),
+                count(g, parent, colors=col, fixed_root=1),
+                count(g, parent, colors=col, relabel_seed=12345),
+                count(g, parent, colors=perm[col]),
+                count(g, parent, colors=col, segment_len=7)]
+        # exact below 2^53; above it (the 12-vertex tree) within the fp64 bar
+        assert all(rel_err(r, want) <= TOL_FP64 for r in runs), (parent, runs, want)
+        if want < 2.0 ** 53:
+            assert runs == [want] * len(runs), (parent, runs, want)
+
+
 def test_estimator_matches_oracle_formula():
     cc = lib()
     g = synth.gnp(40, 0.3, 3)
