@@ -40,6 +40,8 @@ struct Pass {
   int64_t *seg_b = nullptr, *seg_e = nullptr;
   int64_t n_light = 0, n_seg = 0, n_hv = 0;
   int64_t small_from = 0;      // first item (segments first, then light) of the <= 8-neighbour tail
+  int64_t split[8] = {0};      // split[i]: first item of the <= (8 << i)-neighbour tail
+  int64_t seg_len = 0;         // segment length s of the heavy items
   int64_t nnz = 0;             // adjacency entries covered
   const int64_t *beg = nullptr, *end = nullptr;  // device
   uint16_t *goff = nullptr;    // n_items x 16 colour-group ends (per colouring)

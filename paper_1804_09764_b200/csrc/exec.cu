@@ -27,10 +27,11 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
                 Pass &w) {
   // segment length s of Alg. 4; colour-group offsets are stored as uint16.
   // Auto: with W adjacency entries per resident warp (16 per SM), s ~
-  // sqrt(20 W) rounded to a power of two in [64, 4096], and 4096 once W >=
-  // 100K (measured optimum: configs[1] 128, [2] 512, [3] 4096 -- a long
-  // hub list on one warp is the tail of small graphs, partial-row traffic
-  // the cost of short segments on big ones)
+  // 4 sqrt(20 W) rounded to a power of two in [64, 4096], and 4096 once W >=
+  // 100K (measured optimum with the row-parallel kernel for long narrow
+  // lists: configs[1] 512, [2] 2048-4096, [3] 4096 -- a long hub list on one
+  // warp is the tail of small graphs, partial-row traffic the cost of short
+  // segments on big ones; with sub-warp rings only it was 128 / 512 / 4096)
   int64_t L = c->opt.segment_len;
   if (L <= 0) {
     int64_t nnz_all = 0;
@@ -39,10 +40,11 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
     L = 4096;
     if (W < 100000.0) {
       L = 64;
-      while (L < 4096 && (double)(2 * L) <= std::sqrt(20.0 * W) * 1.414) L *= 2;
+      while (L < 4096 && (double)(2 * L) <= std::sqrt(320.0 * W) * 1.414) L *= 2;
     }
   }
   L = std::min<int64_t>(L, 65535);
+  w.seg_len = L;
   std::vector<int32_t> light, seg_v, seg_hv, hv_first, hv_nseg;
   std::vector<int64_t> seg_b, seg_e;
   int64_t nnz = 0;
@@ -70,6 +72,11 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
     int64_t i = (int64_t)light.size();
     while (i > 0 && end[light[i - 1]] - beg[light[i - 1]] <= 8) --i;
     w.small_from = (int64_t)seg_v.size() + i;
+    for (int q = 0; q < 8; ++q) {
+      int64_t iq = (int64_t)light.size();
+      while (iq > 0 && end[light[iq - 1]] - beg[light[iq - 1]] <= (8 << q)) --iq;
+      w.split[q] = (int64_t)seg_v.size() + iq;
+    }
   }
   w.n_seg = (int64_t)seg_v.size();
   w.n_hv = (int64_t)hv_first.size();
@@ -292,6 +299,17 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   a.src = P;
   a.ld_src = c->ld_of(W_in);
   a.W_in = W_in;
+  {
+    // narrow rows: items with more than T neighbours (heavy segments first,
+    // then light items in degree order) go to the warp-per-item row-parallel
+    // kernel, the rest to the sub-warp rings; T = 8 << q = max(32, s / 16)
+    // (measured, profiles/r1/SUMMARY.md); none when segments are <= T long
+    const char *ns = getenv("CC_NARROW_SPLIT");
+    int q = 2;  // auto: T = max(32, s / 16)
+    while (q < 7 && (8 << (q + 1)) <= w.seg_len / 16) ++q;
+    if (ns) q = std::min(7, std::max(0, atoi(ns)));
+    a.item_split = w.seg_len > (8 << q) ? w.split[q] : 0;
+  }
   a.map = c->d_map[p];
   a.map_ld = gather_map_ld(k, p);
   {

@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
   const int grp = threadIdx.x / G;
   const unsigned gmask = group_mask<G>();
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / G;
-  const int64_t n_items = a.work.n_seg + a.work.n_light;
+  const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
   const int groups_per_block = blockDim.x / G;
   V *ring = reinterpret_cast<V *>(smem_ring) + (int64_t)grp * D * NV * G;  // [D][NV][G]
   double *sacc = reinterpret_cast<double *>(reinterpret_cast<V *>(smem_ring) + (int64_t)groups_per_block * D * NV * G) +
@@ -519,7 +519,8 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
   const T *__restrict__ src = static_cast<const T *>(a.src);
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
 
-  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items; it += ngroups) {
+  for (int64_t it = a.item_from + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items;
+       it += ngroups) {
     int32_t v;
     int64_t b, e;
     const bool heavy = item_range(a.work, a.beg, a.end, it, v, b, e);
@@ -783,6 +784,162 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
   }
 }
 
+// ------------------------------------------------------------------ gather, narrow rows
+// Rows of <= 16 vectors: one warp per item as in k_gather_ldg (no divergence
+// between items), but a row is covered by G lanes, so one warp-wide load
+// instruction reads RG = 32 / G rows of the same colour group (lane = row
+// slot rs x column vector vl); U such loads per lane in flight.  At the end
+// of a chunk of <= 32 rows the RG slot sums are combined by XOR shuffles
+// (fp32 block of <= 32 rows, then fp64: DESIGN.md C-6) and expanded into the
+// fp64 N'' row through the colour-pair map, vector j by slot j mod RG.
+template <typename T, int G, int NV, int U>
+__global__ void __launch_bounds__(256, 2) k_gather_rows(GatherArgs a, int nch) {
+  using V = typename Vec<T>::type;
+  constexpr int VW = Vec<T>::W;
+  constexpr int RG = 32 / G;
+  constexpr int CAP = G * NV * VW;  // columns per pass
+  extern __shared__ __align__(16) unsigned char sacc_raw[];
+  const int lane = threadIdx.x & 31, vl = lane % G, rs = lane / G;
+  double *sacc = reinterpret_cast<double *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)a.W_out;
+  const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const char *__restrict__ srcb = static_cast<const char *>(a.src);
+  const uint32_t ld_bytes = (uint32_t)(a.ld_src * sizeof(T));
+
+  int64_t it = a.item_from + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int4 dx = make_int4(0, 0, 0, 0), dy = make_int4(0, 0, 0, 0);
+  int go_n = 0;
+  if (it < n_items) load_desc(a, it, lane, dx, dy, go_n);
+  for (; it < n_items; it += nw) {
+    const int64_t b = (int64_t)(((uint64_t)(uint32_t)dx.y << 32) | (uint32_t)dx.x);
+    const int32_t v = dx.z;
+    const int cv = dy.z;
+    const bool heavy = dy.w != 0;
+    const int hi_l = go_n;
+    const int lo_l = __shfl_up_sync(0xffffffffu, hi_l, 1);
+    const unsigned gm = __ballot_sync(0xffffffffu, lane < a.k && lane != cv && hi_l > (lane == 0 ? 0 : lo_l));
+    if (it + nw < n_items) load_desc(a, it + nw, lane, dx, dy, go_n);  // prefetch the next item
+    for (int j = lane; j < a.W_out; j += 32) sacc[j] = 0.0;
+    __syncwarp();
+    for (int ch = 0; ch < nch; ++ch) {
+      const int c0 = ch * CAP + vl * VW;
+      bool valid[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) valid[j] = c0 + j * G * VW < a.W_in;
+      const char *lbase = srcb + (size_t)c0 * sizeof(T);
+      for (unsigned g = gm; g; g &= g - 1) {
+        const int cu = __ffs(g) - 1;
+        const int lo = cu == 0 ? 0 : __shfl_sync(0xffffffffu, hi_l, cu - 1);
+        const int hi = __shfl_sync(0xffffffffu, hi_l, cu);
+        bool use[NV];
+        {
+          const int cvu = cv < cu ? cv : cv - 1;  // sq_{c_u}(c_v)
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            use[j] = valid[j];
+            if (a.skip && valid[j]) {
+              const int vi = c0 / VW + j * G;  // the lane's 16-byte vector of the row
+              use[j] = !((__ldg(a.skip + (int64_t)cvu * a.skip_words + (vi >> 5)) >> (vi & 31)) & 1u);
+            }
+          }
+        }
+        uint16_t m[NV][VW];
+        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          if (valid[j] && rs == j % RG) {
+            if constexpr (VW == 4) {
+              const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + c0 + j * G * VW));
+              m[j][0] = w.x & 0xFFFF;
+              m[j][1 % VW] = w.x >> 16;
+              m[j][2 % VW] = w.y & 0xFFFF;
+              m[j][3 % VW] = w.y >> 16;
+            } else {
+              const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + c0 + j * G * VW));
+              m[j][0] = w & 0xFFFF;
+              m[j][1 % VW] = w >> 16;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < VW; ++q) m[j][q] = 0xFFFF;
+          }
+        }
+        int32_t u_next = lane < hi - lo ? __ldg(a.col + b + lo + lane) : 0;
+        for (int p = lo; p < hi; p += 32) {
+          const int cnt = min(32, hi - p);
+          const int32_t my_u = u_next;
+          if (p + 32 < hi) u_next = p + 32 + lane < hi ? __ldg(a.col + b + p + 32 + lane) : 0;
+          V blk[NV];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) zero_vec(blk[j]);
+          for (int r = 0; r < cnt; r += RG * U) {
+            V x[U][NV];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+              const int rr = r + uu * RG + rs;
+              const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, rr & 31);
+              const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
+#pragma unroll
+              for (int j = 0; j < NV; ++j) {
+                if (rr < cnt && use[j]) x[uu][j] = __ldg(row + G * j);
+                else zero_vec(x[uu][j]);
+              }
+            }
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+              for (int j = 0; j < NV; ++j) add_same(blk[j], x[uu][j]);
+          }
+          // the RG row slots' sums
+#pragma unroll
+          for (int off = G; off < 32; off <<= 1)
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              V o;
+              if constexpr (VW == 4) {
+                o.x = __shfl_xor_sync(0xffffffffu, blk[j].x, off);
+                o.y = __shfl_xor_sync(0xffffffffu, blk[j].y, off);
+                o.z = __shfl_xor_sync(0xffffffffu, blk[j].z, off);
+                o.w = __shfl_xor_sync(0xffffffffu, blk[j].w, off);
+              } else {
+                o.x = __shfl_xor_sync(0xffffffffu, blk[j].x, off);
+                o.y = __shfl_xor_sync(0xffffffffu, blk[j].y, off);
+              }
+              add_same(blk[j], o);
+            }
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            const double e[4] = {(double)vec_at(blk[j], 0), (double)vec_at(blk[j], 1), (double)vec_at(blk[j], 2 % VW),
+                                 (double)vec_at(blk[j], 3 % VW)};
+#pragma unroll
+            for (int q = 0; q < VW; ++q)
+              if (m[j][q] != 0xFFFF) sacc[m[j][q]] += e[q];
+          }
+        }
+        __syncwarp();  // groups of different colours may map to the same N'' entries
+      }
+    }
+    gather_epilogue<T, 32, double>(a, sacc, it, v, heavy, lane, 0xffffffffu);
+    __syncwarp();
+  }
+}
+
+template <typename T, int G, int NV, int U>
+void rows_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = G * NV * VW;
+  auto kern = k_gather_rows<T, G, NV, U>;
+  const size_t row = (size_t)a.W_out * sizeof(double);
+  int warps = 8;
+  while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
+  const int threads = warps * 32;
+  const size_t smem = row * warps;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, threads, smem, num_sms);
+  const int nch = (a.W_in + CAP - 1) / CAP;
+  kern<<<grid, threads, smem, s>>>(a, nch);
+}
+
 template <typename T, int NV, int U, int MINB = 2>
 void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
@@ -843,6 +1000,38 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
     } else {
       if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);
       else ldg_go<T, 4, 2>(a, num_sms, s);
+    }
+    return;
+  }
+  // narrow rows: 4 (default) = long lists on k_gather_rows, the rest on
+  // k_gather_ring; 0 = rings only; 1-3 = k_gather_rows only (tuning)
+  const int nr = env_int("CC_NARROW_IMPL", 4);
+  if (nr == 4 && wvec <= 16 && a.item_to < 0) {
+    // long lists (items before a.item_split) on warp-per-item row-parallel
+    // loads, the short tail on sub-warp rings
+    GatherArgs h = a, t = a;
+    h.item_to = a.item_split;
+    t.item_from = a.item_split;
+    t.item_to = a.work.n_seg + a.work.n_light;
+    if (h.item_to > 0) {
+      if (wvec <= 4) rows_go<T, 4, 1, 4>(h, num_sms, s);
+      else if (wvec <= 8) rows_go<T, 8, 1, 4>(h, num_sms, s);
+      else rows_go<T, 8, 2, 4>(h, num_sms, s);
+    }
+    if (t.item_from < t.item_to) gather_typed<T>(t, num_sms, s);
+    return;
+  }
+  if (nr >= 1 && nr <= 3 && wvec <= 16) {
+    if (wvec <= 4) {
+      if (nr == 2) rows_go<T, 4, 1, 2>(a, num_sms, s);
+      else rows_go<T, 4, 1, 4>(a, num_sms, s);
+    } else if (wvec <= 8) {
+      if (nr == 2) rows_go<T, 8, 1, 2>(a, num_sms, s);
+      else rows_go<T, 8, 1, 4>(a, num_sms, s);
+    } else {
+      if (nr == 2) rows_go<T, 8, 2, 2>(a, num_sms, s);
+      else if (nr == 3) rows_go<T, 16, 1, 4>(a, num_sms, s);
+      else rows_go<T, 8, 2, 4>(a, num_sms, s);
     }
     return;
   }

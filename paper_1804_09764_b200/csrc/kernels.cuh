@@ -56,6 +56,9 @@ struct GatherArgs {
   const void *src;        // passive table P' (rows x ld_src), W_in = C(k-1, p-1) valid columns
   int64_t ld_src;
   int W_in;
+  int64_t item_from = 0;  // narrow-row kernels: this launch takes items [item_from, item_to)
+  int64_t item_to = -1;   // (-1: all items)
+  int64_t item_split = 0; // first light item with <= 32 neighbours (items are in degree order)
   const uint16_t *map;    // [c_u][c_v][map_ld] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
   int64_t map_ld;         // map row stride (multiple of 8 entries, padding = 0xFFFF)
   const uint32_t *skip = nullptr;  // [k-1][skip_words]: bit v of word w set = 16-byte vector 32 w + v of a
