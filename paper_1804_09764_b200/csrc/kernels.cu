@@ -321,14 +321,21 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
   const int W = WA + WN;
   const size_t bstride = ((size_t)S * V * W * sizeof(T) + 15) / 16 * 16 / sizeof(T);
   T *bufs = reinterpret_cast<T *>(smem_raw);
-  uint16_t *zs = reinterpret_cast<uint16_t *>(bufs + (size_t)nbuf * bstride);
-  for (int i = threadIdx.x; i < nblocks * zld; i += blockDim.x) zs[i] = ztab[i];
+  // the cover in shared memory as 32-bit entries: the staged-tile byte
+  // offset (column x CB) of each active / passive set, then the raw output
+  // columns -- one LDS.128 gives 4 ready addresses
+  constexpr uint32_t CB = S * sizeof(LV);
+  uint32_t *zs = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * bstride);
+  for (int i = threadIdx.x; i < nblocks * zld; i += blockDim.x) {
+    const uint32_t x = ztab[i];
+    zs[i] = (i % zld) < NA + NN ? x * CB : x;
+  }
   // fused root (per_vertex != nullptr): the outputs are not stored; each
   // output T'(v, X') (rounded to the storage type, as the stored table would
   // be) is multiplied in fp64 by the staged N''(v, comp X') -- the root step
   // (Eq. 2 at the root) shares this step's passive -- and the per-warp sums
   // are added in warp order into X_v (Eq. 3's summand)
-  double *red = reinterpret_cast<double *>(smem_raw + ((size_t)nbuf * bstride * sizeof(T) + (size_t)nblocks * zld * 2 + 7) / 8 * 8);
+  double *red = reinterpret_cast<double *>(smem_raw + ((size_t)nbuf * bstride * sizeof(T) + (size_t)nblocks * zld * 4 + 7) / 8 * 8);
   const int64_t ntiles = (n + TV - 1) / TV;
   auto stage = [&](int64_t tile, T *b) {
     const int64_t v0 = tile * TV;
@@ -356,24 +363,22 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
     __syncthreads();
     const char *Ab = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + lane);
     const char *Nb = reinterpret_cast<const char *>(reinterpret_cast<const LV *>(cur) + (size_t)WA * S + lane);
-    constexpr uint32_t CB = S * sizeof(LV);
     const int64_t vb = tile * TV + (int64_t)lane * V;
     double rsum[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) rsum[i] = 0.0;
     for (int zb = warp; zb < nblocks; zb += nwarp) {
-      const uint16_t *e = zs + (size_t)zb * zld;
-      // block entries read 4 at a time (one 8-byte broadcast load per 4
-      // column indices instead of one 2-byte load each)
-      const uint2 *e4 = reinterpret_cast<const uint2 *>(e);
-      auto idx = [&](int i) -> uint32_t {
-        const uint2 w = e4[i >> 2];
-        const uint32_t h = (i & 2) ? w.y : w.x;
-        return (i & 1) ? h >> 16 : h & 0xFFFFu;
+      const uint32_t *e = zs + (size_t)zb * zld;
+      // block entries read 4 at a time (one 16-byte broadcast load per 4
+      // ready byte offsets)
+      const uint4 *e4 = reinterpret_cast<const uint4 *>(e);
+      auto off = [&](int i) -> uint32_t {
+        const uint4 w = e4[i >> 2];
+        return (i & 3) == 0 ? w.x : (i & 3) == 1 ? w.y : (i & 3) == 2 ? w.z : w.w;
       };
       LV nv[NN];
 #pragma unroll
-      for (int j = 0; j < NN; ++j) nv[j] = *reinterpret_cast<const LV *>(Nb + idx(NA + j) * CB);
+      for (int j = 0; j < NN; ++j) nv[j] = *reinterpret_cast<const LV *>(Nb + off(NA + j));
       T acc[ZS][V];
 #pragma unroll
       for (int zz = 0; zz < ZS; ++zz)
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
         for (int i = 0; i < V; ++i) acc[zz][i] = (T)0;
 #pragma unroll
       for (int a = 0; a < NA; ++a) {
-        const LV av = *reinterpret_cast<const LV *>(Ab + idx(a) * CB);
+        const LV av = *reinterpret_cast<const LV *>(Ab + off(a));
 #pragma unroll
         for (int q = 0; q <= PS; ++q)
 #pragma unroll
@@ -391,8 +396,8 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
       }
 #pragma unroll
       for (int zz = 0; zz < ZS; ++zz) {
-        const uint16_t oc = e[NA + NN + zz];
-        if (oc != 0xFFFF) {
+        const uint32_t oc = e[NA + NN + zz];
+        if (oc != 0xFFFFu) {
           if (per_vertex) {
             const LV ny = *reinterpret_cast<const LV *>(Nb + (uint32_t)__ldg(comp + oc) * CB);
 #pragma unroll
@@ -630,7 +635,7 @@ int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
   const size_t cap = 227 * 1024;
   const size_t tile = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
   // (+ the fused root's per-warp vertex sums: 16 warps x 32 doubles)
-  const size_t zbytes = ((size_t)nblocks * zld * 2 + 7) / 8 * 8 + (per_vertex ? 16 * 32 * 8 : 0);
+  const size_t zbytes = ((size_t)nblocks * zld * 4 + 7) / 8 * 8 + (per_vertex ? 16 * 32 * 8 : 0);
   if (tile + zbytes > cap) return 0;
   // two single-buffered CTAs of 8 warps per SM when they fit (one computes
   // while the other stages or waits at its barrier; measured 5% faster on
