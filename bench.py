@@ -328,7 +328,7 @@ def run_ours(args, cfg, rank, world, dist):
                              "dram_frac": traffic / (top_ms * 1e-3) / 1e9 / peak if traffic and top_ms else None,
                              "note": "algorithmic bytes include L2 hits on hub rows, so frac can exceed 1; "
                                      "traffic = ncu DRAM read+write bytes of the same launch"},
-                "gather_family": {"launches_per_step": stats["gather_launches"],
+                "gather_family": {"passes_per_step": stats["gather_launches"],
                                   "algorithmic_bytes_per_step": agg_bytes, "ms_per_step": agg_avg_ms,
                                   "achieved_gbs": agg_bytes / (agg_avg_ms * 1e-3) / 1e9 if agg_avg_ms > 0 else None},
                 "model_bytes_per_step": stats["model_bytes"],

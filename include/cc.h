@@ -275,8 +275,8 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * last count (0: none, 1: root dot with the active table, 2: self dot with
  * the lifted neighbour sum -- both in the last gather's epilogue; 3: root dot
  * in the epilogue of the combine that produces the root's active table), out[6] / out[7] (cap >= 8) = algorithmic bytes
- * and device ms of the longest neighbour-sum launch, out[8] = number of
- * neighbour-sum launches, out[9] = halo bytes received by this rank (1D
+ * and device ms of the longest neighbour-sum pass, out[8] = number of
+ * neighbour-sum passes (a narrow-row pass is one or two kernels), out[9] = halo bytes received by this rank (1D
  * partition), out[10] (cap >= 11) = the exchange schedule in use
  * (0: none -- one rank or replicas, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING).
  * cap >= 5. */

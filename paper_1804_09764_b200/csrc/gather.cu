@@ -978,7 +978,7 @@ void ring_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
 }
 
 template <typename T>
-void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
+int gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {  // returns the launches
   constexpr int VW = Vec<T>::W;
   const int wvec = (a.W_in + VW - 1) / VW;
   const char *impl = getenv("CC_GATHER_IMPL");  // "ring" / "ldg" for every width; default: by width
@@ -1001,7 +1001,7 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
       if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);
       else ldg_go<T, 4, 2>(a, num_sms, s);
     }
-    return;
+    return 1;
   }
   // narrow rows: 4 (default) = long lists on k_gather_rows, the rest on
   // k_gather_ring; 0 = rings only; 1-3 = k_gather_rows only (tuning)
@@ -1013,13 +1013,15 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
     h.item_to = a.item_split;
     t.item_from = a.item_split;
     t.item_to = a.work.n_seg + a.work.n_light;
+    int launches = 0;
     if (h.item_to > 0) {
       if (wvec <= 4) rows_go<T, 4, 1, 4>(h, num_sms, s);
       else if (wvec <= 8) rows_go<T, 8, 1, 4>(h, num_sms, s);
       else rows_go<T, 8, 2, 4>(h, num_sms, s);
+      ++launches;
     }
-    if (t.item_from < t.item_to) gather_typed<T>(t, num_sms, s);
-    return;
+    if (t.item_from < t.item_to) launches += gather_typed<T>(t, num_sms, s);
+    return launches;
   }
   if (nr >= 1 && nr <= 3 && wvec <= 16) {
     if (wvec <= 4) {
@@ -1033,7 +1035,7 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
       else if (nr == 3) rows_go<T, 16, 1, 4>(a, num_sms, s);
       else rows_go<T, 8, 2, 4>(a, num_sms, s);
     }
-    return;
+    return 1;
   }
   const int vr = env_int("CC_RING_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
   // narrow rows: small rings (more resident groups) measured faster
@@ -1052,6 +1054,7 @@ void gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {
   else if (wvec <= 64) ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
   else if (vr == 1) ring_go<T, 32, 4, 5, 2>(a, num_sms, s);
   else ring_go<T, 32, 4, 4, 2>(a, num_sms, s);
+  return 1;
 }
 
 }  // namespace
@@ -1131,9 +1134,7 @@ int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t 
 
 int launch_gather(int elem, const GatherArgs &a, int num_sms, cudaStream_t s) {
   if (a.work.n_seg + a.work.n_light == 0) return 0;
-  if (elem == 8) gather_typed<double>(a, num_sms, s);
-  else gather_typed<float>(a, num_sms, s);
-  return 1;
+  return elem == 8 ? gather_typed<double>(a, num_sms, s) : gather_typed<float>(a, num_sms, s);
 }
 
 }  // namespace dev
