@@ -243,3 +243,30 @@ def test_exchange_model(cc, world):
             assert m["ring_s"] == pytest.approx(m["grouped_s"], rel=1e-12)
     with pytest.raises(cc.CCError):
         cc.cc_exchange_model(g.n, g.row_ptr, g.col, 1, 0)
+
+
+def test_no_fallback_without_the_library(tmp_path):
+    """The product path fails loudly: the package without libcc.so raises
+    ImportError (there is no CPU fallback), and without a GPU cc_create
+    reports a CUDA error instead of computing anything."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1804_09764_b200")
+    dst = tmp_path / "paper_1804_09764_b200"
+    dst.mkdir()
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            shutil.copy(os.path.join(pkg, f), dst / f)
+    r = subprocess.run([sys.executable, "-c", "import paper_1804_09764_b200"], cwd=tmp_path,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr and "not built" in r.stderr
+
+
+def test_create_without_a_gpu_is_an_error(cc):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(cc.CCError) as e:
+        cc.cc_create(device=0)
+    assert e.value.status == cc.CC_ERR_CUDA
