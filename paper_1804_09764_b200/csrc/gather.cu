@@ -792,8 +792,8 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
 // of a chunk of <= 32 rows the RG slot sums are combined by XOR shuffles
 // (fp32 block of <= 32 rows, then fp64: DESIGN.md C-6) and expanded into the
 // fp64 N'' row through the colour-pair map, vector j by slot j mod RG.
-template <typename T, int G, int NV, int U>
-__global__ void __launch_bounds__(256, 2) k_gather_rows(GatherArgs a, int nch) {
+template <typename T, int G, int NV, int U, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr int RG = 32 / G;
@@ -928,7 +928,12 @@ template <typename T, int G, int NV, int U>
 void rows_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
-  auto kern = k_gather_rows<T, G, NV, U>;
+  // 3 CTAs of 8 warps per SM (<= 85 registers, no spills): configs[2] -4%,
+  // configs[3] -1 to -2% against 2 CTAs
+  const int minb = env_int("CC_ROWS_MINB", 3);
+  auto kern = minb == 4   ? k_gather_rows<T, G, NV, U, 4>
+              : minb == 2 ? k_gather_rows<T, G, NV, U, 2>
+                          : k_gather_rows<T, G, NV, U, 3>;
   const size_t row = (size_t)a.W_out * sizeof(double);
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
