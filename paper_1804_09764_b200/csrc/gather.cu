@@ -1048,12 +1048,14 @@ int gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {  // returns
   // D 4: 31.5 -> 19.8 ms, the lean kernel 27.8 ms)
   if (wvec <= 4) {
     if (vr == 2) ring_go<T, 4, 1, 3, 2>(a, num_sms, s);
-    else ring_go<T, 4, 1, 4, 2>(a, num_sms, s);
+    else if (vr == 4) ring_go<T, 4, 1, 4, 2>(a, num_sms, s);
+    else ring_go<T, 4, 1, 4, 3>(a, num_sms, s);  // 3 CTAs/SM: configs[2] -1.5%
   } else if (wvec <= 8) ring_go<T, 8, 1, 4, 2>(a, num_sms, s);
   else if (wvec <= 16) {
     if (vr == 2) ring_go<T, 8, 2, 3, 2>(a, num_sms, s);
     else if (vr == 3) ring_go<T, 16, 1, 4, 2>(a, num_sms, s);
-    else ring_go<T, 8, 2, 4, 2>(a, num_sms, s);
+    else if (vr == 4) ring_go<T, 8, 2, 4, 2>(a, num_sms, s);
+    else ring_go<T, 8, 2, 4, 3>(a, num_sms, s);
   }
   else if (wvec <= 32) ring_go<T, 32, 1, 16, 2>(a, num_sms, s);
   else if (wvec <= 64) ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
