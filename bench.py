@@ -364,6 +364,11 @@ def run_ours(args, cfg, rank, world, dist):
 
 def main():
     args = parse()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+    if local_world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # every rank validates and partitions the whole graph on the host (OpenMP):
+        # share the host cores instead of oversubscribing them N times
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
     import synth
     cfg = synth.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
