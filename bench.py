@@ -365,9 +365,10 @@ def run_ours(args, cfg, rank, world, dist):
 def main():
     args = parse()
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
-    if local_world > 1 and "OMP_NUM_THREADS" not in os.environ:
+    if local_world > 1:
         # every rank validates and partitions the whole graph on the host (OpenMP):
-        # share the host cores instead of oversubscribing them N times
+        # share the host cores (torchrun's default OMP_NUM_THREADS=1 would make
+        # that serial, the OpenMP default would oversubscribe them N times)
         os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
     import synth
     cfg = synth.CONFIGS[args.config]
