@@ -123,3 +123,44 @@ def test_halo_exchange_gloo(world, schedule):
         errs.append(errq.get())
     assert not errs, errs
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+def _opts_worker(rank, world, port, errq, outq):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        os.environ["LOCAL_RANK"] = str(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import ctypes
+
+        import paper_1804_09764_b200 as cc
+        opt, buf = cc.distributed_options(precision=cc.CC_FP32, exchange=cc.CC_EXCHANGE_RING)
+        uid = ctypes.string_at(opt.nccl_id, 128)
+        outq.put((rank, opt.world, opt.rank, opt.device, opt.precision, opt.exchange, uid))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+def test_distributed_options_share_one_nccl_id():
+    """The torch.distributed plumbing bench.py uses for N > 1: every rank
+    gets world / rank / device from the process group and the SAME
+    128-byte NCCL unique id (generated on rank 0, broadcast)."""
+    import __graft_entry__
+    __graft_entry__._product_build()
+    ctx = mp.get_context("spawn")
+    errq, outq = ctx.SimpleQueue(), ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_opts_worker, args=(r, 2, port, errq, outq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    got = sorted(outq.get() for _ in range(2))
+    assert [g[:6] for g in got] == [(0, 2, 0, 0, 1, 2), (1, 2, 1, 1, 1, 2)]
+    assert got[0][6] == got[1][6] and any(got[0][6])
