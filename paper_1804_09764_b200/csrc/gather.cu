@@ -952,7 +952,13 @@ void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   // fp32 tables with N'' rows wider than 1600 entries (configs[4]'s root:
   // 3432) keep the shared-memory row in fp32 so that 16 warps fit per SM
   // (each entry adds at most k-1 colour-group block sums; C-6)
-  const bool acc32 = sizeof(T) == 4 && a.W_out > 1600;
+  // fp32 tables keep the shared-memory N'' row in fp32 (scaled by 2^-64):
+  // half the shared memory leaves more L1 for the rows (configs[3]: gathers
+  // -1.5 to -2%), and rows wider than 1600 entries (configs[4]'s fused root)
+  // need it to fit 16 warps per SM.  Each entry adds at most ceil(s/32) +
+  // k - 1 fp32 block sums (C-6); CC_ACC32=0 keeps fp64 rows where
+  // they fit.
+  const bool acc32 = sizeof(T) == 4 && (a.W_out > 1600 || (env_int("CC_ACC32", 1) && !a.root_mode));
   auto kern = acc32 ? k_gather_ldg<T, NV, U, float, MINB> : k_gather_ldg<T, NV, U, double, MINB>;
   const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
