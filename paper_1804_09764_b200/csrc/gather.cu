@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
 // of a chunk of <= 32 rows the RG slot sums are combined by XOR shuffles
 // (fp32 block of <= 32 rows, then fp64: DESIGN.md C-6) and expanded into the
 // fp64 N'' row through the colour-pair map, vector j by slot j mod RG.
-template <typename T, int G, int NV, int U, int MINB = 2>
+template <typename T, int G, int NV, int U, int MINB = 2, typename AccT = double>
 __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
   constexpr int CAP = G * NV * VW;  // columns per pass
   extern __shared__ __align__(16) unsigned char sacc_raw[];
   const int lane = threadIdx.x & 31, vl = lane % G, rs = lane / G;
-  double *sacc = reinterpret_cast<double *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)a.W_out;
+  AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)a.W_out;
   const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const char *__restrict__ srcb = static_cast<const char *>(a.src);
@@ -913,13 +913,13 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
                                  (double)vec_at(blk[j], 3 % VW)};
 #pragma unroll
             for (int q = 0; q < VW; ++q)
-              if (m[j][q] != 0xFFFF) sacc[m[j][q]] += e[q];
+              if (m[j][q] != 0xFFFF) sacc[m[j][q]] += (AccT)(e[q] * AccScale<AccT>::in);
           }
         }
         __syncwarp();  // groups of different colours may map to the same N'' entries
       }
     }
-    gather_epilogue<T, 32, double>(a, sacc, it, v, heavy, lane, 0xffffffffu);
+    gather_epilogue<T, 32, AccT>(a, sacc, it, v, heavy, lane, 0xffffffffu);
     __syncwarp();
   }
 }
@@ -931,10 +931,11 @@ void rows_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   // 3 CTAs of 8 warps per SM (<= 85 registers, no spills): configs[2] -4%,
   // configs[3] -1 to -2% against 2 CTAs
   const int minb = env_int("CC_ROWS_MINB", 3);
-  auto kern = minb == 4   ? k_gather_rows<T, G, NV, U, 4>
-              : minb == 2 ? k_gather_rows<T, G, NV, U, 2>
-                          : k_gather_rows<T, G, NV, U, 3>;
-  const size_t row = (size_t)a.W_out * sizeof(double);
+  // fp32 tables: fp32 shared-memory rows as in the lean gather (C-6)
+  const bool acc32 = sizeof(T) == 4 && env_int("CC_ACC32", 1);
+  auto kern = acc32 ? (minb == 2 ? k_gather_rows<T, G, NV, U, 2, float> : k_gather_rows<T, G, NV, U, 3, float>)
+                    : (minb == 2 ? k_gather_rows<T, G, NV, U, 2, double> : k_gather_rows<T, G, NV, U, 3, double>);
+  const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
   const int threads = warps * 32;
