@@ -124,20 +124,39 @@ def dominant_traffic(config_idx: int, precision: str):
     return None, None
 
 
-def method_updates(g_nnz: int, parent) -> float:
-    """U = sum over distinct passive sub-templates of 2m * C(k, p)."""
-    import paper_1804_09764_b200 as cc
+def updates_per_entry(parent) -> int:
+    """sum over the DISTINCT passive sub-templates of C(k, p) (U =
+    that x 2m), for the paper's own partition of the template: root = the
+    parent -1 vertex, each sub-template (x, j) = x with its first j children
+    split into (x, j-1) + the full subtree of child j (PAPER.md lines 110-113,
+    122), isomorphic passives counted once.  Plain Python, so that both arms
+    use the same U and the reference arm never loads the product library."""
     k = len(parent)
-    plan = cc.cc_plan_template(parent)
-    seen = set()
-    u = 0.0
-    for s in plan["steps"]:
-        key = s["passive"] if s["p"] > 1 else "hist"
-        if key in seen:
-            continue
-        seen.add(key)
-        u += g_nnz * math.comb(k, s["p"])
+    children = [[] for _ in range(k)]
+    root = parent.index(-1)
+    for v, p in enumerate(parent):
+        if p >= 0:
+            children[p].append(v)
+
+    def code(x):  # AHU canonical code of the full subtree at x
+        return "(" + "".join(sorted(code(y) for y in children[x])) + ")"
+
+    def size(x):
+        return 1 + sum(size(y) for y in children[x])
+
+    seen, u = set(), 0
+    for x in range(k):
+        for y in children[x]:  # every child subtree is a passive part of some step
+            key = code(y) if size(y) > 1 else "leaf"
+            if key not in seen:
+                seen.add(key)
+                u += math.comb(k, size(y))
+    del root
     return u
+
+
+def method_updates(g_nnz: int, parent) -> float:
+    return float(g_nnz) * updates_per_entry(parent)
 
 
 # ---------------------------------------------------------------- oracle (CPU) timing
@@ -272,13 +291,9 @@ def run_ours(args, cfg, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    updates_local = stats["updates"]
-    if dist is not None:
-        t = torch.tensor([updates_local], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
-        updates = float(t.item())
-    else:
-        updates = updates_local
+    # U per colouring (the whole job: every adjacency entry is processed by
+    # its owner once per distinct passive); replicas: world colourings per step
+    updates = method_updates(g.nnz, cfg.parent) * (world if (args.replicas and world > 1) else 1)
     value = updates / (ms_per_step * 1e-3) / 1e9
 
     # e2e: public API with host inputs (a colouring passed in from pinned host
@@ -353,6 +368,10 @@ def run_ours(args, cfg, rank, world, dist):
                             "peak_gbs": 900.0, "peak_source": "nominal NVLink 5 per direction per GPU"}
                            if world > 1 and not args.replicas else None),
                 "clocks": clk}
+        if world > 1:
+            sizes = nccl_comm_sizes()
+            line["nccl"] = {"comm_nranks": sizes, "comm_nranks_ok": bool(sizes) and all(x == world for x in sizes),
+                            "log_dir": os.environ.get("CC_NCCL_LOG_DIR")}
         if not args.no_cpu_baseline and world == 1:
             scale = args.cpu_scale or auto_cpu_scale(cfg)
             v, ms, desc = oracle_sample(cfg, scale, args.seed)
@@ -362,8 +381,57 @@ def run_ours(args, cfg, rank, world, dist):
     cc.cc_destroy(ctx)
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: start N ranks (one
+    process per GPU) through torch.distributed.run on this node and return
+    its exit code.  NCCL's INIT log of every rank goes to files under
+    $CC_NCCL_LOG_DIR (default /tmp/cc_nccl_logs) so the communicator sizes can be
+    checked; rank 0's JSON line is the only line on stdout."""
+    import torch
+    have = torch.cuda.device_count()
+    if args.impl != "reference" and have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    logdir = env.setdefault("CC_NCCL_LOG_DIR", "/tmp/cc_nccl_logs")
+    os.makedirs(logdir, exist_ok=True)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", os.path.join(logdir, "nccl.%h.%p.log"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def nccl_comm_sizes() -> list:
+    """nRanks of every NCCL communicator this process initialised (from its
+    NCCL INIT log, when NCCL_DEBUG_FILE was set by self_launch)."""
+    import glob
+    import re
+    logdir = os.environ.get("CC_NCCL_LOG_DIR")
+    if not logdir:
+        return []
+    sizes = []
+    for p in glob.glob(os.path.join(logdir, f"nccl.*.{os.getpid()}.log")):
+        with open(p, errors="replace") as f:
+            for line in f:
+                m = re.search(r"comm 0x[0-9a-f]+ rank (\d+) nRanks (\d+)", line)
+                if m:
+                    sizes.append(int(m.group(2)))
+    return sizes
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
     if local_world > 1:
         # every rank validates and partitions the whole graph on the host (OpenMP):
@@ -374,8 +442,9 @@ def main():
     cfg = synth.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world != args.gpus and "WORLD_SIZE" in os.environ:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     dist = None
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

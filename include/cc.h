@@ -63,8 +63,14 @@ typedef enum {
 /* Table precision (reading C-6; the paper states none). */
 enum {
   CC_FP64 = 0, /* fp64 tables and accumulation: exact for integers < 2^53 */
-  CC_FP32 = 1  /* fp32 table storage; fp64 neighbour-sum accumulation,
-                  fp64 root products and fp64 final reduction */
+  CC_FP32 = 1  /* fp32 table storage.  Neighbour sums: fp32 over blocks of at
+                  most 32 neighbour rows of one colour group, the blocks added
+                  into the vertex's N'' row held in shared memory in fp32
+                  scaled by 2^-64 (acc32 knob, default) or fp64 (short-list
+                  kernels, acc32 = 0); heavy-segment partial rows and their
+                  sum in fp64; combine split sums fp32 FMA; root products and
+                  the final reduction fp64.  Worst-case relative error of X
+                  ~8e-5 (reading C-6), measured 1e-10..1e-9 */
 };
 
 /* Halo-exchange schedule of the 1D partition (cc_options.exchange; PAPER.md
@@ -254,6 +260,17 @@ cc_status cc_get_subtree_counts(cc_ctx *ctx, int32_t x, double *out);
  * after their table is produced).  world == 1 only.  Errors: CC_ERR_ARG (bad
  * x / id / pointer), CC_ERR_STATE. */
 cc_status cc_get_subtree_rows(cc_ctx *ctx, int32_t x, const int32_t *vertices, int32_t nv, double *out);
+
+/* Implementation knobs (A/B switches of the launchers; every setting
+ * computes the same values): name is one of fused_root, sector_skip,
+ * gather_impl, narrow_impl, narrow_split, csort_small, combine_impl, acc32,
+ * phase_events, hub_l2_pct, grid_reserve (meanings and defaults: DESIGN.md
+ * section 9a).  Each context reads CC_<NAME> from the environment ONCE, in
+ * cc_create; these calls change or read the context's value.  CC_ERR_ARG on
+ * an unknown name or a NULL pointer.  Not collective: set the same value on
+ * every rank. */
+cc_status cc_set_knob(cc_ctx *ctx, const char *name, int32_t value);
+cc_status cc_get_knob(cc_ctx *ctx, const char *name, int32_t *value);
 
 /* Per-kernel timing events on (1, default) or off (0): off, cc_last_profile
  * reports only the total and the colouring, and cc_last_stats the bytes but

@@ -162,6 +162,17 @@ def cc_get_subtree_counts(ctx, x: int, n: int, k: int, size: int) -> np.ndarray:
     return out
 
 
+def cc_set_knob(ctx, name: str, value: int) -> None:
+    """Implementation knob of this context (every value computes the same result)."""
+    _check(ctx, _lib.cc_set_knob(ctx, name.encode(), int(value)))
+
+
+def cc_get_knob(ctx, name: str) -> int:
+    v = ctypes.c_int32()
+    _check(ctx, _lib.cc_get_knob(ctx, name.encode(), ctypes.byref(v)))
+    return v.value
+
+
 def cc_set_profiling(ctx, on: bool) -> None:
     _check(ctx, _lib.cc_set_profiling(ctx, 1 if on else 0))
 

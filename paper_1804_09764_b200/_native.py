@@ -61,6 +61,8 @@ SIGNATURES = {
     "cc_niter": (c_i32, [c_dbl, c_dbl, c_i32, c_dbl, vp]),
     "cc_last_profile": (c_i32, [vp, vp, c_i32, vp]),
     "cc_set_profiling": (c_i32, [vp, c_i32]),
+    "cc_set_knob": (c_i32, [vp, ctypes.c_char_p, c_i32]),
+    "cc_get_knob": (c_i32, [vp, ctypes.c_char_p, vp]),
     "cc_last_stats": (c_i32, [vp, vp, c_i32]),
     "cc_colex_rank": (c_i64, [c_u32]),
     "cc_colex_unrank": (c_u32, [c_i32, c_i64]),

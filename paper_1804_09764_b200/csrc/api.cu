@@ -1,7 +1,9 @@
 // api.cu -- the C ABI of include/cc.h: argument checks, state machine,
 // error conversion (no C++ exception crosses the boundary).
 #include <algorithm>
+#include <cctype>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -71,6 +73,33 @@ void alloc_scratch(cc_ctx *c) {
   c->n_partials = cc::dev::root_partials_blocks(c->num_sms);
   c->d_partials = c->pmalloc<double>((size_t)c->n_partials);
   c->d_result = c->pmalloc<double>(1);
+}
+
+// Implementation knobs by name.
+int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
+  if (name == "fused_root") return &k.fused_root;
+  if (name == "sector_skip") return &k.sector_skip;
+  if (name == "gather_impl") return &k.gather_impl;
+  if (name == "narrow_impl") return &k.narrow_impl;
+  if (name == "narrow_split") return &k.narrow_split;
+  if (name == "csort_small") return &k.csort_small;
+  if (name == "combine_impl") return &k.combine_impl;
+  if (name == "acc32") return &k.acc32;
+  if (name == "phase_events") return &k.phase_events;
+  if (name == "hub_l2_pct") return &k.hub_l2_pct;
+  if (name == "grid_reserve") return &k.grid_reserve;
+  return nullptr;
+}
+
+// CC_<NAME> from the environment, read once per context
+void knobs_from_env(cc::dev::Knobs &k) {
+  static const char *names[] = {"fused_root", "sector_skip", "gather_impl", "narrow_impl", "narrow_split",
+                                "csort_small", "combine_impl", "acc32", "phase_events", "hub_l2_pct", "grid_reserve"};
+  for (const char *n : names) {
+    std::string env = "CC_";
+    for (const char *q = n; *q; ++q) env += (char)std::toupper((unsigned char)*q);
+    if (const char *v = std::getenv(env.c_str())) *knob_ptr(k, n) = std::atoi(v);
+  }
 }
 
 // dense colex index (k-universe) -> compressed index of the row of colour c
@@ -160,6 +189,7 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   std::unique_ptr<cc_ctx> c(new cc_ctx());
   c->opt = *opt;
   c->opt.nccl_id = nullptr;
+  knobs_from_env(c->knobs);
   try {
     CUDA_OK(cudaSetDevice(opt->device));
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, opt->device));
@@ -499,6 +529,25 @@ cc_status cc_get_subtree_rows(cc_ctx *c, int32_t x, const int32_t *vertices, int
     }
   }
   API_END(c)
+}
+
+cc_status cc_set_knob(cc_ctx *c, const char *name, int32_t value) {
+  if (!c || !name) return CC_ERR_ARG;
+  int *p = knob_ptr(c->knobs, name);
+  if (!p) {
+    c->err = std::string("unknown knob ") + name;
+    return CC_ERR_ARG;
+  }
+  *p = value;
+  return CC_OK;
+}
+
+cc_status cc_get_knob(cc_ctx *c, const char *name, int32_t *value) {
+  if (!c || !name || !value) return CC_ERR_ARG;
+  int *p = knob_ptr(c->knobs, name);
+  if (!p) return CC_ERR_ARG;
+  *value = *p;
+  return CC_OK;
 }
 
 cc_status cc_set_profiling(cc_ctx *c, int32_t on) {

@@ -91,6 +91,7 @@ struct TableCache {
 
 struct cc_ctx {
   cc_options opt{};
+  cc::dev::Knobs knobs;  // implementation switches (env at cc_create, cc_set_knob)
   std::string err;
   bool poisoned = false;
   int num_sms = 148;
@@ -115,6 +116,10 @@ struct cc_ctx {
   int xmode = 0;                       // exchange schedule in use: 0 none, CC_EXCHANGE_GROUPED / _RING
   double xmodel[2] = {0, 0};           // modelled grouped / ring seconds (max over ranks)
   int64_t max_seg = 0, max_hv = 0;
+  // adjacency entries per non-isolated vertex of the GLOBAL graph: the
+  // planner's statistic, identical on every rank (a per-rank figure could
+  // pick different plans on different ranks, and their exchanges would not match)
+  double avg_degree = 0;
 
   // template
   bool has_template = false;
@@ -211,7 +216,13 @@ struct cc_ctx {
     return ev_pool[ev_used++];
   }
   bool profiling = true;     // cc_set_profiling
-  bool phase_events = true;  // per-kernel event pairs for cc_last_profile (CC_PHASE_EVENTS=0: off)
+  bool phase_events = true;  // per-kernel event pairs for cc_last_profile (knob phase_events = 0: off)
+  // SMs the gathers may fill: all, or all but knobs.grid_reserve while a halo
+  // exchange over NCCL is in flight (NCCL's kernels need SMs to progress)
+  int gather_sms(bool exchanging) const {
+    const int r = knobs.grid_reserve >= 0 ? knobs.grid_reserve : (exchanging && comm ? 8 : 0);
+    return exchanging ? std::max(1, num_sms - r) : num_sms;
+  }
   cudaEvent_t begin(cudaStream_t s) {
     if (!phase_events) return nullptr;
     cudaEvent_t b = ev();

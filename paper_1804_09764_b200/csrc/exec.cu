@@ -93,11 +93,24 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
   c->max_seg = std::max(c->max_seg, w.n_seg);
 }
 
-// Stream-ordered buffers with shared ownership (see Buf).
+// Stream-ordered buffers with shared ownership (see Buf).  Whatever is still
+// owned when the executor unwinds (an exception: OOM, a NCCL error, a
+// rendezvous timeout) is released by the destructor, so a failed count does
+// not leave tens of GB in the pool.
 struct Bufs {
   cc_ctx *c;
   std::vector<Buf> pool;
   explicit Bufs(cc_ctx *cx) : c(cx) { pool.reserve(256); }
+  ~Bufs() {
+    for (auto &b : pool)
+      if (b.p && b.owned) {
+        cudaFreeAsync(b.p, c->s_main);  // no throw from a destructor
+        c->cur_bytes -= b.bytes;
+        b.p = nullptr;
+      }
+  }
+  Bufs(const Bufs &) = delete;
+  Bufs &operator=(const Bufs &) = delete;
   int make(size_t bytes) {
     pool.push_back({c->amalloc(bytes, c->s_main), bytes, 1, true});
     return (int)pool.size() - 1;
@@ -114,6 +127,26 @@ struct Bufs {
   void *ptr(int b) const { return b < 0 ? nullptr : pool[b].p; }
 };
 
+// A stream-ordered scratch buffer released on scope exit (also when a launch
+// or a NCCL call throws).
+struct ScopedAsync {
+  cc_ctx *c;
+  cudaStream_t s;
+  size_t bytes = 0;
+  void *p = nullptr;
+  ScopedAsync(cc_ctx *cx, size_t b, cudaStream_t st) : c(cx), s(st), bytes(b) {
+    if (b) p = c->amalloc(b, s);
+  }
+  ~ScopedAsync() {
+    if (p) {
+      cudaFreeAsync(p, s);
+      c->cur_bytes -= bytes;
+    }
+  }
+  ScopedAsync(const ScopedAsync &) = delete;
+  ScopedAsync &operator=(const ScopedAsync &) = delete;
+};
+
 }  // namespace
 
 void allreduce_host(cc_ctx *c, std::vector<double> &v);
@@ -122,6 +155,11 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
   c->part = partition_graph(g, c->pworld(), c->pworld() == 1 ? 0 : c->opt.rank, c->opt.relabel_seed);
   const auto &R = c->part;
   c->n_global = g.n;
+  {
+    int64_t nz = 0;
+    for (int64_t v = 0; v < g.n; ++v) nz += g.rp[v + 1] > g.rp[v];
+    c->avg_degree = nz ? (double)g.col.size() / (double)nz : 0.0;
+  }
   c->n_own = R.n_own;
   c->n_halo = R.n_halo;
   c->n_rows = R.n_own + R.n_halo;
@@ -202,7 +240,7 @@ void replan(cc_ctx *c, bool fixed) {
   o.auto_root = !(fixed || c->opt.fixed_root);
   o.elem = c->elem();
   o.kc = c->user_kc;
-  if (c->has_graph && c->n_own > 0) o.avg_degree = (double)c->part.col.size() / (double)c->n_own;
+  if (c->has_graph && c->avg_degree > 0) o.avg_degree = c->avg_degree;  // rank-invariant (global graph)
   c->plan = make_plan((int)c->user_parent.size(), c->user_parent.data(), &o);
   if (c->has_graph) upload_template(c);
 }
@@ -286,7 +324,8 @@ struct RootFuse {
 };
 
 // N'' = neighbour sum of the passive table P' (size p >= 2) over one pass.
-void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, const RootFuse *rf = nullptr) {
+// sms: the SMs the launch may fill (c->gather_sms)
+void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, const RootFuse *rf, int sms) {
   const int k = c->plan.colours(), elem = c->elem();
   const int W_in = (int)binom(k - 1, p - 1), W_out = (int)binom(k - 1, p);
   dev::GatherArgs a;
@@ -304,26 +343,19 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
     // then light items in degree order) go to the warp-per-item row-parallel
     // kernel, the rest to the sub-warp rings; T = 8 << q = max(32, s / 16)
     // (measured, profiles/r1/SUMMARY.md); none when segments are <= T long
-    const char *ns = getenv("CC_NARROW_SPLIT");
     int q = 2;  // auto: T = max(32, s / 16)
     while (q < 7 && (8 << (q + 1)) <= w.seg_len / 16) ++q;
-    if (ns) q = std::min(7, std::max(0, atoi(ns)));
+    if (c->knobs.narrow_split >= 0) q = std::min(7, c->knobs.narrow_split);
     a.item_split = w.seg_len > (8 << q) ? w.split[q] : 0;
   }
   a.map = c->d_map[p];
   a.map_ld = gather_map_ld(k, p);
-  {
-    const char *sk = getenv("CC_SECTOR_SKIP");
-    if (!(sk && sk[0] == '0')) {
-      a.skip = c->d_skip[p];
-      a.skip_words = c->skip_words[p];
-    }
+  if (c->knobs.sector_skip) {
+    a.skip = c->d_skip[p];
+    a.skip_words = c->skip_words[p];
   }
-  {  // hub rows kept in L2: a fraction of the L2 (rows are degree-ordered, hubs first)
-    const char *f = getenv("CC_HUB_L2_FRAC");
-    const double frac = f ? atof(f) : 0.5;
-    a.hub_rows = (int64_t)(frac * (double)c->l2_bytes / (double)(a.ld_src * elem));
-  }
+  // hub rows kept in L2: a fraction of the L2 (rows are degree-ordered, hubs first)
+  a.hub_rows = (int64_t)(c->knobs.hub_l2_pct / 100.0 * (double)c->l2_bytes / (double)(a.ld_src * elem));
   a.dst = N;
   a.ld_dst = c->ld_of(W_out);
   a.W_out = W_out;
@@ -331,13 +363,9 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   a.accumulate = accumulate;
   a.work = w.view();
   a.ld_scratch = W_out;
-  void *scratch = nullptr;
-  const size_t sbytes = (size_t)w.n_seg * W_out * sizeof(double);
-  if (w.n_seg) {
-    scratch = c->amalloc(sbytes, c->s_main);
-    CUDA_OK(cudaMemsetAsync(c->d_arrive, 0, (size_t)w.n_hv * sizeof(unsigned int), c->s_main));
-  }
-  a.scratch = static_cast<double *>(scratch);
+  ScopedAsync scratch(c, (size_t)w.n_seg * W_out * sizeof(double), c->s_main);
+  if (w.n_seg) CUDA_OK(cudaMemsetAsync(c->d_arrive, 0, (size_t)w.n_hv * sizeof(unsigned int), c->s_main));
+  a.scratch = static_cast<double *>(scratch.p);
   a.arrive = c->d_arrive;
   if (rf) {
     a.root_mode = rf->mode;
@@ -348,10 +376,9 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
     a.per_vertex = rf->per_vertex;
   }
   cudaEvent_t b = c->begin(c->s_main);
-  c->stats[3] += dev::launch_gather(elem, a, c->num_sms, c->s_main);
+  c->stats[3] += dev::launch_gather(elem, a, c->knobs, sms, c->s_main);
   c->check_launch();
   c->end(PH_GATHER, c->s_main, b);
-  if (scratch) c->afree(scratch, sbytes, c->s_main);
   // algorithmic bytes: index stream + compressed rows of the neighbours whose
   // colour differs from the row vertex's (expected fraction (k-1)/k) + N'' rows
   // written (+ read when accumulating)
@@ -433,8 +460,8 @@ cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p, std::vector<std::pair<int, 
   CUDA_OK(cudaStreamWaitEvent(c->s_comm, ready, 0));
   const auto &R = c->part;
   const int64_t send_rows = R.send_off[c->pworld()];
-  const size_t sbytes = (size_t)send_rows * ld * elem;
-  void *sendbuf = send_rows ? c->amalloc(sbytes, c->s_comm) : nullptr;
+  ScopedAsync sb(c, (size_t)send_rows * ld * elem, c->s_comm);  // released after the sends (stream order)
+  void *sendbuf = sb.p;
   cudaEvent_t xb = c->begin(c->s_comm);
   c->stats[3] += dev::launch_pack(elem, P, ld, c->d_send_idx, send_rows, sendbuf, c->s_comm);
   c->check_launch();
@@ -478,7 +505,6 @@ cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p, std::vector<std::pair<int, 
   NCCL_OK(api.GroupEnd());
   }
   c->end(PH_EXCHANGE, c->s_comm, xb);
-  if (sendbuf) c->afree(sendbuf, sbytes, c->s_comm);
   CUDA_OK(cudaEventRecord(recvd, c->s_comm));
   c->stats[1] += (double)send_rows * ld * elem * 2;
   c->stats[9] += (double)(R.recv_off[c->pworld()]) * ld * elem;  // halo bytes received
@@ -487,7 +513,7 @@ cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p, std::vector<std::pair<int, 
 
 void aggregate(cc_ctx *c, void *P, int p, void *N) {
   if (c->pworld() == 1) {
-    gather_pass(c, c->p_full, P, p, N, 0);
+    gather_pass(c, c->p_full, P, p, N, 0, nullptr, c->num_sms);
     return;
   }
   // world > 1: exchange the boundary rows of P' on the comm stream while the
@@ -498,7 +524,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
   std::vector<std::pair<int, cudaEvent_t>> steps;
   const bool ring = c->xmode == CC_EXCHANGE_RING;
   cudaEvent_t recvd = exchange_halo(c, P, p, ring ? &steps : nullptr);
-  gather_pass(c, c->p_local, P, p, N, 0);
+  gather_pass(c, c->p_local, P, p, N, 0, nullptr, c->gather_sms(true));
   if (!ring) steps.push_back({-1, recvd});
   for (const auto &st : steps) {
     Pass &w = st.first < 0 ? c->p_remote : c->p_peer[st.first];
@@ -506,7 +532,7 @@ void aggregate(cc_ctx *c, void *P, int p, void *N) {
     cudaEvent_t wb = c->begin(c->s_main);  // exposed exchange: s_main idles until the rows are in
     CUDA_OK(cudaStreamWaitEvent(c->s_main, st.second, 0));
     c->end(PH_EXPOSED, c->s_main, wb);
-    gather_pass(c, w, P, p, N, 1);
+    gather_pass(c, w, P, p, N, 1, nullptr, c->gather_sms(ring));  // ring: the next step transfers meanwhile
   }
   CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));  // the send buffer's release is ordered after every step
 }
@@ -554,10 +580,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   const int k = pl.colours(), elem = c->elem();
   std::fill(c->stats, c->stats + 11, 0.0);
   c->stats[10] = c->xmode;
-  {
-    const char *pe = getenv("CC_PHASE_EVENTS");
-    c->phase_events = c->profiling && !(pe && pe[0] == '0');
-  }
+  c->phase_events = c->profiling && c->knobs.phase_events;
   c->gather_log.clear();
   c->ev_used = 0;
   c->ev_log.clear();
@@ -596,8 +619,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   std::vector<int> last_use(pl.table_last_use);
   {
     const Step &rs = pl.steps[sr];
-    const char *f = getenv("CC_FUSED_ROOT");
-    if (pl.k == k && !cache && (dump_table < 0 || dump_rows) && !(f && f[0] == '0') && rs.out < 0 && rs.p >= 2) {
+    if (pl.k == k && !cache && (dump_table < 0 || dump_rows) && c->knobs.fused_root && rs.out < 0 && rs.p >= 2) {
       const int P = rs.passive;
       int s_l = -1, users = 0;
       for (int s = 0; s < sr; ++s) {
@@ -624,8 +646,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   bool cr_done = false;
   {
     const Step &rs = pl.steps[sr];
-    const char *f = getenv("CC_FUSED_ROOT");
-    if (!fuse && pl.k == k && !cache && !(f && f[0] == '0') && rs.out < 0 && rs.a > 1 && rs.p >= 2 &&
+    if (!fuse && pl.k == k && !cache && c->knobs.fused_root && rs.out < 0 && rs.a > 1 && rs.p >= 2 &&
         (dump_table < 0 || (dump_rows && dump_table != rs.active)) && pl.table_last_use[rs.active] == sr) {
       for (int s = 0; s < sr; ++s) {
         const Step &cs = pl.steps[s];
@@ -646,7 +667,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     if (pl.steps[s].p == 1) last_hist_use = s;
   double *per_vertex = nullptr;
   if (root_out || fuse || fuse_cr >= 0)
-    per_vertex = static_cast<double *>(c->amalloc((size_t)std::max<int64_t>(n, 1) * 8, c->s_main));
+    per_vertex = static_cast<double *>(bufs.ptr(bufs.make((size_t)std::max<int64_t>(n, 1) * 8)));
   if (cache && cache->sorted) {  // an earlier template of this colouring sorted and built the leaf level
     if (last_hist_use >= 0) hist = bufs.alias(cache->hist, cache->hist_bytes);
   } else if (c->pworld() == 1) {  // colour sort + leaf level N''(v, {y}) in one pass over the adjacency
@@ -664,7 +685,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     Pass &p = c->p_full;
     c->stats[3] += dev::launch_csort_hist(elem, p.beg, p.end, c->d_col, c->d_colors, p.view(), k, c->d_col_sorted,
                                           p.goff, p.desc, hist >= 0 ? bufs.ptr(hist) : nullptr, c->ld_of(k - 1), rows,
-                                          p.small_from, c->num_sms, c->s_main);
+                                          p.small_from, c->knobs, c->num_sms, c->s_main);
     c->check_launch();
     c->end(PH_CSORT, c->s_main, b);
     c->sorted_valid = true;
@@ -740,7 +761,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
         cudaEvent_t recvd = exchange_halo(c, bufs.ptr(T[st.passive]), st.p);
         CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
       }
-      gather_pass(c, c->p_full, bufs.ptr(T[st.passive]), st.p, nullptr, 0, &rf);
+      gather_pass(c, c->p_full, bufs.ptr(T[st.passive]), st.p, nullptr, 0, &rf, c->num_sms);
       cudaEvent_t b = c->begin(c->s_main);
       c->stats[3] += dev::launch_root(8, nullptr, 0, 0, per_vertex, 1, nullptr, n, c->d_partials, c->n_partials,
                                       nullptr, c->d_result, c->s_main);
@@ -794,8 +815,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
         c->stats[3] += dev::launch_combine(elem, bufs.ptr(T[st.active]), c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, Wp,
                                            c->d_split[s], (int)binom(st.t - 1, st.a - 1), n, bufs.ptr(rb),
                                            c->ld_of(Wt), Wt, c->d_ztab[s], c->zblocks[s],
-                                           (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->num_sms,
-                                           c->s_main);
+                                           (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->knobs,
+                                           c->num_sms, c->s_main);
         c->check_launch();
         c->end(PH_COMBINE, c->s_main, b);
         c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;
@@ -830,7 +851,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
                  const int l = dev::launch_combine_root(
                      elem, bufs.ptr(T[st.active]), c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, Wp, c->d_ztab[s],
                      c->zblocks[s], (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->d_comp, n, per_vertex,
-                     c->num_sms, c->s_main);
+                     c->knobs, c->num_sms, c->s_main);
                  if (!l) return false;
                  c->check_launch();
                  c->end(PH_COMBINE, c->s_main, b);
@@ -846,8 +867,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       c->stats[3] += dev::launch_combine(elem, bufs.ptr(T[st.active]), c->ld_of(Wa), Wa, bufs.ptr(nbuf), ldN, Wp,
                                          c->d_split[s], (int)binom(st.t - 1, st.a - 1), n, bufs.ptr(T[st.out]),
                                          c->ld_of(Wt), Wt, c->d_ztab[s], c->zblocks[s],
-                                         (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->num_sms,
-                                         c->s_main);
+                                         (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1, c->knobs,
+                                         c->num_sms, c->s_main);
       c->check_launch();
       c->end(PH_COMBINE, c->s_main, b);
       c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;
@@ -919,11 +940,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     if (n) CUDA_OK(cudaMemcpyAsync(root_out->data(), per_vertex, (size_t)n * 8, cudaMemcpyDeviceToHost, c->s_main));
   }
   for (auto &b : bufs.pool)
-    if (b.p && b.owned && b.refs > 0) c->afree(b.p, b.bytes, c->s_main);
-  if (per_vertex) {
-    void *pv = per_vertex;
-    c->afree(pv, (size_t)std::max<int64_t>(n, 1) * 8, c->s_main);
-  }
+    if (b.p && b.owned) c->afree(b.p, b.bytes, c->s_main);
   CUDA_OK(cudaStreamSynchronize(c->s_main));
   if (c->pworld() > 1) CUDA_OK(cudaStreamSynchronize(c->s_comm));
   float ms = 0;

@@ -35,11 +35,6 @@ namespace dev {
 
 namespace {
 
-int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
 // ------------------------------------------------------------------ colour sort
 // One warp per item.  Pass 1 counts colours; pass 2 places each neighbour at
 // base[colour] + (rank among equal colours in this 32-wide window): stable.
@@ -925,16 +920,14 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
 }
 
 template <typename T, int G, int NV, int U>
-void rows_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+void rows_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
   // 3 CTAs of 8 warps per SM (<= 85 registers, no spills): configs[2] -4%,
-  // configs[3] -1 to -2% against 2 CTAs
-  const int minb = env_int("CC_ROWS_MINB", 3);
+  // configs[3] -1 to -2% against 2 CTAs (profiles/r1/SUMMARY.md)
   // fp32 tables: fp32 shared-memory rows as in the lean gather (C-6)
-  const bool acc32 = sizeof(T) == 4 && env_int("CC_ACC32", 1);
-  auto kern = acc32 ? (minb == 2 ? k_gather_rows<T, G, NV, U, 2, float> : k_gather_rows<T, G, NV, U, 3, float>)
-                    : (minb == 2 ? k_gather_rows<T, G, NV, U, 2, double> : k_gather_rows<T, G, NV, U, 3, double>);
+  const bool acc32 = sizeof(T) == 4 && kn.acc32;
+  auto kern = acc32 ? k_gather_rows<T, G, NV, U, 3, float> : k_gather_rows<T, G, NV, U, 3, double>;
   const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
@@ -947,7 +940,7 @@ void rows_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
 }
 
 template <typename T, int NV, int U, int MINB = 2>
-void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+void ldg_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = 32 * NV * VW;
   // fp32 tables with N'' rows wider than 1600 entries (configs[4]'s root:
@@ -959,7 +952,7 @@ void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
   // need it to fit 16 warps per SM.  Each entry adds at most ceil(s/32) +
   // k - 1 fp32 block sums (C-6); CC_ACC32=0 keeps fp64 rows where
   // they fit.
-  const bool acc32 = sizeof(T) == 4 && (a.W_out > 1600 || (env_int("CC_ACC32", 1) && !a.root_mode));
+  const bool acc32 = sizeof(T) == 4 && (a.W_out > 1600 || (kn.acc32 && !a.root_mode));
   auto kern = acc32 ? k_gather_ldg<T, NV, U, float, MINB> : k_gather_ldg<T, NV, U, double, MINB>;
   const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
@@ -974,7 +967,7 @@ void ldg_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
 
 // ------------------------------------------------------------------ launchers
 template <typename T, int G, int NV, int D, int MINB = 1>
-void ring_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
+void ring_go(const GatherArgs &a, const Knobs &, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
   auto kern = k_gather_ring<T, G, NV, D, MINB>;
@@ -990,84 +983,52 @@ void ring_go(const GatherArgs &a, int num_sms, cudaStream_t s) {
 }
 
 template <typename T>
-int gather_typed(const GatherArgs &a, int num_sms, cudaStream_t s) {  // returns the launches
+int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {  // returns the launches
   constexpr int VW = Vec<T>::W;
   const int wvec = (a.W_in + VW - 1) / VW;
-  const char *impl = getenv("CC_GATHER_IMPL");  // "ring" / "ldg" for every width; default: by width
-  // default: rows of <= 8 vectors (a few lanes per row) go to the cp.async
-  // ring with sub-warp groups; wider rows to the lean kernel (measured,
-  // profiles/r1/SUMMARY.md).  The fused root exists in the lean kernel only.
-  const bool lean = impl ? impl[0] == 'l' : wvec > 16;
+  // default: rows of <= 16 vectors go to the narrow kernels, wider rows to
+  // the lean kernel (measured, profiles/r1/SUMMARY.md).  The fused root
+  // exists in the lean kernel only.
+  const bool lean = kn.gather_impl ? kn.gather_impl == 2 : wvec > 16;
   if (lean || a.root_mode) {
-    const int lv = env_int("CC_LDG_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
-    if (wvec <= 32) {
-      if (lv == 1) ldg_go<T, 1, 4>(a, num_sms, s);
-      else ldg_go<T, 1, 8>(a, num_sms, s);
-    } else if (wvec <= 64) {
-      if (lv == 1) ldg_go<T, 2, 4>(a, num_sms, s);
-      else ldg_go<T, 2, 8>(a, num_sms, s);
-    } else if (wvec <= 96) {
-      if (lv == 1) ldg_go<T, 3, 2>(a, num_sms, s);
-      else ldg_go<T, 3, 4>(a, num_sms, s);
-    } else {
-      if (lv == 1) ldg_go<T, 4, 4>(a, num_sms, s);
-      else ldg_go<T, 4, 2>(a, num_sms, s);
-    }
+    if (wvec <= 32) ldg_go<T, 1, 8>(a, kn, num_sms, s);
+    else if (wvec <= 64) ldg_go<T, 2, 8>(a, kn, num_sms, s);
+    else if (wvec <= 96) ldg_go<T, 3, 4>(a, kn, num_sms, s);
+    else ldg_go<T, 4, 2>(a, kn, num_sms, s);
     return 1;
   }
-  // narrow rows: 4 (default) = long lists on k_gather_rows, the rest on
-  // k_gather_ring; 0 = rings only; 1-3 = k_gather_rows only (tuning)
-  const int nr = env_int("CC_NARROW_IMPL", 4);
-  if (nr == 4 && wvec <= 16 && a.item_to < 0) {
-    // long lists (items before a.item_split) on warp-per-item row-parallel
-    // loads, the short tail on sub-warp rings
+  // narrow rows: long lists (items before a.item_split) on warp-per-item
+  // row-parallel loads, the short tail on sub-warp rings
+  if (kn.narrow_impl == 4 && wvec <= 16 && a.item_to < 0) {
     GatherArgs h = a, t = a;
     h.item_to = a.item_split;
     t.item_from = a.item_split;
     t.item_to = a.work.n_seg + a.work.n_light;
     int launches = 0;
     if (h.item_to > 0) {
-      if (wvec <= 4) rows_go<T, 4, 1, 4>(h, num_sms, s);
-      else if (wvec <= 8) rows_go<T, 8, 1, 4>(h, num_sms, s);
-      else rows_go<T, 8, 2, 4>(h, num_sms, s);
+      if (wvec <= 4) rows_go<T, 4, 1, 4>(h, kn, num_sms, s);
+      else if (wvec <= 8) rows_go<T, 8, 1, 4>(h, kn, num_sms, s);
+      else rows_go<T, 8, 2, 4>(h, kn, num_sms, s);
       ++launches;
     }
-    if (t.item_from < t.item_to) launches += gather_typed<T>(t, num_sms, s);
+    if (t.item_from < t.item_to) launches += gather_typed<T>(t, kn, num_sms, s);
     return launches;
   }
-  if (nr >= 1 && nr <= 3 && wvec <= 16) {
-    if (wvec <= 4) {
-      if (nr == 2) rows_go<T, 4, 1, 2>(a, num_sms, s);
-      else rows_go<T, 4, 1, 4>(a, num_sms, s);
-    } else if (wvec <= 8) {
-      if (nr == 2) rows_go<T, 8, 1, 2>(a, num_sms, s);
-      else rows_go<T, 8, 1, 4>(a, num_sms, s);
-    } else {
-      if (nr == 2) rows_go<T, 8, 2, 2>(a, num_sms, s);
-      else if (nr == 3) rows_go<T, 16, 1, 4>(a, num_sms, s);
-      else rows_go<T, 8, 2, 4>(a, num_sms, s);
-    }
+  if (kn.narrow_impl >= 1 && kn.narrow_impl <= 3 && wvec <= 16) {
+    if (wvec <= 4) rows_go<T, 4, 1, 4>(a, kn, num_sms, s);
+    else if (wvec <= 8) rows_go<T, 8, 1, 4>(a, kn, num_sms, s);
+    else rows_go<T, 8, 2, 4>(a, kn, num_sms, s);
     return 1;
   }
-  const int vr = env_int("CC_RING_VARIANT", 0);  // tuning knob (scripts/agg_sweep.py)
   // narrow rows: small rings (more resident groups) measured faster
   // (p = 2: D 16 -> 4: 12.3 -> 9.0 ms; p = 3: G 16 x 1 -> 8 x 2 vectors,
   // D 4: 31.5 -> 19.8 ms, the lean kernel 27.8 ms)
-  if (wvec <= 4) {
-    if (vr == 2) ring_go<T, 4, 1, 3, 2>(a, num_sms, s);
-    else if (vr == 4) ring_go<T, 4, 1, 4, 2>(a, num_sms, s);
-    else ring_go<T, 4, 1, 4, 3>(a, num_sms, s);  // 3 CTAs/SM: configs[2] -1.5%
-  } else if (wvec <= 8) ring_go<T, 8, 1, 4, 2>(a, num_sms, s);
-  else if (wvec <= 16) {
-    if (vr == 2) ring_go<T, 8, 2, 3, 2>(a, num_sms, s);
-    else if (vr == 3) ring_go<T, 16, 1, 4, 2>(a, num_sms, s);
-    else if (vr == 4) ring_go<T, 8, 2, 4, 2>(a, num_sms, s);
-    else ring_go<T, 8, 2, 4, 3>(a, num_sms, s);
-  }
-  else if (wvec <= 32) ring_go<T, 32, 1, 16, 2>(a, num_sms, s);
-  else if (wvec <= 64) ring_go<T, 32, 2, 8, 2>(a, num_sms, s);
-  else if (vr == 1) ring_go<T, 32, 4, 5, 2>(a, num_sms, s);
-  else ring_go<T, 32, 4, 4, 2>(a, num_sms, s);
+  if (wvec <= 4) ring_go<T, 4, 1, 4, 3>(a, kn, num_sms, s);  // 3 CTAs/SM: configs[2] -1.5%
+  else if (wvec <= 8) ring_go<T, 8, 1, 4, 2>(a, kn, num_sms, s);
+  else if (wvec <= 16) ring_go<T, 8, 2, 4, 3>(a, kn, num_sms, s);
+  else if (wvec <= 32) ring_go<T, 32, 1, 16, 2>(a, kn, num_sms, s);
+  else if (wvec <= 64) ring_go<T, 32, 2, 8, 2>(a, kn, num_sms, s);
+  else ring_go<T, 32, 4, 4, 2>(a, kn, num_sms, s);
   return 1;
 }
 
@@ -1077,48 +1038,44 @@ int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, con
                  const AggWork &work, int32_t *col_out, uint16_t *goff, ItemDesc *desc, int num_sms,
                  cudaStream_t s) {
   if (work.n_seg + work.n_light == 0) return 0;
-  static int grid = 0;
-  if (!grid) grid = persistent_grid(k_csort, 256, 0, num_sms);
+  const int grid = persistent_grid(k_csort, 256, 0, num_sms);
   k_csort<<<grid, 256, 0, s>>>(beg, end, col, colors, work, col_out, goff, desc);
   return 1;
 }
 
 int launch_csort_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                       const AggWork &work, int k, int32_t *col_out, uint16_t *goff, ItemDesc *desc, void *hist,
-                      int64_t ldh, int64_t hist_rows, int64_t small_from, int num_sms, cudaStream_t s) {
+                      int64_t ldh, int64_t hist_rows, int64_t small_from, const Knobs &kn, int num_sms,
+                      cudaStream_t s) {
   const int64_t n_items = work.n_seg + work.n_light;
   if (n_items == 0) return 0;
   int launches = 1;
   // the items before small_from: one warp each (k_csort2 walks n_items on its
   // own work view, so it gets a view truncated to small_from)
   AggWork head = work;
-  const bool split = getenv("CC_CSORT_SMALL") == nullptr || getenv("CC_CSORT_SMALL")[0] != '0';
+  const bool split = kn.csort_small != 0;
   if (split && small_from < n_items) head.n_light = small_from - work.n_seg;
   if (hist && work.n_seg) {  // heavy rows accumulate segment counts atomically
     cudaMemsetAsync(hist, 0, (size_t)hist_rows * ldh * elem, s);
     ++launches;
   }
   if (elem == 8) {
-    static int grid = 0;
-    if (!grid) grid = persistent_grid(k_csort2<double>, 256, 0, num_sms);
+    const int grid = persistent_grid(k_csort2<double>, 256, 0, num_sms);
     k_csort2<double><<<grid, 256, 0, s>>>(beg, end, col, colors, head, k, col_out, goff, desc,
                                           static_cast<double *>(hist), ldh);
   } else {
-    static int grid = 0;
-    if (!grid) grid = persistent_grid(k_csort2<float>, 256, 0, num_sms);
+    const int grid = persistent_grid(k_csort2<float>, 256, 0, num_sms);
     k_csort2<float><<<grid, 256, 0, s>>>(beg, end, col, colors, head, k, col_out, goff, desc,
                                          static_cast<float *>(hist), ldh);
   }
   if (split && small_from < n_items) {
     ++launches;
     if (elem == 8) {
-      static int grid = 0;
-      if (!grid) grid = persistent_grid(k_csort_small<double>, 256, 0, num_sms);
+      const int grid = persistent_grid(k_csort_small<double>, 256, 0, num_sms);
       k_csort_small<double><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, small_from, col_out, goff, desc,
                                                  static_cast<double *>(hist), ldh);
     } else {
-      static int grid = 0;
-      if (!grid) grid = persistent_grid(k_csort_small<float>, 256, 0, num_sms);
+      const int grid = persistent_grid(k_csort_small<float>, 256, 0, num_sms);
       k_csort_small<float><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, small_from, col_out, goff, desc,
                                                 static_cast<float *>(hist), ldh);
     }
@@ -1135,20 +1092,18 @@ int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t 
     ++launches;
   }
   if (elem == 8) {
-    static int grid = 0;
-    if (!grid) grid = persistent_grid(k_hist<double, 8>, 256, 0, num_sms);
+    const int grid = persistent_grid(k_hist<double, 8>, 256, 0, num_sms);
     k_hist<double, 8><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, static_cast<double *>(out), ld);
   } else {
-    static int grid = 0;
-    if (!grid) grid = persistent_grid(k_hist<float, 8>, 256, 0, num_sms);
+    const int grid = persistent_grid(k_hist<float, 8>, 256, 0, num_sms);
     k_hist<float, 8><<<grid, 256, 0, s>>>(beg, end, col, colors, work, k, static_cast<float *>(out), ld);
   }
   return launches;
 }
 
-int launch_gather(int elem, const GatherArgs &a, int num_sms, cudaStream_t s) {
+int launch_gather(int elem, const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   if (a.work.n_seg + a.work.n_light == 0) return 0;
-  return elem == 8 ? gather_typed<double>(a, num_sms, s) : gather_typed<float>(a, num_sms, s);
+  return elem == 8 ? gather_typed<double>(a, kn, num_sms, s) : gather_typed<float>(a, kn, num_sms, s);
 }
 
 }  // namespace dev

@@ -30,11 +30,6 @@ namespace dev {
 
 namespace {
 
-int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
 // ------------------------------------------------------------------ colour
 __global__ void k_color(const int32_t *__restrict__ orig, int64_t n, uint64_t seed, int k,
                         uint8_t *__restrict__ out) {
@@ -550,19 +545,17 @@ void combine_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, 
 
 template <typename T>
 int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
-                   int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
-  const char *impl = getenv("CC_COMBINE_IMPL");  // "tile": V-tile kernel; default: lane-per-vertex
+                   int nq, int64_t n, void *out, int64_t ldO, int WO, const Knobs &kn, int num_sms, cudaStream_t s) {
   const size_t split_bytes = (size_t)nq * ((WO + 7) & ~7) * 4;
   const size_t cap = 227 * 1024;
   // V = 2 vertices per lane (one address per 2 FMAs, single-buffered
   // 64-vertex tiles) when that tile plus the whole split table fits; else
   // V = 1 double-buffered with the whole table; else V = 1 single-buffered
   // with the outputs in chunks whose table slices fit (configs[4]'s (7;4,3)).
-  const int vpref = env_int("CC_COMBINE_V", 2);
   const size_t tile2 = ((size_t)(WA + WN) * 33 * 2 * sizeof(T) + 15) / 16 * 16;
   const size_t tile1 = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
   int V = 1, nbuf = 1, chunk = WO;
-  if (vpref == 2 && tile2 + split_bytes <= cap) V = 2;
+  if (tile2 + split_bytes <= cap) V = 2;
   else if (2 * tile1 + split_bytes <= cap) nbuf = 2;
   else if (tile1 + (size_t)nq * 4 * 64 <= cap) chunk = (int)((cap - tile1) / ((size_t)nq * 4) / 8 * 8);
   else chunk = 0;  // even 64 outputs do not fit: V-tile kernel
@@ -572,7 +565,7 @@ int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN
   // config 3 at 11.7 FMA/entry wins, config 2's (7;4,3) at 6.7 and (4;3,1)
   // at 2.1 lose)
   const double intensity = (double)WO * nq / (double)(WA + WN + WO);
-  const bool lane_ok = (impl && impl[0] != 'z') ? impl[0] != 't' : intensity >= 8.0;
+  const bool lane_ok = kn.combine_impl >= 2 ? kn.combine_impl == 2 : intensity >= 8.0;
   if (lane_ok && chunk > 0) {
     const int WOcp = (std::min(chunk, WO) + 7) & ~7;
     const size_t smem = nbuf * tile_bytes + (size_t)nq * WOcp * 4;
@@ -640,10 +633,8 @@ int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
   // two single-buffered CTAs of 8 warps per SM when they fit (one computes
   // while the other stages or waits at its barrier; measured 5% faster on
   // config 3), else one CTA of 16 warps, double-buffered when it fits
-  // (CC_Z_CTAS=1 forces the latter)
-  const int ctas = env_int("CC_Z_CTAS", 2);
   int nbuf = 2 * tile + zbytes <= cap ? 2 : 1, threads = 512;
-  if (ctas == 2 && 2 * (tile + zbytes) <= cap) {
+  if (2 * (tile + zbytes) <= cap) {
     nbuf = 1;
     threads = 256;
   }
@@ -659,10 +650,9 @@ int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
 
 int launch_combine_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
                         const uint16_t *ztab, int nblocks, int zld, int ts, int as, const uint16_t *comp, int64_t n,
-                        double *per_vertex, int num_sms, cudaStream_t s) {
+                        double *per_vertex, const Knobs &kn, int num_sms, cudaStream_t s) {
   if (n == 0 || !ztab || !comp || !per_vertex) return 0;
-  const char *impl = getenv("CC_COMBINE_IMPL");
-  if (impl && impl[0] != 'z') return 0;
+  if (kn.combine_impl >= 2) return 0;
   if (elem == 4 && ts == 8 && as == 5)
     return z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
   if (elem == 4 && ts == 6 && as == 3)
@@ -674,18 +664,17 @@ int launch_combine_root(int elem, const void *A, int64_t ldA, int WA, const void
 
 int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
-                   int nblocks, int zld, int ts, int as, int num_sms, cudaStream_t s) {
+                   int nblocks, int zld, int ts, int as, const Knobs &kn, int num_sms, cudaStream_t s) {
   if (n == 0) return 0;
-  const char *impl = getenv("CC_COMBINE_IMPL");  // "z" / "lane" / "tile"; default: z when available
-  if (ztab && (!impl || impl[0] == 'z')) {
+  if (ztab && kn.combine_impl <= 1) {  // the Z-block kernel when the shape has one
     int l = 0;
     if (elem == 4 && ts == 8 && as == 5) l = z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     else if (elem == 4 && ts == 6 && as == 3) l = z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     if (l) return l;
   }
-  if (elem == 8) return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  return combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+  if (elem == 8) return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, kn, num_sms, s);
+  return combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, kn, num_sms, s);
 }
 
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, const uint16_t *comp,

@@ -16,6 +16,26 @@
 namespace cc {
 namespace dev {
 
+// Implementation switches of the launchers (A/B knobs, not results: every
+// setting computes the same values).  Read ONCE from the environment at
+// cc_create (CC_<NAME>) and changeable per context with
+// cc_set_knob; the defaults are the measured choices.
+struct Knobs {
+  int fused_root = 1;      // CC_FUSED_ROOT: 0 = never evaluate the root in an epilogue
+  int sector_skip = 1;     // CC_SECTOR_SKIP: 0 = read every sector of a neighbour's row
+  int gather_impl = 0;     // CC_GATHER_IMPL: 0 = by row width, 1 = rings only, 2 = lean only
+  int narrow_impl = 4;     // CC_NARROW_IMPL: 4 = long lists row-parallel + short tail on rings, 0 = rings only,
+                           //                 1 = row-parallel only
+  int narrow_split = -1;   // CC_NARROW_SPLIT: log2(T/8), items with > T neighbours row-parallel; -1 = auto
+  int csort_small = 1;     // CC_CSORT_SMALL: 0 = no separate kernel for the <= 8-neighbour items
+  int combine_impl = 0;    // CC_COMBINE_IMPL: 0 = auto, 1 = Z-block, 2 = lane, 3 = V-tile
+  int acc32 = 1;           // CC_ACC32: fp32 tables keep the shared-memory N'' rows in fp32 (scaled)
+  int phase_events = 1;    // CC_PHASE_EVENTS: per-kernel events for cc_last_profile
+  int hub_l2_pct = 50;     // CC_HUB_L2_PCT: % of the L2 given an evict-last policy for hub rows (rings)
+  int grid_reserve = -1;   // CC_GRID_RESERVE: SMs left free for NCCL while an exchange is in flight
+                           //                  (-1 = auto: 8 when world > 1 over NCCL, else 0)
+};
+
 // Work list of one aggregation pass (Alg. 4: the
 // neighbour list of a vertex is cut into tasks of at most s neighbours).
 //   light[i]       vertices whose [beg, end) range has <= s neighbours
@@ -97,17 +117,18 @@ int launch_csort(const int64_t *beg, const int64_t *end, const int32_t *col, con
 // N''(v, {y}) into hist (rows x ldh, k-1 columns) unless hist is null.
 int launch_csort_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                       const AggWork &work, int k, int32_t *col_out, uint16_t *goff, ItemDesc *desc, void *hist,
-                      int64_t ldh, int64_t hist_rows, int64_t small_from, int num_sms, cudaStream_t s);
+                      int64_t ldh, int64_t hist_rows, int64_t small_from, const Knobs &kn, int num_sms,
+                      cudaStream_t s);
 // N''(v, {y}) = #{u in N(v) : sq_{c_v}(col u) = y}, k-1 columns.
 int launch_hist(int elem, const int64_t *beg, const int64_t *end, const int32_t *col, const uint8_t *colors,
                 const AggWork &work, int64_t n, int k, void *out, int64_t ld, int num_sms, cudaStream_t s);
 // The neighbour sum of a passive table of size p >= 2 (compressed).
-int launch_gather(int elem, const GatherArgs &a, int num_sms, cudaStream_t s);
+int launch_gather(int elem, const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s);
 // Combine step; ztab (nullable) = its Z-block cover (zblock_table, nblocks
 // blocks of zld entries) for the register-blocked kernel when combine_z_supported.
 int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
-                   int nblocks, int zld, int ts, int as, int num_sms, cudaStream_t s);
+                   int nblocks, int zld, int ts, int as, const Knobs &kn, int num_sms, cudaStream_t s);
 bool combine_z_supported(int elem, int ts, int as);
 // The last combine fused with the root step that shares its passive table:
 // X_v = sum_{X'} T'(v, X') N''(v, comp X') into per_vertex[v] (fp64), T'
@@ -116,7 +137,7 @@ bool combine_z_supported(int elem, int ts, int as);
 // combine and launch_root.
 int launch_combine_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
                         const uint16_t *ztab, int nblocks, int zld, int ts, int as, const uint16_t *comp, int64_t n,
-                        double *per_vertex, int num_sms, cudaStream_t s);
+                        double *per_vertex, const Knobs &kn, int num_sms, cudaStream_t s);
 // Root step + deterministic reduction into result[0] (double).  A == nullptr
 // means a single-vertex active part: sum_v N''(v, [k-1]) (one column).
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN,

@@ -1,7 +1,8 @@
 """Tuning sweep (GPU): per-phase device ms of one colouring for each kernel
-variant (environment knobs) / segment length.  Not a bench.
+variant (implementation knobs, cc_set_knob) / segment length.
+Not a bench.
 
-  --envs "CC_GATHER_IMPL=reg;CC_RING_VARIANT=0,1,2"
+  --knobs "gather_impl=0,2;narrow_impl=0,4"
 expands to the cartesian product of the listed values."""
 import argparse
 import itertools
@@ -17,7 +18,7 @@ import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
-ap.add_argument("--envs", default="CC_RING_VARIANT=0")
+ap.add_argument("--knobs", default="fused_root=1")
 ap.add_argument("--segs", default="4096")
 ap.add_argument("--precision", default=None)
 ap.add_argument("--reps", type=int, default=2)
@@ -26,7 +27,7 @@ ap.add_argument("--fixed-root", default="0")
 args = ap.parse_args()
 
 knobs = []
-for part in args.envs.split(";"):
+for part in args.knobs.split(";"):
     name, vals = part.split("=")
     knobs.append([(name, v) for v in vals.split(",")])
 combos = list(itertools.product(*knobs))
@@ -46,7 +47,7 @@ for seg, fr in itertools.product(map(int, args.segs.split(",")), map(int, args.f
     ref = None
     for combo in combos:
         for name, val in combo:
-            os.environ[name] = val
+            cc.cc_set_knob(ctx, name, int(val))
         cc.cc_color(ctx, 2)
         cc.cc_count_colorful(ctx)  # warm
         best = None
@@ -60,7 +61,7 @@ for seg, fr in itertools.product(map(int, args.segs.split(",")), map(int, args.f
         st = cc.cc_last_stats(ctx)
         if ref is None:
             ref = xs
-        rec = {"env": dict(combo), "seg": seg, "fixed_root": fr, "load_s": round(load_s, 1),
+        rec = {"knobs": dict(combo), "seg": seg, "fixed_root": fr, "load_s": round(load_s, 1),
                "gather_GBs": round(st["agg_bytes"] / best["gather"] / 1e6, 1),
                "same_as_first": xs == ref,
                **{k: round(v, 3) for k, v in best.items()}}

@@ -174,3 +174,26 @@ def test_nccl_calls_on_one_rank():
     values with the same grouped ncclSend/ncclRecv and ncclAllReduce calls
     (and argument types) the halo exchange and the final reduction use."""
     lib().cc_nccl_selftest(0)
+
+
+def test_ranks_plan_from_the_global_degree():
+    """Every rank must run the SAME plan (the exchanges of different plans do
+    not match).  The planner's root depends on the average degree; this
+    template's choice switches inside the spread of the per-rank averages of
+    an 8-way split of R-MAT scale 13, so a per-rank statistic
+    would diverge.  With the global statistic the 8 ranks agree with the
+    single-rank count and the oracle."""
+    cc = lib()
+    parent = [-1, 0, 0, 2, 0, 0, 1, 3, 6, 6, 0, 5]
+    roots = {cc.cc_plan_template_auto(parent, d, 8)["root"] for d in (28.0, 32.0, 36.0, 40.0)}
+    assert len(roots) > 1, "the template's plan must switch inside the per-rank degree spread"
+    g = synth.rmat(13, 16, seed=5)
+    k = len(parent)
+    col = oracle.color(g.n, k, 17)
+    want = oracle.dp_count(g, parent, col, oracle.NUM_LONGDOUBLE).total
+    one = count(g, parent, colors=col)
+    assert rel_err(one, want) <= 1e-12
+    for world in (4, 8):
+        got, _ = run_ranks(g, parent, world, colors=col)
+        assert all(x == got[0] for x in got)
+        assert rel_err(got[0], want) <= 1e-12, (world, got[0], want)

@@ -199,7 +199,7 @@ FUSED_CASES = [
 
 
 @pytest.mark.parametrize("parent,mode", FUSED_CASES)
-def test_fused_root_exact(parent, mode, monkeypatch):
+def test_fused_root_exact(parent, mode):
     cc = lib()
     k = len(parent)
     graphs = [synth.gnp(60, 0.25, 11), synth.scaled_twin(synth.CONFIGS[3], 10, 16).graph()]
@@ -212,10 +212,10 @@ def test_fused_root_exact(parent, mode, monkeypatch):
                 x = cc.cc_count_colorful(ctx)
                 assert cc.cc_last_stats(ctx)["fused_root"] == mode
                 root = cc.cc_get_subtree_counts(ctx, parent.index(-1), g.n, k, k)
-                monkeypatch.setenv("CC_FUSED_ROOT", "0")
+                cc.cc_set_knob(ctx, "fused_root", 0)
                 x_unfused = cc.cc_count_colorful(ctx)
                 assert cc.cc_last_stats(ctx)["fused_root"] == 0
-                monkeypatch.delenv("CC_FUSED_ROOT")
+                cc.cc_set_knob(ctx, "fused_root", 1)
             # exact while every partial sum stays below 2^53; the 15-vertex tree's
             # root products do not, so the bar there is the fp64 1e-12
             assert rel_err(x, float(want.total)) <= TOL_FP64, (parent, gi, seg)
@@ -227,7 +227,7 @@ def test_fused_root_exact(parent, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("ci", [2, 3])
-def test_fused_combine_root(ci, monkeypatch):
+def test_fused_combine_root(ci):
     """Fused combine + root (fused_root mode 3): configs[2]'s and [3]'s root
     step takes its active table from a register-blocked combine over the
     same passive neighbour sum, so X_v is formed in that combine's epilogue
@@ -249,10 +249,10 @@ def test_fused_combine_root(ci, monkeypatch):
                     x = cc.cc_count_colorful(ctx)
                     assert cc.cc_last_stats(ctx)["fused_root"] == 3, (ci, prec)
                     root = cc.cc_get_subtree_counts(ctx, parent.index(-1), g.n, k, k)
-                    monkeypatch.setenv("CC_FUSED_ROOT", "0")
+                    cc.cc_set_knob(ctx, "fused_root", 0)
                     x_unfused = cc.cc_count_colorful(ctx)
                     assert cc.cc_last_stats(ctx)["fused_root"] == 0
-                    monkeypatch.delenv("CC_FUSED_ROOT")
+                    cc.cc_set_knob(ctx, "fused_root", 1)
                 assert rel_err(x, float(want.total)) <= tol, (ci, gi, prec, seg)
                 assert rel_err(x_unfused, x) <= tol
                 assert_close_entries(root, want.root.reshape(-1, 1), tol, f"fused combine root X_v config {ci}")
@@ -564,4 +564,64 @@ def test_options_and_hooks_are_validated():
         assert prof["gather"] > 0 and prof["csort"] > 0
         with pytest.raises(cc.CCError) as e:
             cc.cc_set_colors(ctx, np.full(g.n, 7, np.uint8))  # colour out of range
+        assert e.value.status == cc.CC_ERR_ARG
+
+
+def test_fp32_overflow_is_reported_nonfinite():
+    """Reading C-13: fp32 tables that overflow make the count non-finite and
+    cc_count_colorful returns CC_ERR_NONFINITE.  A 16-vertex star on the
+    clique K_2000 with 16 colours: the active table of the 15-vertex partial
+    star holds 14! prod cnt_j ~ 2e40 > FLT_MAX; in fp64 the count is the
+    clique closed form X = k! prod_j cnt_j (SURVEY 8(c) pins)."""
+    cc = lib()
+    n, k = 2000, 16
+    g = synth.clique(n)
+    parent = [-1] + [0] * (k - 1)
+    col = oracle.color(n, k, 3)
+    cnt = np.bincount(col, minlength=k).astype(np.float64)
+    want = math.factorial(k) * float(np.prod(cnt))
+    assert rel_err(count(g, parent, colors=col, precision="fp64"), want) <= TOL_FP64
+    with context(g, parent, "fp32") as ctx:
+        cc.cc_set_colors(ctx, col)
+        with pytest.raises(cc.CCError) as e:
+            cc.cc_count_colorful(ctx)
+        assert e.value.status == cc.CC_ERR_NONFINITE
+        # not poisoned: the context still counts (fp32 overflow is not a CUDA error)
+        cc.cc_set_colors(ctx, np.zeros(n, np.uint8))
+        assert cc.cc_count_colorful(ctx) == 0.0
+
+
+KNOB_SETTINGS = [("gather_impl", 1), ("gather_impl", 2), ("narrow_impl", 0), ("narrow_impl", 1),
+                 ("narrow_split", 0), ("narrow_split", 7), ("csort_small", 0), ("sector_skip", 0),
+                 ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("acc32", 0),
+                 ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32)]
+
+
+@pytest.mark.parametrize("ci", [2, 3, 4])
+def test_every_knob_setting_computes_the_same_count(ci):
+    """The implementation knobs select kernels, never results:
+    fp64 counts equal the oracle within 1e-12 under every setting (exactly
+    equal to the default when the integer counts stay below 2^53), fp32
+    within 1e-4."""
+    cc = lib()
+    cfg = synth.scaled_twin(synth.CONFIGS[ci], 11, 16)
+    g = cfg.graph()
+    col = oracle.color(g.n, cfg.k, 23)
+    want = float(oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE).total)
+    for prec, tol in (("fp64", TOL_FP64), ("fp32", TOL_FP32)):
+        with context(g, cfg.parent, prec, segment_len=64) as ctx:
+            cc.cc_set_colors(ctx, col)
+            base = cc.cc_count_colorful(ctx)
+            assert rel_err(base, want) <= tol
+            for name, value in KNOB_SETTINGS:
+                old = cc.cc_get_knob(ctx, name)
+                cc.cc_set_knob(ctx, name, value)
+                x = cc.cc_count_colorful(ctx)
+                cc.cc_set_knob(ctx, name, old)
+                assert rel_err(x, want) <= tol, (ci, prec, name, value, x, want)
+                if prec == "fp64" and want < 2.0 ** 53:
+                    assert x == base, (ci, name, value)
+        with pytest.raises(cc.CCError) as e:
+            with context(g, cfg.parent) as ctx:
+                cc.cc_set_knob(ctx, "no_such_knob", 1)
         assert e.value.status == cc.CC_ERR_ARG

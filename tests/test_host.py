@@ -270,3 +270,59 @@ def test_create_without_a_gpu_is_an_error(cc):
     with pytest.raises(cc.CCError) as e:
         cc.cc_create(device=0)
     assert e.value.status == cc.CC_ERR_CUDA
+
+
+def test_bench_updates_match_the_library_plan(cc):
+    """bench.py's U (pure Python, so that the oracle arm never loads the
+    product) equals the distinct-passive count of the library's own
+    fixed-root plan, for the five configs and random trees."""
+    import bench
+    rng = np.random.default_rng(3)
+    parents = [c.parent for c in synth.CONFIGS]
+    for _ in range(40):
+        k = int(rng.integers(2, 13))
+        parents.append([-1] + [int(rng.integers(0, i)) for i in range(1, k)])
+    for parent in parents:
+        k = len(parent)
+        plan = cc.cc_plan_template(parent)
+        seen, u = set(), 0
+        for s in plan["steps"]:
+            key = s["passive"] if s["p"] > 1 else "leaf"
+            if key not in seen:
+                seen.add(key)
+                u += math.comb(k, s["p"])
+        assert bench.updates_per_entry(parent) == u, parent
+
+
+def test_reference_arm_does_not_load_the_product():
+    import subprocess
+    import sys
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', '0', '--steps', '1', "
+            "'--warmup', '1']; runpy.run_path('bench.py', run_name='__main__'); "
+            "assert 'paper_1804_09764_b200' not in sys.modules; "
+            "maps = open('/proc/self/maps').read(); assert 'libcc.so' not in maps, 'libcc.so mapped'")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert '"impl": "reference"' in r.stdout
+
+
+def test_bench_self_launches_n_ranks():
+    """`bench.py --gpus 2` with no torchrun environment starts 2 ranks itself
+    (torch.distributed.run on 127.0.0.1); the reference arm needs no GPU, so
+    the launch is checked here: rank 0 alone prints the line, n_gpus = 2.  Our
+    arm refuses to run when fewer GPUs than --gpus are visible."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--config", "0",
+                        "--steps", "1", "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "0", "--steps", "1", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    import torch
+    if torch.cuda.device_count() < 2:
+        assert r.returncode == 2 and "CUDA device" in r.stderr
