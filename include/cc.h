@@ -95,12 +95,20 @@ typedef struct {
   const void *nccl_id;   /* 128-byte ncclUniqueId when world > 1 (from rank 0's
                             cc_nccl_unique_id, broadcast by the caller); ignored
                             when world == 1 */
-  int64_t chunk_cols;    /* reserved, must be 0: column chunking is internal --
-                            the gathers walk rows in passes of 32 x NV x VW
-                            columns, the combine stages split-table slices, and
-                            the fused root keeps the widest neighbour sum out
-                            of HBM ("intermediate
-                            data partitioning"); CC_ERR_ARG otherwise */
+  int64_t chunk_cols;    /* column chunks ("intermediate data
+                            partitioning", lines 391-396 / 420-428 PeakMem): 0 =
+                            none; > 0 = every neighbour sum reads its passive
+                            table in launches of chunk_cols columns (rounded up
+                            to a multiple of 8), the later ones accumulating into
+                            N''; with world > 1 the halo rows are then exchanged
+                            per chunk into two chunk-wide buffers (chunk i + 1
+                            transfers while chunk i is summed) and tables keep
+                            only the owned rows.  Independently of this option
+                            the memory plan of every count runs the tail of the
+                            plan in row batches, recomputing the tail's passive
+                            table per batch in column chunks, when the tables
+                            would not fit the free device memory (one rank).
+                            < 0: CC_ERR_ARG */
   int32_t segment_len;   /* neighbour-list task size s: neighbour lists longer
                             than this are split into segments of at most s
                             neighbours (Alg. 4); 0 = auto */
@@ -295,7 +303,10 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * and device ms of the longest neighbour-sum pass, out[8] = number of
  * neighbour-sum passes (a narrow-row pass is one or two kernels), out[9] = halo bytes received by this rank (1D
  * partition), out[10] (cap >= 11) = the exchange schedule in use
- * (0: none -- one rank or replicas, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING).
+ * (0: none -- one rank or replicas, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING),
+ * out[11] (cap >= 12) = column-chunk launches of the chunked neighbour sums
+ * (0: none), out[12] = row batches of the memory plan's tail (0: none),
+ * out[13] = column width of the tail's recomputed passive table (0: none).
  * cap >= 5. */
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
 

@@ -88,13 +88,16 @@ int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
   if (name == "phase_events") return &k.phase_events;
   if (name == "hub_l2_pct") return &k.hub_l2_pct;
   if (name == "grid_reserve") return &k.grid_reserve;
+  if (name == "tail_batches") return &k.tail_batches;
+  if (name == "tail_recompute_cols") return &k.tail_recompute_cols;
   return nullptr;
 }
 
 // CC_<NAME> from the environment, read once per context
 void knobs_from_env(cc::dev::Knobs &k) {
   static const char *names[] = {"fused_root", "sector_skip", "gather_impl", "narrow_impl", "narrow_split",
-                                "csort_small", "combine_impl", "acc32", "phase_events", "hub_l2_pct", "grid_reserve"};
+                                "csort_small", "combine_impl", "acc32", "phase_events", "hub_l2_pct", "grid_reserve",
+                                "tail_batches", "tail_recompute_cols"};
   for (const char *n : names) {
     std::string env = "CC_";
     for (const char *q = n; *q; ++q) env += (char)std::toupper((unsigned char)*q);
@@ -183,12 +186,13 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   if (opt->precision != CC_FP64 && opt->precision != CC_FP32) return CC_ERR_ARG;
   if (opt->world < 1 || opt->world > 64 || opt->rank < 0 || opt->rank >= opt->world) return CC_ERR_ARG;
   if (opt->world > 1 && !opt->nccl_id && !opt->loopback) return CC_ERR_ARG;
-  if (opt->chunk_cols != 0 || opt->segment_len < 0 || opt->use_graphs < 0 || opt->use_graphs > 1) return CC_ERR_ARG;
+  if (opt->chunk_cols < 0 || opt->segment_len < 0 || opt->use_graphs < 0 || opt->use_graphs > 1) return CC_ERR_ARG;
   if (opt->replicas < 0 || opt->replicas > 1) return CC_ERR_ARG;
   if (opt->exchange < CC_EXCHANGE_AUTO || opt->exchange > CC_EXCHANGE_RING) return CC_ERR_ARG;
   std::unique_ptr<cc_ctx> c(new cc_ctx());
   c->opt = *opt;
   c->opt.nccl_id = nullptr;
+  c->chunk_cols = opt->chunk_cols;
   knobs_from_env(c->knobs);
   try {
     CUDA_OK(cudaSetDevice(opt->device));
@@ -567,7 +571,7 @@ cc_status cc_last_profile(cc_ctx *c, double *ms, int32_t cap, int32_t *n) {
 
 cc_status cc_last_stats(cc_ctx *c, double *out, int32_t cap) {
   if (!c || !out || cap < 5) return CC_ERR_ARG;
-  for (int i = 0; i < std::min<int32_t>(cap, 11); ++i) out[i] = c->stats[i];
+  for (int i = 0; i < std::min<int32_t>(cap, cc::kNStats); ++i) out[i] = c->stats[i];
   return CC_OK;
 }
 

@@ -30,6 +30,8 @@
 
 namespace cc {
 
+constexpr int kNStats = 14;  // cc_last_stats entries
+
 // Phases reported by cc_last_profile after "total": PROFILE order.
 enum Phase { PH_COLOR = 0, PH_CSORT, PH_HIST, PH_GATHER, PH_COMBINE, PH_ROOT, PH_EXCHANGE, PH_EXPOSED, PH_N };
 
@@ -43,6 +45,9 @@ struct Pass {
   int64_t split[8] = {0};      // split[i]: first item of the <= (8 << i)-neighbour tail
   int64_t seg_len = 0;         // segment length s of the heavy items
   int64_t nnz = 0;             // adjacency entries covered
+  std::vector<int64_t> pref;   // host: adjacency entries before item i (items() + 1 entries)
+  std::vector<int32_t> light_h;  // host copy of the light items' vertices (increasing)
+  int64_t max_heavy_v = -1;      // largest vertex with heavy segments
   const int64_t *beg = nullptr, *end = nullptr;  // device
   uint16_t *goff = nullptr;    // n_items x 16 colour-group ends (per colouring)
   dev::ItemDesc *desc = nullptr;  // n_items descriptors (per colouring)
@@ -114,6 +119,12 @@ struct cc_ctx {
   cc::Pass p_full, p_local, p_remote;  // world 1: p_full; world > 1: p_local + p_remote (+ p_full for hist)
   std::vector<cc::Pass> p_peer;        // ring exchange: the remote pass per source peer (replaces p_remote)
   int xmode = 0;                       // exchange schedule in use: 0 none, CC_EXCHANGE_GROUPED / _RING
+  // column chunks: chunk_cols > 0 splits every neighbour sum's
+  // passive columns into launches of that width; chunked (world > 1) then
+  // exchanges halo rows per chunk into double buffers and tables keep only
+  // the owned rows
+  int64_t chunk_cols = 0;
+  bool chunked = false;
   double xmodel[2] = {0, 0};           // modelled grouped / ring seconds (max over ranks)
   int64_t max_seg = 0, max_hv = 0;
   // adjacency entries per non-isolated vertex of the GLOBAL graph: the
@@ -146,7 +157,7 @@ struct cc_ctx {
 
   // profile / stats of the last count
   double prof[cc::PH_N + 1] = {0};
-  double stats[11] = {0};
+  double stats[cc::kNStats] = {0};
   std::vector<std::pair<size_t, double>> gather_log;  // (ev_log index, algorithmic bytes) per gather launch
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;
   std::vector<cudaEvent_t> ev_pool;

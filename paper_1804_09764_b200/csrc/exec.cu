@@ -68,6 +68,11 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
   }
   w.nnz = nnz;
   w.n_light = (int64_t)light.size();
+  // adjacency entries before each item (segments first, then light items)
+  w.pref.assign((size_t)(seg_v.size() + light.size() + 1), 0);
+  for (size_t i = 0; i < seg_v.size(); ++i) w.pref[i + 1] = w.pref[i] + (seg_e[i] - seg_b[i]);
+  for (size_t i = 0; i < light.size(); ++i)
+    w.pref[seg_v.size() + i + 1] = w.pref[seg_v.size() + i] + (end[light[i]] - beg[light[i]]);
   {  // light items are in internal (degree-descending) order: the <= 8-neighbour tail
     int64_t i = (int64_t)light.size();
     while (i > 0 && end[light[i - 1]] - beg[light[i - 1]] <= 8) --i;
@@ -80,6 +85,8 @@ void build_pass(cc_ctx *c, const std::vector<int64_t> &beg, const std::vector<in
   }
   w.n_seg = (int64_t)seg_v.size();
   w.n_hv = (int64_t)hv_first.size();
+  w.light_h = light;
+  w.max_heavy_v = seg_v.empty() ? -1 : *std::max_element(seg_v.begin(), seg_v.end());
   w.light = c->pupload(light);
   w.seg_v = c->pupload(seg_v);
   w.seg_hv = c->pupload(seg_hv);
@@ -229,6 +236,7 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
     c->p_full.col_sorted = nullptr;
     c->d_col_sorted_full = nullptr;
   }
+  c->chunked = c->pworld() > 1 && c->chunk_cols > 0;
   c->d_arrive = c->pmalloc<unsigned int>((size_t)std::max<int64_t>(c->max_hv, 1));
   c->arrive_cap = std::max<int64_t>(c->max_hv, 1);
   c->has_graph = true;
@@ -323,11 +331,30 @@ struct RootFuse {
   double *per_vertex = nullptr;
 };
 
-// N'' = neighbour sum of the passive table P' (size p >= 2) over one pass.
-// sms: the SMs the launch may fill (c->gather_sms)
-void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, const RootFuse *rf, int sms) {
+// The passive rows one neighbour-sum launch reads: columns [c0, c0 + w) of a
+// table whose row r starts at base + r * ld elements, P = base + c0 (a halo
+// buffer of one column chunk: P is its virtual base -- row n_own is the first
+// halo row -- and holds columns c0.. from its column 0).
+struct Src {
+  const void *P;
+  int64_t ld;
+  int c0, w;
+};
+
+Src table_src(const void *base, int64_t ld, int c0, int w, int elem) {
+  return {static_cast<const char *>(base) + (size_t)c0 * elem, ld, c0, w};
+}
+
+// N'' (+)= neighbour sum of the passive columns `src` (size p >= 2) over the
+// items [from, to) of one pass (to < 0: all).  N is the base of the N'' rows
+// (row v at N + v * ldN; a row batch passes a virtual base).  sms: the SMs
+// the launch may fill (c->gather_sms).
+void gather_pass(cc_ctx *c, Pass &w, const Src &src, int p, void *N, int accumulate, const RootFuse *rf, int sms,
+                 int64_t from = 0, int64_t to = -1) {
   const int k = c->plan.colours(), elem = c->elem();
-  const int W_in = (int)binom(k - 1, p - 1), W_out = (int)binom(k - 1, p);
+  const int W_out = (int)binom(k - 1, p);
+  if (to < 0) to = w.items();
+  if (from >= to) return;
   dev::GatherArgs a;
   a.beg = w.beg;
   a.end = w.end;
@@ -335,9 +362,12 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   a.goff = w.goff;
   a.desc = w.desc;
   a.colors = c->d_colors;
-  a.src = P;
-  a.ld_src = c->ld_of(W_in);
-  a.W_in = W_in;
+  a.src = src.P;
+  a.ld_src = src.ld;
+  a.W_in = src.w;
+  a.col_base = src.c0;
+  a.item_from = from;
+  a.item_to = to;
   {
     // narrow rows: items with more than T neighbours (heavy segments first,
     // then light items in degree order) go to the warp-per-item row-parallel
@@ -363,8 +393,9 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   a.accumulate = accumulate;
   a.work = w.view();
   a.ld_scratch = W_out;
-  ScopedAsync scratch(c, (size_t)w.n_seg * W_out * sizeof(double), c->s_main);
-  if (w.n_seg) CUDA_OK(cudaMemsetAsync(c->d_arrive, 0, (size_t)w.n_hv * sizeof(unsigned int), c->s_main));
+  const bool segs = from < w.n_seg;
+  ScopedAsync scratch(c, segs ? (size_t)w.n_seg * W_out * sizeof(double) : 0, c->s_main);
+  if (segs) CUDA_OK(cudaMemsetAsync(c->d_arrive, 0, (size_t)w.n_hv * sizeof(unsigned int), c->s_main));
   a.scratch = static_cast<double *>(scratch.p);
   a.arrive = c->d_arrive;
   if (rf) {
@@ -382,12 +413,15 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
   // algorithmic bytes: index stream + compressed rows of the neighbours whose
   // colour differs from the row vertex's (expected fraction (k-1)/k) + N'' rows
   // written (+ read when accumulating)
-  const double rows = (double)w.nnz * (double)(k - 1) / k * W_in * elem;
-  const double out_bytes = rf ? (double)(w.n_light + w.n_hv) * (8.0 + (rf->mode == 1 ? (double)rf->WA * elem : 0.0))
-                              : (double)(w.n_light + w.n_hv) * W_out * elem * (1 + accumulate);
-  const double bytes = (double)w.nnz * 4.0 + rows + out_bytes;
+  const double nnz = (double)(w.pref[(size_t)to] - w.pref[(size_t)from]);
+  const double rows_out = (double)(to - from) - (segs ? (double)(std::min(to, w.n_seg) - from) : 0.0) +
+                          (segs ? (double)w.n_hv : 0.0);
+  const double rows = nnz * (double)(k - 1) / k * src.w * elem;
+  const double out_bytes = rf ? rows_out * (8.0 + (rf->mode == 1 ? (double)rf->WA * elem : 0.0))
+                              : rows_out * W_out * elem * (1 + accumulate);
+  const double bytes = nnz * 4.0 + rows + out_bytes;
   if (!c->ev_log.empty()) c->gather_log.push_back({c->ev_log.size() - 1, bytes});
-  c->stats[0] += (double)w.nnz * (double)binom(k, p);  // U: dense edge x colour-set updates
+  c->stats[0] += nnz * (double)src.w / (double)binom(k - 1, p - 1) * (double)binom(k, p);  // U
   c->stats[1] += bytes;
   c->stats[2] += bytes;
 }
@@ -395,7 +429,7 @@ void gather_pass(cc_ctx *c, Pass &w, void *P, int p, void *N, int accumulate, co
 // Loopback transport (cc_options.loopback): the halo rows of this rank come
 // from the peers' send buffers by device copies ordered by the peers' pack
 // events; this rank's send buffer is released only after every peer's copy.
-void loopback_exchange(cc_ctx *c, void *sendbuf, void *P, int64_t ld, int elem,
+void loopback_exchange(cc_ctx *c, void *sendbuf, void *H, int64_t ldH, int elem,
                        std::vector<std::pair<int, cudaEvent_t>> *steps) {
   LoopbackGroup &G = *c->loop;
   const auto &R = c->part;
@@ -412,9 +446,9 @@ void loopback_exchange(cc_ctx *c, void *sendbuf, void *P, int64_t ld, int elem,
     const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
     if (nr) {
       CUDA_OK(cudaStreamWaitEvent(c->s_comm, G.ev[q], 0));
-      CUDA_OK(cudaMemcpyAsync(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[q]) * ld * elem,
-                              static_cast<const char *>(G.ptr[q]) + (size_t)G.offs[q][me] * ld * elem,
-                              (size_t)nr * ld * elem, cudaMemcpyDeviceToDevice, c->s_comm));
+      CUDA_OK(cudaMemcpyAsync(static_cast<char *>(H) + (size_t)R.recv_off[q] * ldH * elem,
+                              static_cast<const char *>(G.ptr[q]) + (size_t)G.offs[q][me] * ldH * elem,
+                              (size_t)nr * ldH * elem, cudaMemcpyDeviceToDevice, c->s_comm));
     }
     if (ring && steps) {
       cudaEvent_t e = c->ev();
@@ -446,28 +480,26 @@ void loopback_allreduce(cc_ctx *c, double *d, size_t count, cudaStream_t s) {
   CUDA_OK(cudaStreamSynchronize(s));
 }
 
-// world > 1: send this rank's boundary rows of P' to the peers that need
-// them and receive the halo rows (after the owned rows of P') on the comm
-// stream; returns an event recorded when the halo rows have arrived.
-// ring schedule: *steps (nullable) receives (source peer, event recorded
-// when that peer's rows have arrived) in step order.
-cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p, std::vector<std::pair<int, cudaEvent_t>> *steps = nullptr) {
+// world > 1, on the comm stream (the caller orders it after the producer of
+// P): send columns [c0, c0 + w) of this rank's boundary rows of P (owned
+// rows, stride ldP) to the peers that need them and receive the peers' rows
+// into H (halo row i at H + i * ldH).  Returns an event recorded when every
+// halo row has arrived; ring schedule: *steps (nullable) receives (source
+// peer, event recorded when that peer's rows have arrived) in step order.
+cudaEvent_t exchange_halo(cc_ctx *c, const void *P, int64_t ldP, int64_t c0, int64_t w, void *H, int64_t ldH,
+                          std::vector<std::pair<int, cudaEvent_t>> *steps = nullptr) {
   auto &api = nccl();
-  const int k = c->plan.colours(), elem = c->elem();
-  const int64_t ld = c->ld_of(binom(k - 1, p - 1));
-  cudaEvent_t ready = c->ev(), recvd = c->ev();
-  CUDA_OK(cudaEventRecord(ready, c->s_main));
-  CUDA_OK(cudaStreamWaitEvent(c->s_comm, ready, 0));
+  const int elem = c->elem();
   const auto &R = c->part;
   const int64_t send_rows = R.send_off[c->pworld()];
-  ScopedAsync sb(c, (size_t)send_rows * ld * elem, c->s_comm);  // released after the sends (stream order)
+  ScopedAsync sb(c, (size_t)send_rows * ldH * elem, c->s_comm);  // released after the sends (stream order)
   void *sendbuf = sb.p;
   cudaEvent_t xb = c->begin(c->s_comm);
-  c->stats[3] += dev::launch_pack(elem, P, ld, c->d_send_idx, send_rows, sendbuf, c->s_comm);
+  c->stats[3] += dev::launch_pack(elem, P, ldP, c0, w, c->d_send_idx, send_rows, sendbuf, ldH, c->s_comm);
   c->check_launch();
   const ncclDataType_t dt = elem == 8 ? ncclFloat64 : ncclFloat32;
   if (c->loop) {
-    loopback_exchange(c, sendbuf, P, ld, elem, steps);
+    loopback_exchange(c, sendbuf, H, ldH, elem, steps);
   } else if (c->xmode == CC_EXCHANGE_RING) {
     // Alg. 3 lines 2-6: step r sends to rank + r and receives from rank - r
     const int W = c->pworld(), me = c->opt.rank;
@@ -477,11 +509,11 @@ cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p, std::vector<std::pair<int, 
       const int64_t nr = R.recv_off[src + 1] - R.recv_off[src];
       NCCL_OK(api.GroupStart());
       if (ns)
-        NCCL_OK(api.Send(static_cast<char *>(sendbuf) + (size_t)R.send_off[dst] * ld * elem, (size_t)(ns * ld), dt,
+        NCCL_OK(api.Send(static_cast<char *>(sendbuf) + (size_t)R.send_off[dst] * ldH * elem, (size_t)(ns * ldH), dt,
                          dst, c->comm, c->s_comm));
       if (nr)
-        NCCL_OK(api.Recv(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[src]) * ld * elem,
-                         (size_t)(nr * ld), dt, src, c->comm, c->s_comm));
+        NCCL_OK(api.Recv(static_cast<char *>(H) + (size_t)R.recv_off[src] * ldH * elem, (size_t)(nr * ldH), dt, src,
+                         c->comm, c->s_comm));
       NCCL_OK(api.GroupEnd());
       if (steps) {
         cudaEvent_t e = c->ev();
@@ -490,51 +522,107 @@ cudaEvent_t exchange_halo(cc_ctx *c, void *P, int p, std::vector<std::pair<int, 
       }
     }
   } else {
-  NCCL_OK(api.GroupStart());
-  for (int q = 0; q < c->pworld(); ++q) {
-    if (q == c->opt.rank) continue;
-    const int64_t ns = R.send_off[q + 1] - R.send_off[q];
-    const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
-    if (ns)
-      NCCL_OK(api.Send(static_cast<char *>(sendbuf) + (size_t)R.send_off[q] * ld * elem, (size_t)(ns * ld), dt, q,
-                       c->comm, c->s_comm));
-    if (nr)
-      NCCL_OK(api.Recv(static_cast<char *>(P) + (size_t)(c->n_own + R.recv_off[q]) * ld * elem, (size_t)(nr * ld), dt,
-                       q, c->comm, c->s_comm));
-  }
-  NCCL_OK(api.GroupEnd());
+    NCCL_OK(api.GroupStart());
+    for (int q = 0; q < c->pworld(); ++q) {
+      if (q == c->opt.rank) continue;
+      const int64_t ns = R.send_off[q + 1] - R.send_off[q];
+      const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
+      if (ns)
+        NCCL_OK(api.Send(static_cast<char *>(sendbuf) + (size_t)R.send_off[q] * ldH * elem, (size_t)(ns * ldH), dt, q,
+                         c->comm, c->s_comm));
+      if (nr)
+        NCCL_OK(api.Recv(static_cast<char *>(H) + (size_t)R.recv_off[q] * ldH * elem, (size_t)(nr * ldH), dt, q,
+                         c->comm, c->s_comm));
+    }
+    NCCL_OK(api.GroupEnd());
   }
   c->end(PH_EXCHANGE, c->s_comm, xb);
+  cudaEvent_t recvd = c->ev();
   CUDA_OK(cudaEventRecord(recvd, c->s_comm));
-  c->stats[1] += (double)send_rows * ld * elem * 2;
-  c->stats[9] += (double)(R.recv_off[c->pworld()]) * ld * elem;  // halo bytes received
+  c->stats[1] += (double)send_rows * w * elem * 2;
+  c->stats[9] += (double)(R.recv_off[c->pworld()]) * w * elem;  // halo bytes received
   return recvd;
 }
 
-void aggregate(cc_ctx *c, void *P, int p, void *N) {
+// The comm stream waits for everything queued on the main stream so far.
+void comm_after_main(cc_ctx *c) {
+  cudaEvent_t e = c->ev();
+  CUDA_OK(cudaEventRecord(e, c->s_main));
+  CUDA_OK(cudaStreamWaitEvent(c->s_comm, e, 0));
+}
+
+// Column chunks of a passive table of W_in columns: widths that
+// are multiples of 8 columns (32-byte sectors of fp32 rows), chunk_cols wide.
+std::vector<std::pair<int, int>> column_chunks(int W_in, int64_t chunk_cols) {
+  std::vector<std::pair<int, int>> out;
+  const int w = chunk_cols > 0 ? (int)std::min<int64_t>(W_in, (chunk_cols + 7) / 8 * 8) : W_in;
+  for (int c0 = 0; c0 < W_in; c0 += w) out.push_back({c0, std::min(w, W_in - c0)});
+  return out;
+}
+
+// N'' = neighbour sum of the passive table P (rows of stride ldP, size p >= 2).
+// One rank: one launch per column chunk, the later ones accumulating.  The
+// 1D partition: the boundary rows of P are exchanged on the comm stream while
+// the local part runs; then the remote part --
+// grouped: one pass once every halo row is in; ring: one pass per step, each
+// as soon as its peer's rows have arrived.  Unchunked, halo rows land in P
+// after the owned rows; chunked (c->chunked), per column chunk into one of
+// two halo buffers (chunk i + 1 transfers while chunk i is summed): the
+// pipeline's memory bound PeakMem^pip.
+void aggregate(cc_ctx *c, void *P, int64_t ldP, int p, void *N) {
+  const int k = c->plan.colours(), elem = c->elem();
+  const int W_in = (int)binom(k - 1, p - 1);
+  const auto chunks = column_chunks(W_in, c->chunk_cols);
+  if (chunks.size() > 1) c->stats[11] += (double)chunks.size();
   if (c->pworld() == 1) {
-    gather_pass(c, c->p_full, P, p, N, 0, nullptr, c->num_sms);
+    for (size_t i = 0; i < chunks.size(); ++i)
+      gather_pass(c, c->p_full, table_src(P, ldP, chunks[i].first, chunks[i].second, elem), p, N, i > 0, nullptr,
+                  c->num_sms);
     return;
   }
-  // world > 1: exchange the boundary rows of P' on the comm stream while the
-  // local part runs; then add the remote part --
-  // grouped: one pass once every halo row is in; ring: one pass per step,
-  // each as soon as its peer's rows have arrived (the next step transfers
-  // meanwhile)
-  std::vector<std::pair<int, cudaEvent_t>> steps;
   const bool ring = c->xmode == CC_EXCHANGE_RING;
-  cudaEvent_t recvd = exchange_halo(c, P, p, ring ? &steps : nullptr);
-  gather_pass(c, c->p_local, P, p, N, 0, nullptr, c->gather_sms(true));
-  if (!ring) steps.push_back({-1, recvd});
-  for (const auto &st : steps) {
-    Pass &w = st.first < 0 ? c->p_remote : c->p_peer[st.first];
-    if (!w.items()) continue;
-    cudaEvent_t wb = c->begin(c->s_main);  // exposed exchange: s_main idles until the rows are in
-    CUDA_OK(cudaStreamWaitEvent(c->s_main, st.second, 0));
-    c->end(PH_EXPOSED, c->s_main, wb);
-    gather_pass(c, w, P, p, N, 1, nullptr, c->gather_sms(ring));  // ring: the next step transfers meanwhile
+  auto remote = [&](const std::vector<std::pair<int, cudaEvent_t>> &steps, const Src &src) {
+    for (const auto &st : steps) {
+      Pass &w = st.first < 0 ? c->p_remote : c->p_peer[st.first];
+      if (!w.items()) continue;
+      cudaEvent_t wb = c->begin(c->s_main);  // exposed exchange: s_main idles until the rows are in
+      CUDA_OK(cudaStreamWaitEvent(c->s_main, st.second, 0));
+      c->end(PH_EXPOSED, c->s_main, wb);
+      gather_pass(c, w, src, p, N, 1, nullptr, c->gather_sms(ring));  // ring: the next step transfers meanwhile
+    }
+  };
+  if (!c->chunked) {
+    comm_after_main(c);
+    std::vector<std::pair<int, cudaEvent_t>> steps;
+    cudaEvent_t recvd = exchange_halo(c, P, ldP, 0, ldP, static_cast<char *>(P) + (size_t)c->n_own * ldP * elem, ldP,
+                                      ring ? &steps : nullptr);
+    gather_pass(c, c->p_local, table_src(P, ldP, 0, W_in, elem), p, N, 0, nullptr, c->gather_sms(true));
+    if (!ring) steps.push_back({-1, recvd});
+    remote(steps, table_src(P, ldP, 0, W_in, elem));
+    CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));  // the send buffer's release is ordered after every step
+    return;
   }
-  CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));  // the send buffer's release is ordered after every step
+  // chunked: double-buffered halo buffers of the chunk width
+  const int64_t ldH = c->ld_of(chunks[0].second);
+  const size_t hbytes = (size_t)std::max<int64_t>(c->n_halo, 1) * ldH * elem;
+  ScopedAsync H0(c, hbytes, c->s_main), H1(c, chunks.size() > 1 ? hbytes : 0, c->s_main);
+  void *H[2] = {H0.p, H1.p ? H1.p : H0.p};
+  cudaEvent_t hfree[2] = {nullptr, nullptr};
+  comm_after_main(c);  // P produced and the halo buffers allocated
+  cudaEvent_t recvd = nullptr;
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const int c0 = chunks[i].first, w = chunks[i].second;
+    if (hfree[i % 2]) CUDA_OK(cudaStreamWaitEvent(c->s_comm, hfree[i % 2], 0));  // chunk i - 2 summed
+    std::vector<std::pair<int, cudaEvent_t>> steps;
+    recvd = exchange_halo(c, P, ldP, c0, w, H[i % 2], ldH, ring ? &steps : nullptr);
+    gather_pass(c, c->p_local, table_src(P, ldP, c0, w, elem), p, N, i > 0, nullptr, c->gather_sms(true));
+    if (!ring) steps.push_back({-1, recvd});
+    // the remote rows of this chunk: halo row j at H + j * ldH, i.e. table row n_own + j
+    remote(steps, Src{static_cast<char *>(H[i % 2]) - (size_t)c->n_own * ldH * elem, ldH, c0, w});
+    hfree[i % 2] = c->ev();
+    CUDA_OK(cudaEventRecord(hfree[i % 2], c->s_main));
+  }
+  CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));  // every send buffer released before the halo buffers
 }
 
 }  // namespace
@@ -574,11 +662,186 @@ void free_cache(cc_ctx *c, TableCache &cache) {
   cache.bytes = 0;
 }
 
+namespace {
+
+// The memory plan of one count.  tail >= 0: steps [tail, end)
+// run in nb row batches; rc >= 0: step rc (the producer of step tail's
+// passive table) is not run in full but per batch, in column chunks of rc_w.
+struct MemPlan {
+  int tail = -1, nb = 1, rc = -1, rc_w = 0;
+};
+
+// Modelled peak of the stream-ordered table memory of run_count's schedule
+// (same buffers, same reference counts, same releases), for a memory plan.
+double model_peak(cc_ctx *c, const Plan &pl, int64_t rows, int fuse, int defer_lift, int fuse_cr, int last_hist_use,
+                  bool per_vertex, const MemPlan &mp) {
+  const int k = pl.colours(), elem = c->elem(), nt = (int)pl.tables.size(), sr = (int)pl.steps.size() - 1;
+  const int64_t n = c->n_own;
+  std::vector<int> last_use(pl.table_last_use), n_last(pl.n_last_use);
+  if (mp.tail >= 0) {
+    fuse = 0;
+    defer_lift = -1;
+  } else if (fuse == 2) {
+    last_use[pl.steps[sr].passive] = sr;
+  }
+  if (mp.rc >= 0) {
+    const Step &q = pl.steps[mp.rc];
+    if (q.active >= 0) last_use[q.active] = sr + 1;
+    if (q.p == 1) last_hist_use = sr + 1;
+    else n_last[q.passive] = sr + 1;
+  }
+  auto tbytes = [&](int size) { return (double)rows * c->ld_of(binom(k - 1, size - 1)) * elem; };
+  auto nbytes = [&](int p) { return (double)rows * c->ld_of(binom(k - 1, p)) * elem; };
+  std::vector<double> bb;  // buffers: bytes (0 = freed)
+  std::vector<int> refs;
+  double live = 0, peak = 0;
+  auto make = [&](double b) {
+    bb.push_back(b);
+    refs.push_back(1);
+    live += b;
+    return (int)bb.size() - 1;
+  };
+  auto unref = [&](int b) {
+    if (b >= 0 && --refs[b] == 0) live -= bb[b];
+  };
+  if (per_vertex || fuse || fuse_cr >= 0 || mp.tail >= 0) make((double)n * 8);
+  const double scratch = (double)c->p_full.n_seg * 8;  // x W_out: heavy partial rows of one gather
+  std::vector<int> T(nt, -1), Nb(nt, -1);
+  int hist = -1;
+  const int stop = mp.tail >= 0 ? mp.tail : sr + 1;
+  for (int s = 0; s < stop; ++s) {
+    const Step &st = pl.steps[s];
+    if (s == mp.rc || s == defer_lift) continue;
+    double transient = 0;
+    if (s == sr && fuse) {
+      peak = std::max(peak, live + scratch * binom(k - 1, st.p));
+      break;
+    }
+    int nbuf;
+    if (st.p == 1) {
+      if (hist < 0) hist = make((double)rows * c->ld_of(k - 1) * elem);
+      nbuf = hist;
+    } else {
+      if (Nb[st.passive] < 0) {
+        Nb[st.passive] = make(nbytes(st.p));
+        transient = scratch * binom(k - 1, st.p);
+      }
+      nbuf = Nb[st.passive];
+    }
+    if (st.out < 0) {
+      if (pl.k < k && st.a > 1) transient += tbytes(st.t);
+    } else if (st.a == 1) {
+      T[st.out] = nbuf;
+      ++refs[nbuf];
+    } else if (s != fuse_cr) {
+      T[st.out] = make(tbytes(st.t));
+    }
+    peak = std::max(peak, live + transient);
+    for (int id = 0; id < nt; ++id) {
+      if (T[id] >= 0 && last_use[id] == s) unref(T[id]), T[id] = -1;
+      if (Nb[id] >= 0 && n_last[id] == s) unref(Nb[id]), Nb[id] = -1;
+    }
+    if (hist >= 0 && s == last_hist_use) unref(hist), hist = -2;
+  }
+  if (mp.tail >= 0) {  // one batch of the tail on top of what is alive
+    const int64_t br = (n + mp.nb - 1) / mp.nb + std::max<int64_t>(c->p_full.max_heavy_v + 1 - n / mp.nb, 0);
+    const Step &gs = pl.steps[mp.tail];
+    double batch = (double)br * c->ld_of(binom(k - 1, gs.p)) * elem + scratch * binom(k - 1, gs.p);
+    for (int s = mp.tail; s <= sr; ++s) {
+      const Step &st = pl.steps[s];
+      if ((st.out >= 0 && st.a > 1 && s != fuse_cr) || (st.out < 0 && pl.k < k && st.a > 1))
+        batch += (double)br * c->ld_of(binom(k - 1, st.t - 1)) * elem;
+    }
+    if (mp.rc >= 0) batch += (double)rows * c->ld_of(mp.rc_w) * elem;
+    peak = std::max(peak, live + batch);
+  }
+  return peak;
+}
+
+MemPlan plan_memory(cc_ctx *c, const Plan &pl, int64_t rows, int fuse, int defer_lift, int fuse_cr, int last_hist_use,
+                    bool per_vertex) {
+  MemPlan none;
+  const int sr = (int)pl.steps.size() - 1, forced_nb = c->knobs.tail_batches, forced_w = c->knobs.tail_recompute_cols;
+  if (c->pworld() > 1) return none;  // one rank only (the 1D partition bounds memory with chunked halo buffers)
+  // the budget: free device memory + what the stream-ordered pool holds unused, less a margin
+  size_t free_b = 0, total_b = 0;
+  CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+  cudaMemPool_t pool;
+  CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, c->opt.device));
+  uint64_t reserved = 0, used = 0;
+  CUDA_OK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  CUDA_OK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  const double budget = ((double)free_b + (double)(reserved - std::min(reserved, used))) * 0.97 - 1.5e9;
+  if (forced_nb <= 0 && forced_w <= 0 &&
+      model_peak(c, pl, rows, fuse, defer_lift, fuse_cr, last_hist_use, per_vertex, none) <= budget)
+    return none;
+  // the tail: the last step that starts a neighbour sum; every later step must be row-local
+  int g = -1;
+  for (int s = 0; s <= sr; ++s)
+    if (pl.steps[s].p >= 2 && pl.n_first_use[pl.steps[s].passive] == s) g = s;
+  if (g < 0) return none;
+  for (int s = g + 1; s <= sr; ++s)
+    if (pl.steps[s].p >= 2 && pl.n_first_use[pl.steps[s].passive] > g) return none;
+  // the producer of the tail's passive table may be recomputed when it is a
+  // combine and that table feeds nothing but this neighbour sum
+  const int P = pl.steps[g].passive;
+  int q = -1;
+  for (int s = 0; s < g; ++s)
+    if (pl.steps[s].out == P) q = s;
+  bool rc_ok = q >= 0 && pl.steps[q].a >= 2 && pl.table_last_use[P] == g;
+  for (int s = 0; s <= sr; ++s) rc_ok = rc_ok && pl.steps[s].active != P;
+  const int Win = (int)binom(pl.colours() - 1, pl.steps[g].p - 1);
+  auto fits = [&](const MemPlan &m) {
+    return model_peak(c, pl, rows, fuse, defer_lift, fuse_cr, last_hist_use, per_vertex, m) <= budget;
+  };
+  if (forced_nb > 0 || forced_w > 0) {  // knobs (tests): this batching, whatever the memory
+    MemPlan m;
+    m.tail = g;
+    m.nb = std::max(1, forced_nb);
+    if (forced_w > 0 && rc_ok) {
+      m.rc = q;
+      m.rc_w = (int)std::min<int64_t>(Win, (forced_w + 7) / 8 * 8);
+    }
+    return m;
+  }
+  static const int nbs[] = {2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};
+  for (int nb : nbs) {
+    MemPlan m;
+    m.tail = g;
+    m.nb = nb;
+    if (fits(m)) return m;
+  }
+  if (rc_ok)
+    for (int nb : nbs)
+      for (int w = (Win + 7) / 8 * 8; w >= 64; w = (w / 2 + 7) / 8 * 8) {
+        MemPlan m;
+        m.tail = g;
+        m.nb = nb;
+        m.rc = q;
+        m.rc_w = std::min(w, Win);
+        if (fits(m)) return m;
+        if (w == 64) break;
+      }
+  return none;  // nothing fits: run as planned (the allocation reports CC_ERR_OOM)
+}
+
+// Row batches [b[i], b[i + 1]) of the n owned rows: equal sizes, the first
+// holding every heavy vertex (hubs are the lowest internal ids, so each
+// batch's work items are one contiguous range of the pass).
+std::vector<int64_t> batch_bounds(const Pass &w, int64_t n, int nb) {
+  std::vector<int64_t> b((size_t)nb + 1);
+  for (int i = 0; i <= nb; ++i) b[i] = n * i / nb;
+  for (int i = 1; i < nb; ++i) b[i] = std::max(b[i], std::min<int64_t>(n, w.max_heavy_v + 1));
+  return b;
+}
+
+}  // namespace
+
 void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out,
                const std::vector<int64_t> *dump_rows, TableCache *cache) {
   const Plan &pl = c->plan;
   const int k = pl.colours(), elem = c->elem();
-  std::fill(c->stats, c->stats + 11, 0.0);
+  std::fill(c->stats, c->stats + kNStats, 0.0);
   c->stats[10] = c->xmode;
   c->phase_events = c->profiling && c->knobs.phase_events;
   c->gather_log.clear();
@@ -590,7 +853,9 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     *X = (double)c->n_global;
     return;
   }
-  const int64_t n = c->n_own, rows = c->n_rows;
+  // table rows: owned + halo (halo rows of passive tables land there), or
+  // owned only when the exchange is chunked (halo rows go to chunk buffers)
+  const int64_t n = c->n_own, rows = c->chunked ? c->n_own : c->n_rows;
   cudaEvent_t t0 = c->ev(), t1 = c->ev();
   CUDA_OK(cudaEventRecord(t0, c->s_main));
 
@@ -619,7 +884,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   std::vector<int> last_use(pl.table_last_use);
   {
     const Step &rs = pl.steps[sr];
-    if (pl.k == k && !cache && (dump_table < 0 || dump_rows) && c->knobs.fused_root && rs.out < 0 && rs.p >= 2) {
+    if (pl.k == k && !cache && (dump_table < 0 || dump_rows) && c->knobs.fused_root && !c->chunked &&
+        c->chunk_cols == 0 && rs.out < 0 && rs.p >= 2) {
       const int P = rs.passive;
       int s_l = -1, users = 0;
       for (int s = 0; s < sr; ++s) {
@@ -657,16 +923,45 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     }
   }
 
-  c->stats[5] = fuse;
-  Bufs bufs(c);
   const int nt = (int)pl.tables.size();
-  std::vector<int> T(nt, -1), Nb(nt, -1);
-  int hist = -1;
   int last_hist_use = -1;
   for (int s = 0; s < (int)pl.steps.size(); ++s)
     if (pl.steps[s].p == 1) last_hist_use = s;
+  std::vector<int> n_last(pl.n_last_use);
+
+  // Memory plan: when the tables of
+  // this plan would not fit the free device memory, the tail of the plan --
+  // its last neighbour sum and the row-local steps after it -- runs in row
+  // batches, and if even that does not fit, the tail's passive table is
+  // never stored but recomputed per batch in column chunks by its combine.
+  const MemPlan mp = (cache || (dump_table >= 0 && !dump_rows))
+                         ? MemPlan()
+                         : plan_memory(c, pl, rows, fuse, defer_lift, fuse_cr, last_hist_use, root_out != nullptr);
+  if (mp.tail >= 0) {  // the batched tail evaluates the root per batch (no gather-epilogue root)
+    if (fuse == 2) last_use[pl.steps[sr].passive] = pl.table_last_use[pl.steps[sr].passive];
+    fuse = 0;
+    defer_lift = -1;
+    if (mp.rc >= 0) {  // the recomputed table's inputs stay until the end
+      const Step &q = pl.steps[mp.rc];
+      if (q.active >= 0) last_use[q.active] = sr + 1;
+      if (q.p == 1) last_hist_use = sr + 1;
+      else n_last[q.passive] = sr + 1;
+    }
+  }
+  if (mp.tail >= 0 && dump_rows && dump_table >= 0) {
+    for (int s = mp.tail; s < (int)pl.steps.size(); ++s)
+      if (pl.steps[s].out == dump_table || (mp.rc >= 0 && pl.steps[mp.rc].out == dump_table))
+        throw Error(CC_ERR_STATE, "the table asked for is produced in the row-batched tail of the memory plan");
+  }
+  c->stats[12] = mp.tail >= 0 ? mp.nb : 0;
+  c->stats[13] = mp.rc >= 0 ? mp.rc_w : 0;
+
+  c->stats[5] = fuse;
+  Bufs bufs(c);
+  std::vector<int> T(nt, -1), Nb(nt, -1);
+  int hist = -1;
   double *per_vertex = nullptr;
-  if (root_out || fuse || fuse_cr >= 0)
+  if (root_out || fuse || fuse_cr >= 0 || mp.tail >= 0)
     per_vertex = static_cast<double *>(bufs.ptr(bufs.make((size_t)std::max<int64_t>(n, 1) * 8)));
   if (cache && cache->sorted) {  // an earlier template of this colouring sorted and built the leaf level
     if (last_hist_use >= 0) hist = bufs.alias(cache->hist, cache->hist_bytes);
@@ -729,6 +1024,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   for (int s = 0; s < (int)pl.steps.size(); ++s) {
     const Step &st = pl.steps[s];
     const int Wa = (int)binom(k - 1, st.a - 1), Wp = (int)binom(k - 1, st.p), Wt = (int)binom(k - 1, st.t - 1);
+    if (mp.tail >= 0 && s >= mp.tail) break;  // the batched tail (below)
+    if (s == mp.rc) continue;                  // recomputed per batch in column chunks
     if (s == defer_lift) continue;  // T_out = N''(P) is evaluated inside the fused root
     if (cache && st.out >= 0) {
       if (!need[st.out]) continue;  // only feeds tables this template finds cached
@@ -746,6 +1043,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       rf.ldA = c->ld_of(Wa);
       rf.WA = Wa;
       rf.per_vertex = per_vertex;
+      void *Pp = bufs.ptr(T[st.passive]);
+      const int64_t ldP = c->ld_of(binom(k - 1, st.p - 1));
       if (c->pworld() > 1) {
         // partitioned: the fused root needs whole neighbour ranges, so the
         // halo rows of the passive table arrive first and the full ranges
@@ -758,10 +1057,13 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
           c->end(PH_CSORT, c->s_main, b);
           c->full_sorted_valid = true;
         }
-        cudaEvent_t recvd = exchange_halo(c, bufs.ptr(T[st.passive]), st.p);
+        comm_after_main(c);
+        cudaEvent_t recvd =
+            exchange_halo(c, Pp, ldP, 0, ldP, static_cast<char *>(Pp) + (size_t)c->n_own * ldP * elem, ldP);
         CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));
       }
-      gather_pass(c, c->p_full, bufs.ptr(T[st.passive]), st.p, nullptr, 0, &rf, c->num_sms);
+      gather_pass(c, c->p_full, table_src(Pp, ldP, 0, (int)binom(k - 1, st.p - 1), elem), st.p, nullptr, 0, &rf,
+                  c->num_sms);
       cudaEvent_t b = c->begin(c->s_main);
       c->stats[3] += dev::launch_root(8, nullptr, 0, 0, per_vertex, 1, nullptr, n, c->d_partials, c->n_partials,
                                       nullptr, c->d_result, c->s_main);
@@ -794,7 +1096,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
           ++cache->reused;
         } else {
           Nb[P] = bufs.make((size_t)rows * c->ld_of(Wp) * elem);
-          aggregate(c, bufs.ptr(T[P]), st.p, bufs.ptr(Nb[P]));
+          aggregate(c, bufs.ptr(T[P]), c->ld_of(binom(k - 1, st.p - 1)), st.p, bufs.ptr(Nb[P]));
           Buf &bb = bufs.pool[Nb[P]];
           if (cache && cache->bytes + bb.bytes <= cache->budget) {
             cache->tables[nkey] = {bb.p, bb.bytes};
@@ -901,7 +1203,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
           bufs.unref(T[id]);
           T[id] = -1;
         }
-        if (Nb[id] >= 0 && pl.n_last_use[id] == s) {
+        if (Nb[id] >= 0 && n_last[id] == s) {
           bufs.unref(Nb[id]);
           Nb[id] = -1;
         }
@@ -911,6 +1213,119 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
         hist = -2;  // computed and released
       }
     }
+  }
+  if (mp.tail >= 0) {
+    // The batched tail (memory plan): for each batch of rows [r0, r1), the
+    // neighbour sum of step g for those rows only (their work items), from
+    // the stored passive table or from its column chunks recomputed by their
+    // combine for every row, then the row-local steps g..root on those rows.
+    const int g = mp.tail;
+    const Step &gs = pl.steps[g];
+    const int P = gs.passive;
+    const int WinP = (int)binom(k - 1, gs.p - 1), WpP = (int)binom(k - 1, gs.p);
+    const int64_t ldP = c->ld_of(WinP), ldNP = c->ld_of(WpP);
+    Pass &w = c->p_full;
+    const std::vector<int64_t> bounds = batch_bounds(w, n, mp.nb);
+    int rcb = -1;
+    const int64_t ldw = mp.rc >= 0 ? c->ld_of(mp.rc_w) : 0;
+    if (mp.rc >= 0) rcb = bufs.make((size_t)std::max<int64_t>(rows, 1) * ldw * elem);
+    for (size_t b = 0; b + 1 < bounds.size(); ++b) {
+      const int64_t r0 = bounds[b], r1 = bounds[b + 1], nr = r1 - r0;
+      if (nr <= 0) continue;
+      // the batch's work items: its light vertices (contiguous in the item
+      // list) and, in batch 0, every heavy segment
+      const int64_t lo = std::lower_bound(w.light_h.begin(), w.light_h.end(), (int32_t)r0) - w.light_h.begin();
+      const int64_t hi = std::lower_bound(w.light_h.begin(), w.light_h.end(), (int32_t)r1) - w.light_h.begin();
+      const int64_t from = b == 0 ? 0 : w.n_seg + lo, to = w.n_seg + hi;
+      // row r0 of every table the tail reads: stored in full (offset) or made in this batch
+      std::vector<const void *> TB(nt, nullptr), NB(nt, nullptr);
+      std::vector<int> batch_bufs;
+      auto row0 = [&](int buf, int64_t ld) -> const void * {
+        return static_cast<const char *>(bufs.ptr(buf)) + (size_t)r0 * ld * elem;
+      };
+      const int nbb = bufs.make((size_t)nr * ldNP * elem);
+      batch_bufs.push_back(nbb);
+      NB[P] = bufs.ptr(nbb);
+      void *Nv = static_cast<char *>(bufs.ptr(nbb)) - (size_t)r0 * ldNP * elem;  // row v at Nv + v ldNP
+      if (mp.rc < 0) {
+        gather_pass(c, w, table_src(bufs.ptr(T[P]), ldP, 0, WinP, elem), gs.p, Nv, 0, nullptr, c->num_sms, from, to);
+      } else {
+        const Step &q = pl.steps[mp.rc];
+        const int qa = (int)binom(k - 1, q.a - 1), qp = (int)binom(k - 1, q.p);
+        const void *Aq = bufs.ptr(T[q.active]);
+        const void *Nq = q.p == 1 ? bufs.ptr(hist) : bufs.ptr(Nb[q.passive]);
+        const auto chunks = column_chunks(WinP, mp.rc_w);
+        for (size_t i = 0; i < chunks.size(); ++i) {
+          const int c0 = chunks[i].first, cw = chunks[i].second;
+          // columns [c0, c0 + cw) of the passive table, every row: column o of row v at outv + v ldw + o
+          void *outv = static_cast<char *>(bufs.ptr(rcb)) - (size_t)c0 * elem;
+          cudaEvent_t e = c->begin(c->s_main);
+          c->stats[3] += dev::launch_combine_cols(elem, Aq, c->ld_of(qa), qa, Nq, c->ld_of(qp), qp, c->d_split[mp.rc],
+                                                  (int)binom(q.t - 1, q.a - 1), n, outv, ldw, WinP, c0, c0 + cw,
+                                                  c->knobs, c->num_sms, c->s_main);
+          c->check_launch();
+          c->end(PH_COMBINE, c->s_main, e);
+          c->stats[1] += (double)n * (qa + qp + cw) * elem;
+          gather_pass(c, w, Src{bufs.ptr(rcb), ldw, c0, cw}, gs.p, Nv, i > 0, nullptr, c->num_sms, from, to);
+        }
+      }
+      double *pv = per_vertex + r0;
+      bool cr_batch = false;
+      for (int s2 = g; s2 <= sr; ++s2) {
+        const Step &st = pl.steps[s2];
+        const int Wa = (int)binom(k - 1, st.a - 1), Wp = (int)binom(k - 1, st.p), Wt = (int)binom(k - 1, st.t - 1);
+        const int64_t ldA = c->ld_of(Wa), ldN = c->ld_of(Wp), ldT = c->ld_of(Wt);
+        const void *A = st.active < 0 ? nullptr : (TB[st.active] ? TB[st.active] : row0(T[st.active], ldA));
+        const void *Nn = st.p == 1 ? row0(hist, c->ld_of(k - 1))
+                                   : (NB[st.passive] ? NB[st.passive] : row0(Nb[st.passive], ldN));
+        cudaEvent_t e = c->begin(c->s_main);
+        if (st.out < 0 && pl.k < k) {  // fewer template vertices than colours: root table, row sums
+          const void *R = Nn;
+          if (st.a > 1) {
+            const int rb = bufs.make((size_t)nr * ldT * elem);
+            batch_bufs.push_back(rb);
+            c->stats[3] += dev::launch_combine(elem, A, ldA, Wa, Nn, ldN, Wp, c->d_split[s2],
+                                               (int)binom(st.t - 1, st.a - 1), nr, bufs.ptr(rb), ldT, Wt,
+                                               c->d_ztab[s2], c->zblocks[s2], (int)zblock_ld(st.t - 1, st.a - 1),
+                                               st.t - 1, st.a - 1, c->knobs, c->num_sms, c->s_main);
+            R = bufs.ptr(rb);
+          }
+          c->stats[3] += dev::launch_rowsum(elem, R, ldT, Wt, nr, c->d_partials, c->n_partials, pv, c->d_result,
+                                            c->s_main);
+        } else if (st.out < 0 && !cr_batch && !cr_done) {  // the root on these rows (X_v into per_vertex)
+          c->stats[3] += dev::launch_root(elem, A, ldA, Wa, Nn, ldN, c->d_comp, nr, c->d_partials, c->n_partials, pv,
+                                          c->d_result, c->s_main);
+        } else if (st.out < 0) {
+          // X_v came from the combine's epilogue (fused mode 3)
+        } else if (st.a == 1) {
+          TB[st.out] = Nn;  // the lift is the neighbour sum itself
+        } else if (s2 == fuse_cr &&
+                   (cr_batch = dev::launch_combine_root(elem, A, ldA, Wa, Nn, ldN, Wp, c->d_ztab[s2], c->zblocks[s2],
+                                                        (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1,
+                                                        c->d_comp, nr, pv, c->knobs, c->num_sms, c->s_main) > 0)) {
+          c->stats[3] += 1;
+          c->stats[5] = 3;
+        } else {
+          const int ob = bufs.make((size_t)nr * ldT * elem);
+          batch_bufs.push_back(ob);
+          TB[st.out] = bufs.ptr(ob);
+          c->stats[3] += dev::launch_combine(elem, A, ldA, Wa, Nn, ldN, Wp, c->d_split[s2],
+                                             (int)binom(st.t - 1, st.a - 1), nr, bufs.ptr(ob), ldT, Wt, c->d_ztab[s2],
+                                             c->zblocks[s2], (int)zblock_ld(st.t - 1, st.a - 1), st.t - 1, st.a - 1,
+                                             c->knobs, c->num_sms, c->s_main);
+        }
+        c->check_launch();
+        c->end(st.out < 0 ? PH_ROOT : PH_COMBINE, c->s_main, e);
+        c->stats[1] += (double)nr * (Wa + Wp + (st.out < 0 ? 1 : Wt)) * elem;
+      }
+      for (int bb : batch_bufs) bufs.unref(bb);
+    }
+    // X = sum of X_v over every row, in a fixed order
+    cudaEvent_t e = c->begin(c->s_main);
+    c->stats[3] += dev::launch_root(8, nullptr, 0, 0, per_vertex, 1, nullptr, n, c->d_partials, c->n_partials,
+                                    nullptr, c->d_result, c->s_main);
+    c->check_launch();
+    c->end(PH_ROOT, c->s_main, e);
   }
   if (c->pworld() > 1) {
     cudaEvent_t b = c->begin(c->s_main);

@@ -438,7 +438,7 @@ __device__ __forceinline__ void root_epilogue(const GatherArgs &a, AccT *sacc, i
 template <int NV, int VW, int G>
 __device__ __forceinline__ void expand(const GatherArgs &a, int cu, int cv, int c0, double (&acc)[NV][VW],
                                        double *sacc) {
-  const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
+  const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int y0 = c0 + j * G * VW;
@@ -645,13 +645,14 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
   extern __shared__ __align__(16) unsigned char sacc_raw[];
   const int lane = threadIdx.x & 31;
   AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)a.W_out;
-  const int64_t n_items = a.work.n_seg + a.work.n_light;
+  const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const char *__restrict__ srcb = static_cast<const char *>(a.src);
   const uint32_t ld_bytes = (uint32_t)(a.ld_src * sizeof(T));
+  const int vbase = a.col_base / VW;  // absolute 16-byte vector index of the chunk's first column
   // (L2 evict-last hints for hub rows measured neutral here: plain loads)
 
-  int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t it = a.item_from + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   int4 dx = make_int4(0, 0, 0, 0), dy = make_int4(0, 0, 0, 0);
   int go_n = 0;
   if (it < n_items) load_desc(a, it, lane, dx, dy, go_n);
@@ -690,13 +691,15 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
             use[j] = valid[j];
-            if (a.skip && valid[j])
-              use[j] = !((__ldg(a.skip + (int64_t)cvu * a.skip_words + ch * NV + j) >> lane) & 1u);
+            if (a.skip && valid[j]) {
+              const int vi = vbase + (ch * NV + j) * 32 + lane;  // the lane's vector of the row
+              use[j] = !((__ldg(a.skip + (int64_t)cvu * a.skip_words + (vi >> 5)) >> (vi & 31)) & 1u);
+            }
           }
         }
         // colour-pair map of this group, for the lane's columns
         uint16_t m[NV][VW];
-        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
+        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
           if (valid[j]) {
@@ -833,13 +836,13 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
           for (int j = 0; j < NV; ++j) {
             use[j] = valid[j];
             if (a.skip && valid[j]) {
-              const int vi = c0 / VW + j * G;  // the lane's 16-byte vector of the row
+              const int vi = (a.col_base + c0) / VW + j * G;  // the lane's 16-byte vector of the row
               use[j] = !((__ldg(a.skip + (int64_t)cvu * a.skip_words + (vi >> 5)) >> (vi & 31)) & 1u);
             }
           }
         }
         uint16_t m[NV][VW];
-        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
+        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
           if (valid[j] && rs == j % RG) {
@@ -999,19 +1002,27 @@ int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t
   }
   // narrow rows: long lists (items before a.item_split) on warp-per-item
   // row-parallel loads, the short tail on sub-warp rings
-  if (kn.narrow_impl == 4 && wvec <= 16 && a.item_to < 0) {
+  if (kn.narrow_impl == 4 && wvec <= 16) {
+    const int64_t from = a.item_from, to = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
+    const int64_t split = std::min(std::max(a.item_split, from), to);
     GatherArgs h = a, t = a;
-    h.item_to = a.item_split;
-    t.item_from = a.item_split;
-    t.item_to = a.work.n_seg + a.work.n_light;
+    h.item_from = from;
+    h.item_to = split;
+    t.item_from = split;
+    t.item_to = to;
     int launches = 0;
-    if (h.item_to > 0) {
+    if (h.item_from < h.item_to) {
       if (wvec <= 4) rows_go<T, 4, 1, 4>(h, kn, num_sms, s);
       else if (wvec <= 8) rows_go<T, 8, 1, 4>(h, kn, num_sms, s);
       else rows_go<T, 8, 2, 4>(h, kn, num_sms, s);
       ++launches;
     }
-    if (t.item_from < t.item_to) launches += gather_typed<T>(t, kn, num_sms, s);
+    if (t.item_from < t.item_to) {
+      if (wvec <= 4) ring_go<T, 4, 1, 4, 3>(t, kn, num_sms, s);
+      else if (wvec <= 8) ring_go<T, 8, 1, 4, 2>(t, kn, num_sms, s);
+      else ring_go<T, 8, 2, 4, 3>(t, kn, num_sms, s);
+      ++launches;
+    }
     return launches;
   }
   if (kn.narrow_impl >= 1 && kn.narrow_impl <= 3 && wvec <= 16) {

@@ -64,7 +64,7 @@ template <typename T, int V>
 __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_t ldA, int WA,
                                                  const T *__restrict__ N, int64_t ldN, int WN,
                                                  const uint32_t *__restrict__ split, int nq, int64_t n,
-                                                 T *__restrict__ out, int64_t ldO, int WO) {
+                                                 T *__restrict__ out, int64_t ldO, int WO, int o_lo, int o_hi) {
   using VT = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   static_assert(V % VW == 0, "tile must be a multiple of the vector width");
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_
       Ns[y * SV + r] = r < nv ? N[(v0 + r) * ldN + y] : (T)0;
     }
     __syncthreads();
-    for (int s = threadIdx.x; s < WO; s += blockDim.x) {
+    for (int s = o_lo + threadIdx.x; s < o_hi; s += blockDim.x) {
       T acc[V];
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] = (T)0;
@@ -517,35 +517,39 @@ __global__ void k_reduce(const double *__restrict__ partials, int np, double *__
 
 // ------------------------------------------------------------------ pack
 template <typename T>
-__global__ void __launch_bounds__(256) k_pack(const T *__restrict__ src, int64_t ld, const int32_t *__restrict__ idx,
-                                              int64_t rows, T *__restrict__ out) {
+__global__ void __launch_bounds__(256) k_pack(const T *__restrict__ src, int64_t ld, int64_t c0, int64_t w,
+                                              const int32_t *__restrict__ idx, int64_t rows, T *__restrict__ out,
+                                              int64_t ldo) {
   using VT = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
-  const int64_t nvec = ld / VW;
+  const int64_t nvec = w / VW;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < rows; i += nwarps) {
-    const VT *s = reinterpret_cast<const VT *>(src + (int64_t)idx[i] * ld);
-    VT *o = reinterpret_cast<VT *>(out + i * ld);
-    for (int64_t j = lane; j < nvec; j += 32) o[j] = s[j];
+    const VT *s = reinterpret_cast<const VT *>(src + (int64_t)idx[i] * ld + c0);
+    VT *o = reinterpret_cast<VT *>(out + i * ldo);
+    for (int64_t j = lane; j < nvec; j += 32) o[j] = __ldg(s + j);
   }
 }
 
 template <typename T, int V>
 void combine_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
-                int nq, int64_t n, void *out, int64_t ldO, int WO, int num_sms, cudaStream_t s) {
+                int nq, int64_t n, void *out, int64_t ldO, int WO, int o_lo, int o_hi, int num_sms, cudaStream_t s) {
   auto kern = k_combine<T, V>;
   const size_t smem = (size_t)(V == Vec<T>::W ? V : V + Vec<T>::W) * (WA + WN) * sizeof(T);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int threads = std::min(256, (WO + 31) / 32 * 32);  // one thread per output column
+  const int threads = std::min(256, (o_hi - o_lo + 31) / 32 * 32);  // one thread per output column
   const int grid = persistent_grid(kern, threads, smem, num_sms);
   kern<<<grid, threads, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq,
-                                   n, static_cast<T *>(out), ldO, WO);
+                                   n, static_cast<T *>(out), ldO, WO, o_lo, o_hi);
 }
 
+// Output colour sets [o_lo, o_hi) only (a column chunk of the output table;
+// out is then the chunk's virtual base: column o of row v at out[v * ldO + o]).
 template <typename T>
 int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint32_t *split,
-                   int nq, int64_t n, void *out, int64_t ldO, int WO, const Knobs &kn, int num_sms, cudaStream_t s) {
+                   int nq, int64_t n, void *out, int64_t ldO, int WO, int o_lo, int o_hi, const Knobs &kn,
+                   int num_sms, cudaStream_t s) {
   const size_t split_bytes = (size_t)nq * ((WO + 7) & ~7) * 4;
   const size_t cap = 227 * 1024;
   // V = 2 vertices per lane (one address per 2 FMAs, single-buffered
@@ -564,10 +568,10 @@ int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN
   // split walk does enough FMAs per staged entry (measured: (9;6,3) of
   // config 3 at 11.7 FMA/entry wins, config 2's (7;4,3) at 6.7 and (4;3,1)
   // at 2.1 lose)
-  const double intensity = (double)WO * nq / (double)(WA + WN + WO);
+  const double intensity = (double)(o_hi - o_lo) * nq / (double)(WA + WN + (o_hi - o_lo));
   const bool lane_ok = kn.combine_impl >= 2 ? kn.combine_impl == 2 : intensity >= 8.0;
   if (lane_ok && chunk > 0) {
-    const int WOcp = (std::min(chunk, WO) + 7) & ~7;
+    const int WOcp = (std::min(chunk, o_hi - o_lo) + 7) & ~7;
     const size_t smem = nbuf * tile_bytes + (size_t)nq * WOcp * 4;
     // 16 warps; output groups of 4 or 8 colour sets, whichever balances the warps better
     const int r8 = ((WOcp + 7) / 8 + 15) / 16, r4 = ((WOcp + 3) / 4 + 15) / 16;
@@ -577,20 +581,20 @@ int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = persistent_grid(kern, 512, smem, num_sms);
     int launches = 0;
-    for (int o0 = 0; o0 < WO; o0 += chunk, ++launches)
+    for (int o0 = o_lo; o0 < o_hi; o0 += chunk, ++launches)
       kern<<<grid, 512, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq,
-                                   n, static_cast<T *>(out), ldO, WO, nbuf, o0, std::min(chunk, WO - o0));
+                                   n, static_cast<T *>(out), ldO, WO, nbuf, o0, std::min(chunk, o_hi - o0));
     return launches;
   }
   // wide rows: tile of V vertices (padded rows); k <= 16 bounds a row by
   // 2 x C(15,7) entries, so the smallest tile always fits in 227 KB
   const size_t row = (size_t)(WA + WN) * sizeof(T);
   const size_t budget = 100 * 1024;
-  if (row * 20 <= budget) { combine_go<T, 16>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s); return 1; }
-  else if (row * 12 <= budget) { combine_go<T, 8>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s); return 1; }
+  if (row * 20 <= budget) { combine_go<T, 16>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, o_lo, o_hi, num_sms, s); return 1; }
+  else if (row * 12 <= budget) { combine_go<T, 8>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, o_lo, o_hi, num_sms, s); return 1; }
   else if (sizeof(T) == 4 || row * 6 <= 220 * 1024)
-    combine_go<T, 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
-  else combine_go<T, sizeof(T) == 8 ? 2 : 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, num_sms, s);
+    combine_go<T, 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, o_lo, o_hi, num_sms, s);
+  else combine_go<T, sizeof(T) == 8 ? 2 : 4>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, o_lo, o_hi, num_sms, s);
   return 1;
 }
 
@@ -673,8 +677,18 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
     else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     if (l) return l;
   }
-  if (elem == 8) return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, kn, num_sms, s);
-  return combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, kn, num_sms, s);
+  if (elem == 8)
+    return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, 0, WO, kn, num_sms, s);
+  return combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, 0, WO, kn, num_sms, s);
+}
+
+int launch_combine_cols(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
+                        const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, int o_lo, int o_hi,
+                        const Knobs &kn, int num_sms, cudaStream_t s) {
+  if (n == 0 || o_lo >= o_hi) return 0;
+  if (elem == 8)
+    return combine_typed<double>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, o_lo, o_hi, kn, num_sms, s);
+  return combine_typed<float>(A, ldA, WA, N, ldN, WN, split, nq, n, out, ldO, WO, o_lo, o_hi, kn, num_sms, s);
 }
 
 int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, const uint16_t *comp,
@@ -703,13 +717,16 @@ int launch_rowsum(int elem, const void *R, int64_t ld, int W, int64_t n, double 
   return 2;
 }
 
-int launch_pack(int elem, const void *src, int64_t ld, const int32_t *idx, int64_t rows, void *out, cudaStream_t s) {
-  if (rows == 0) return 0;
+int launch_pack(int elem, const void *src, int64_t ld, int64_t c0, int64_t w, const int32_t *idx, int64_t rows,
+                void *out, int64_t ldo, cudaStream_t s) {
+  if (rows == 0 || w == 0) return 0;
   const int grid = (int)std::min<int64_t>((rows + 7) / 8, 148 * 8);
   if (elem == 8)
-    k_pack<double><<<grid, 256, 0, s>>>(static_cast<const double *>(src), ld, idx, rows, static_cast<double *>(out));
+    k_pack<double><<<grid, 256, 0, s>>>(static_cast<const double *>(src), ld, c0, w, idx, rows,
+                                        static_cast<double *>(out), ldo);
   else
-    k_pack<float><<<grid, 256, 0, s>>>(static_cast<const float *>(src), ld, idx, rows, static_cast<float *>(out));
+    k_pack<float><<<grid, 256, 0, s>>>(static_cast<const float *>(src), ld, c0, w, idx, rows,
+                                       static_cast<float *>(out), ldo);
   return 1;
 }
 

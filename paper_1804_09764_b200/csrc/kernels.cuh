@@ -34,6 +34,9 @@ struct Knobs {
   int hub_l2_pct = 50;     // CC_HUB_L2_PCT: % of the L2 given an evict-last policy for hub rows (rings)
   int grid_reserve = -1;   // CC_GRID_RESERVE: SMs left free for NCCL while an exchange is in flight
                            //                  (-1 = auto: 8 when world > 1 over NCCL, else 0)
+  int tail_batches = 0;    // CC_TAIL_BATCHES: > 0 forces the memory plan's row batches (0 = by memory)
+  int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
+                                //   per batch in column chunks of this width (0 = by memory)
 };
 
 // Work list of one aggregation pass (Alg. 4: the
@@ -73,11 +76,12 @@ struct GatherArgs {
   const uint16_t *goff;   // per item: 16 cumulative colour-group end offsets (relative to item begin)
   const ItemDesc *desc;   // per item descriptor (bulk gather)
   const uint8_t *colors;  // colour of every row (owned | halo)
-  const void *src;        // passive table P' (rows x ld_src), W_in = C(k-1, p-1) valid columns
-  int64_t ld_src;
+  const void *src;        // passive table P' (rows x ld_src): columns [col_base, col_base + W_in) of
+  int64_t ld_src;         // the compressed rows (C(k-1, p-1) in all), src pointing at column col_base
   int W_in;
-  int64_t item_from = 0;  // narrow-row kernels: this launch takes items [item_from, item_to)
-  int64_t item_to = -1;   // (-1: all items)
+  int col_base = 0;       // column chunk: absolute index of src's first column, a multiple of 8
+  int64_t item_from = 0;  // this launch takes items [item_from, item_to) (a row batch, or the
+  int64_t item_to = -1;   // narrow kernels' split of the list); -1: all items
   int64_t item_split = 0; // first light item with <= 32 neighbours (items are in degree order)
   const uint16_t *map;    // [c_u][c_v][map_ld] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
   int64_t map_ld;         // map row stride (multiple of 8 entries, padding = 0xFFFF)
@@ -130,6 +134,12 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
                    int nblocks, int zld, int ts, int as, const Knobs &kn, int num_sms, cudaStream_t s);
 bool combine_z_supported(int elem, int ts, int as);
+// The combine restricted to the output columns [o_lo, o_hi) (a column chunk
+// of the output table): out is the chunk's virtual base (column o
+// of row v at out[v * ldO + o]); lane or V-tile kernel.
+int launch_combine_cols(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
+                        const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, int o_lo, int o_hi,
+                        const Knobs &kn, int num_sms, cudaStream_t s);
 // The last combine fused with the root step that shares its passive table:
 // X_v = sum_{X'} T'(v, X') N''(v, comp X') into per_vertex[v] (fp64), T'
 // never stored.  Returns 0 (nothing launched) when the shape has no
@@ -147,9 +157,10 @@ int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int
 // than colours), per-vertex sums into per_vertex (nullable), result[0].
 int launch_rowsum(int elem, const void *R, int64_t ld, int W, int64_t n, double *partials, int n_partials,
                   double *per_vertex, double *result, cudaStream_t s);
-// Halo pack: out[i, :] = src[idx[i], :] for i < rows (whole padded rows).
-int launch_pack(int elem, const void *src, int64_t ld, const int32_t *idx, int64_t rows, void *out,
-                cudaStream_t s);
+// Halo pack: out[i, 0:w) = src[idx[i], c0:c0+w) for i < rows (row strides ld / ldo;
+// c0, w and both strides multiples of the 16-byte vector).
+int launch_pack(int elem, const void *src, int64_t ld, int64_t c0, int64_t w, const int32_t *idx, int64_t rows,
+                void *out, int64_t ldo, cudaStream_t s);
 
 int root_partials_blocks(int num_sms);  // grid size used by launch_root partials
 

@@ -539,7 +539,7 @@ def test_errors_are_reported():
 def test_options_and_hooks_are_validated():
     cc = lib()
     with pytest.raises(cc.CCError) as e:
-        cc.cc_create(device=0, chunk_cols=64)  # reserved: must be 0
+        cc.cc_create(device=0, chunk_cols=-1)  # >= 0
     assert e.value.status == cc.CC_ERR_ARG
     with pytest.raises(cc.CCError) as e:
         cc.cc_create(device=0, replicas=2)
