@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(256) k_pack(const T *__restrict__ src, int64_t
   constexpr int VW = Vec<T>::W;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
-  const int64_t nvec = w / VW;
+  const int64_t nvec = (w + VW - 1) / VW;  // a ragged chunk's last vector reads the row's padding
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < rows; i += nwarps) {
     const VT *s = reinterpret_cast<const VT *>(src + (int64_t)idx[i] * ld + c0);
     VT *o = reinterpret_cast<VT *>(out + i * ldo);

@@ -158,7 +158,8 @@ int launch_root(int elem, const void *A, int64_t ldA, int WA, const void *N, int
 int launch_rowsum(int elem, const void *R, int64_t ld, int W, int64_t n, double *partials, int n_partials,
                   double *per_vertex, double *result, cudaStream_t s);
 // Halo pack: out[i, 0:w) = src[idx[i], c0:c0+w) for i < rows (row strides ld / ldo;
-// c0, w and both strides multiples of the 16-byte vector).
+// c0 and both strides multiples of the 16-byte vector; a ragged w is rounded
+// up to whole vectors, reading the source row's padding).
 int launch_pack(int elem, const void *src, int64_t ld, int64_t c0, int64_t w, const int32_t *idx, int64_t rows,
                 void *out, int64_t ldo, cudaStream_t s);
 

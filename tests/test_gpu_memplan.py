@@ -52,7 +52,7 @@ def test_column_chunks_equal_the_oracle(ci, scale, ef):
         if float(want.total) < 2.0 ** 53:
             assert x == base
         assert_close_entries(root[:, 0], want.root, TOL_FP64, f"chunked root X_v ci={ci} w={w}")
-        if w < 64:
+        if w < 64 and ci > 1:  # (configs[1]'s passive rows have <= 15 columns)
             assert st["column_chunks"] > 0
         x32 = count(g, cfg.parent, colors=col, precision="fp32", chunk_cols=w)
         assert rel_err(x32, float(want.total)) <= TOL_FP32, (ci, w)
