@@ -59,6 +59,8 @@ def _load():
         lib.or_dp_count.argtypes = [i64, vp, vp, i32, vp, vp, i32, i32, vp, vp, vp, vp, vp]
         lib.or_dp_count_kc.restype = ctypes.c_int
         lib.or_dp_count_kc.argtypes = [i64, vp, vp, i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]
+        lib.or_dp_root_at.restype = ctypes.c_int
+        lib.or_dp_root_at.argtypes = [i64, vp, vp, i32, vp, vp, i32, i64, vp, vp, vp]
         lib.or_estimate.restype = ctypes.c_double
         lib.or_estimate.argtypes = [i32, vp, i32, u64]
         lib.or_mom.restype = ctypes.c_double
@@ -173,6 +175,24 @@ def dp_count(g, parent, colors, numtype=NUM_EXACT, keep_x=-1, want_root=False, c
     if numtype == NUM_EXACT:
         return DPResult((hi.value << 64) | lo.value, True, table, root)
     return DPResult(float(ld.value), False, table, root)
+
+
+def dp_root_at(g, parent, colors, v0: int, numtype=NUM_EXACT):
+    """D_root(v0, [k]): the DP's per-vertex root count at ONE vertex (each
+    template vertex's table evaluated only within its depth of v0)."""
+    par = _parent(parent)
+    k = len(par)
+    col = np.ascontiguousarray(colors, dtype=np.uint8)
+    assert col.size == g.n
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    ld = ctypes.c_longdouble()
+    rc = _load().or_dp_root_at(g.n, _ptr(g.row_ptr), _ptr(g.col), k, par.ctypes.data, _ptr(col), numtype, int(v0),
+                               ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(ld))
+    if rc == 2:
+        raise OverflowError("oracle DP overflowed the exact u128 type")
+    if rc:
+        raise OracleError(f"or_dp_root_at rc={rc}")
+    return (hi.value << 64) | lo.value if numtype == NUM_EXACT else float(ld.value)
 
 
 def estimate(X, k: int, aut_t: int) -> float:

@@ -23,6 +23,11 @@
  *                    over disjoint S, Y ("S = S1 u S2").
  *                    X = sum_v D_root(v, [k])   (Eq. 3 without the k^k/k!
  *                    scale).
+ *   or_dp_root_at  : or_dp_count's DP at one root vertex v0 (its tables
+ *                    evaluated only within each template vertex's depth of
+ *                    v0): the summand X_v0 of Eq. 3, for sampled outputs of
+ *                    graphs too large for the whole DP (pinned: sum over v0
+ *                    = brute force, and = or_dp_count's per-vertex root).
  *   or_color       : reading C-2 (SplitMix64 finaliser; PAPER.md lines
  *                    156-158 only say "uniformly at random").
  *   or_estimate    : mean_j X_j * k^k/k! / |Aut(T)| (PAPER.md lines 146-147,
@@ -79,6 +84,7 @@ typedef struct {
   int child[16][16]; /* children in increasing index order */
   int size[16];      /* subtree size */
   int post[16];      /* post-order (children before parent) */
+  int depth[16];     /* distance from the root */
   int bfs[16];       /* BFS order from the root */
 } tmpl;
 
@@ -110,6 +116,7 @@ static int tmpl_init(tmpl *t, int k, const int32_t *parent) {
     }
   }
   if (tail != k) return OR_EARG; /* a cycle in the parent pointers */
+  for (int i = 1; i < k; ++i) t->depth[t->bfs[i]] = t->depth[t->parent[t->bfs[i]]] + 1;
   /* post-order = reverse BFS works as "children before parent" */
   for (int i = 0; i < k; ++i) t->post[i] = t->bfs[k - 1 - i];
   for (int i = 0; i < k; ++i) t->size[i] = 1;
@@ -295,10 +302,10 @@ int or_combine_row(int32_t k, int32_t a, int32_t p, const double *A, const doubl
  *   out_table (n x C(k, size_x), colex order; as double), or -1.
  * out_root: if non-NULL, per-vertex D_root(v, [k]) as double (n entries).
  * Total X: exact in (out_lo, out_hi) for numtype 0; as long double in *out_ld. */
-int or_dp_count_kc(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
-                   const int32_t *parent, const uint8_t *colors, int32_t kc, int32_t numtype,
-                   int32_t keep_x, double *out_table, double *out_root,
-                   uint64_t *out_lo, uint64_t *out_hi, long double *out_ld) {
+static int dp_dispatch(int64_t n, const int64_t *rp, const int32_t *col, int32_t k, const int32_t *parent,
+                       const uint8_t *colors, int32_t kc, int32_t numtype, int32_t keep_x, double *out_table,
+                       double *out_root, uint64_t *out_lo, uint64_t *out_hi, long double *out_ld,
+                       const int32_t *dist) {
   tmpl t;
   int rc = tmpl_init(&t, k, parent);
   if (rc) return rc;
@@ -310,19 +317,19 @@ int or_dp_count_kc(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
   switch (numtype) {
     case 0: {
       u128 tot = 0;
-      rc = dp_u128(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot);
+      rc = dp_u128(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot, dist);
       if (!rc) { *out_lo = (uint64_t)tot; *out_hi = (uint64_t)(tot >> 64); if (out_ld) *out_ld = (long double)tot; }
       break;
     }
     case 1: {
       long double tot = 0;
-      rc = dp_ld(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot);
+      rc = dp_ld(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot, dist);
       if (!rc && out_ld) *out_ld = tot;
       break;
     }
     case 2: {
       double tot = 0;
-      rc = dp_f64(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot);
+      rc = dp_f64(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot, dist);
       if (!rc && out_ld) *out_ld = (long double)tot;
       break;
     }
@@ -330,6 +337,45 @@ int or_dp_count_kc(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
       rc = OR_EARG;
   }
   subsets_free(&ss);
+  return rc;
+}
+
+int or_dp_count_kc(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
+                   const int32_t *parent, const uint8_t *colors, int32_t kc, int32_t numtype,
+                   int32_t keep_x, double *out_table, double *out_root,
+                   uint64_t *out_lo, uint64_t *out_hi, long double *out_ld) {
+  return dp_dispatch(n, rp, col, k, parent, colors, kc, numtype, keep_x, out_table, out_root, out_lo, out_hi, out_ld,
+                     NULL);
+}
+
+/* The root's count at ONE vertex v0, D_root(v0, [k]) (the summand of Eq. 3
+ * at v0): the same DP, each template vertex's table evaluated only within
+ * its depth of v0 (BFS distance), so that large graphs cost only the ball of
+ * radius height(T) around v0.  Exact total in (out_lo, out_hi) for numtype 0,
+ * else *out_ld. */
+int or_dp_root_at(int64_t n, const int64_t *rp, const int32_t *col, int32_t k, const int32_t *parent,
+                  const uint8_t *colors, int32_t numtype, int64_t v0, uint64_t *out_lo, uint64_t *out_hi,
+                  long double *out_ld) {
+  if (v0 < 0 || v0 >= n) return OR_EARG;
+  int32_t *dist = (int32_t *)malloc((size_t)(n + 1) * sizeof(int32_t));
+  int64_t *queue = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
+  if (!dist || !queue) { free(dist); free(queue); return OR_ENOMEM; }
+  for (int64_t v = 0; v < n; ++v) dist[v] = 1 << 30;
+  int64_t head = 0, tail = 0;
+  dist[v0] = 0;
+  queue[tail++] = v0;
+  while (head < tail) {
+    const int64_t v = queue[head++];
+    if (dist[v] >= k) continue;  /* deeper than any template vertex */
+    for (int64_t e = rp[v]; e < rp[v + 1]; ++e)
+      if (dist[col[e]] > dist[v] + 1) {
+        dist[col[e]] = dist[v] + 1;
+        queue[tail++] = col[e];
+      }
+  }
+  free(queue);
+  const int rc = dp_dispatch(n, rp, col, k, parent, colors, k, numtype, -1, NULL, NULL, out_lo, out_hi, out_ld, dist);
+  free(dist);
   return rc;
 }
 

@@ -96,3 +96,62 @@ def test_config4_full_size_one_gpu_sampled_rows(graph4):
         if (~zero).any():
             err = np.max(np.abs(rows[i][~zero] - ref[~zero]) / ref[~zero])
             assert err <= TOL_FP32, f"v={v}: max rel err {err:.3e}"
+
+
+def test_config4_template_on_the_clique_every_table_entry():
+    """SURVEY 8(c) pin "Clique K_n, every table entry" with configs[4]'s own
+    template (15-vertex perfect binary tree, k = 15) on K_2000 (4 M adjacency
+    entries): D_x(v, S) = [c_v in S] (s - 1)! prod_{j in S, j != c_v} cnt_j
+    for every template vertex x (subtree size s in {1, 3, 7}) and every S,
+    and the root X_v = [k]'s entry; fp64 within 1e-12 per entry, fp32 X
+    within 1e-4.  The fused root (self dot, mode 2) is on."""
+    import itertools
+    cc = lib()
+    cfg = synth.CONFIGS[4]
+    k, n = cfg.k, 2000
+    g = synth.clique(n)
+    col = oracle.color(n, k, 13)
+    cnt = np.bincount(col, minlength=k).astype(np.float64)
+
+    def closed(S, v):
+        if col[v] not in S:
+            return 0.0
+        return math.factorial(len(S) - 1) * math.prod(cnt[j] - (j == col[v]) for j in S if j != col[v])
+
+    verts = [0, 1, 777, 1999]
+    with context(g, cfg.parent) as ctx:
+        cc.cc_set_colors(ctx, col)
+        x = cc.cc_count_colorful(ctx)
+        assert cc.cc_last_stats(ctx)["fused_root"] == 2
+        assert abs(x - math.factorial(k) * float(np.prod(cnt))) <= 1e-12 * x
+        for xv, s in ((1, 7), (3, 3), (7, 1), (0, 15)):
+            rows = cc.cc_get_subtree_rows(ctx, xv, verts, k, s)
+            subsets = sorted(itertools.combinations(range(k), s), key=lambda t: t[::-1])
+            for i, v in enumerate(verts):
+                want = np.array([closed(S, v) for S in subsets])
+                got = rows[i]
+                assert np.all(got[want == 0] == 0), (xv, v)
+                nz = want != 0
+                assert np.max(np.abs(got[nz] - want[nz]) / want[nz]) <= 1e-12, (xv, v)
+    with context(g, cfg.parent, "fp32") as ctx:
+        cc.cc_set_colors(ctx, col)
+        x32 = cc.cc_count_colorful(ctx)
+    assert abs(x32 - math.factorial(k) * float(np.prod(cnt))) <= TOL_FP32 * x32
+
+
+def test_star_closed_form_full_config4_graph(graph4):
+    """SURVEY 8(c) star pin at full configs[4] scale (2.0 B adjacency
+    entries, hubs of ~1 M neighbours): X(star with k-1 leaves) =
+    (k-1)! sum_v prod_{j != c_v} cnt_j(v), k = 8, fp64 within 1e-12."""
+    g = graph4
+    k = 8
+    col = oracle.color(g.n, k, 21)
+    deg = g.degrees()
+    src = np.repeat(np.arange(g.n, dtype=np.int64), deg)
+    cnt = np.bincount(src * k + col[g.col], minlength=g.n * k).reshape(g.n, k).astype(np.float64)
+    del src
+    cnt[np.arange(g.n), col] = 1.0
+    want = math.factorial(k - 1) * float(np.sum(np.prod(cnt, axis=1) * (deg > 0)))
+    from gpu_util import count
+    got = count(g, [-1] + [0] * (k - 1), seed=21, precision="fp64")
+    assert abs(got - want) <= 1e-12 * want, (got, want)

@@ -327,16 +327,29 @@ def test_config_twins_fp32_total(ci, scale, ef):
 
 
 # ------------------------------------------------------------------ configs[2] at full size
-def test_config2_full_fp32_two_colourings():
+def test_config2_full_fp32_ten_colourings_one_and_two_ranks():
+    """BASELINE.json configs[2] as specified: R-MAT scale 20, the 10-vertex
+    spider, k = 10, fp32 tables with fp64 root, the 10 colourings of seeds
+    2..11 (reading C-2), on one GPU and with the 1D partition over 2 ranks
+    (loopback transport on this GPU; grouped exchange, whole-row and chunked
+    halo rows): every X_j within 1e-4 of the oracle's fold-children DP."""
+    from test_gpu_loopback import run_ranks
     cfg = synth.CONFIGS[2]
     g = cfg.graph()
     cc = lib()
+    want = [float(oracle.dp_count(g, cfg.parent, oracle.color(g.n, cfg.k, cfg.color_seed + j), oracle.NUM_DOUBLE).total)
+            for j in range(10)]
     with context(g, cfg.parent, "fp32") as ctx:
-        for seed in (cfg.color_seed, cfg.color_seed + 1):
-            cc.cc_color(ctx, seed)
-            x = cc.cc_count_colorful(ctx)
-            want = oracle.dp_count(g, cfg.parent, oracle.color(g.n, cfg.k, seed), oracle.NUM_DOUBLE).total
-            assert rel_err(x, want) <= TOL_FP32, seed
+        _, xs = cc.cc_estimate(ctx, 10, cfg.color_seed, per_iter=True)
+    for j in range(10):
+        assert rel_err(xs[j], want[j]) <= TOL_FP32, (j, xs[j], want[j])
+    for chunk in (0, 64):
+        out, _ = run_ranks(g, cfg.parent, 2, precision="fp32", estimate=(10, cfg.color_seed), exchange=1,
+                           chunk_cols=chunk)
+        for r in range(2):
+            est, xr = out[r]
+            for j in range(10):
+                assert rel_err(xr[j], want[j]) <= TOL_FP32, (chunk, r, j, xr[j], want[j])
 
 
 def test_config3_full_size_fp32_vs_oracle():

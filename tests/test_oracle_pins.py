@@ -407,3 +407,54 @@ def test_more_colours_sum_over_all_colourings():
     for col in itertools.product(range(kc), repeat=g.n):
         total += oracle.dp_count(g, parent, np.array(col, np.uint8), colours=kc).total
     assert total == math.perm(kc, k) * kc ** (g.n - k) * maps
+
+
+# ---------------------------------------------------------------- the root count at one vertex
+def test_dp_root_at_sums_to_brute_force_and_equals_the_dp_root_row():
+    """or_dp_root_at (the DP evaluated only within each template vertex's
+    depth of v0): summed over every v0 it is the brute force of the
+    definition -- the pin independent of the
+    DP -- and at each v0 it is the full DP's per-vertex root D_root(v0, [k]);
+    also on the subgraph induced by the ball of radius height(T) around v0
+    (the locality the full-size sampled checks rely on)."""
+    rng = np.random.default_rng(21)
+    for trial in range(40):
+        k = int(rng.integers(1, 8))
+        n = int(rng.integers(max(k, 2), 12))
+        g = synth.gnp(n, float(rng.choice([0.25, 0.5, 0.8])), int(rng.integers(1 << 30)))
+        parent = [-1] + [int(rng.integers(0, i)) for i in range(1, k)]
+        perm = rng.permutation(k)
+        relab = [-1] * k
+        for x in range(k):
+            relab[perm[x]] = -1 if parent[x] < 0 else int(perm[parent[x]])
+        col = rng.integers(0, k, n).astype(np.uint8)
+        per_v = [oracle.dp_root_at(g, relab, col, v) for v in range(n)]
+        assert sum(per_v) == oracle.brute_count(g, relab, col), (relab, per_v)
+        full = oracle.dp_count(g, relab, col, oracle.NUM_EXACT, want_root=True).root
+        assert [float(x) for x in per_v] == full.tolist()
+    # locality: the ball of radius height(T) around v0 carries the whole answer
+    g = synth.rmat(9, 8, seed=4)
+    for parent in (synth.CONFIGS[2].parent, synth.CONFIGS[4].parent):
+        k = len(parent)
+        depth = [0] * k
+        for x in range(k):
+            p = parent[x]
+            while p >= 0:
+                depth[x] += 1
+                p = parent[p]
+        h = max(depth)
+        col = oracle.color(g.n, k, 8)
+        full = oracle.dp_count(g, parent, col, oracle.NUM_EXACT, want_root=True).root
+        for v0 in (0, 5, 100, 300):
+            ball = {v0}
+            frontier = {v0}
+            for _ in range(h):
+                frontier = {int(u) for w in frontier for u in g.neighbors(w)} - ball
+                ball |= frontier
+            verts = np.array(sorted(ball))
+            idx = {int(v): i for i, v in enumerate(verts)}
+            edges = [(idx[int(v)], idx[int(u)]) for v in verts for u in g.neighbors(int(v)) if int(u) in idx and u > v]
+            sub = synth.from_edges(len(verts), edges)
+            got = oracle.dp_root_at(sub, parent, col[verts], idx[v0])
+            assert float(got) == full[v0], (parent, v0)
+            assert oracle.dp_root_at(g, parent, col, v0) == got
