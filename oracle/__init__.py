@@ -19,7 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRCS = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "dp_body.inc")]
+_SRCS = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "dp_body.inc"), os.path.join(_HERE, "dp_root_body.inc")]
 
 NUM_EXACT, NUM_LONGDOUBLE, NUM_DOUBLE = 0, 1, 2
 

@@ -279,6 +279,28 @@ static void subsets_free(subsets *ss) {
 #undef SFX
 #undef EXACT
 
+#define NUM u128
+#define SFX u128
+#define EXACT 1
+#include "dp_root_body.inc"
+#undef NUM
+#undef SFX
+#undef EXACT
+#define NUM long double
+#define SFX ld
+#define EXACT 0
+#include "dp_root_body.inc"
+#undef NUM
+#undef SFX
+#undef EXACT
+#define NUM double
+#define SFX f64
+#define EXACT 0
+#include "dp_root_body.inc"
+#undef NUM
+#undef SFX
+#undef EXACT
+
 /* One row of the combine step of Eq. 1 in double:
  *   T(S u Y) += A(S) * N(Y)  for |S| = a, |Y| = p, S and Y disjoint,
  * rows indexed by colex rank (= increasing-mask order).  Exposed so the
@@ -302,10 +324,10 @@ int or_combine_row(int32_t k, int32_t a, int32_t p, const double *A, const doubl
  *   out_table (n x C(k, size_x), colex order; as double), or -1.
  * out_root: if non-NULL, per-vertex D_root(v, [k]) as double (n entries).
  * Total X: exact in (out_lo, out_hi) for numtype 0; as long double in *out_ld. */
-static int dp_dispatch(int64_t n, const int64_t *rp, const int32_t *col, int32_t k, const int32_t *parent,
-                       const uint8_t *colors, int32_t kc, int32_t numtype, int32_t keep_x, double *out_table,
-                       double *out_root, uint64_t *out_lo, uint64_t *out_hi, long double *out_ld,
-                       const int32_t *dist) {
+int or_dp_count_kc(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
+                   const int32_t *parent, const uint8_t *colors, int32_t kc, int32_t numtype,
+                   int32_t keep_x, double *out_table, double *out_root,
+                   uint64_t *out_lo, uint64_t *out_hi, long double *out_ld) {
   tmpl t;
   int rc = tmpl_init(&t, k, parent);
   if (rc) return rc;
@@ -317,19 +339,19 @@ static int dp_dispatch(int64_t n, const int64_t *rp, const int32_t *col, int32_t
   switch (numtype) {
     case 0: {
       u128 tot = 0;
-      rc = dp_u128(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot, dist);
+      rc = dp_u128(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot);
       if (!rc) { *out_lo = (uint64_t)tot; *out_hi = (uint64_t)(tot >> 64); if (out_ld) *out_ld = (long double)tot; }
       break;
     }
     case 1: {
       long double tot = 0;
-      rc = dp_ld(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot, dist);
+      rc = dp_ld(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot);
       if (!rc && out_ld) *out_ld = tot;
       break;
     }
     case 2: {
       double tot = 0;
-      rc = dp_f64(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot, dist);
+      rc = dp_f64(&ss, &t, n, rp, col, colors, keep_x, out_table, out_root, &tot);
       if (!rc && out_ld) *out_ld = (long double)tot;
       break;
     }
@@ -340,42 +362,81 @@ static int dp_dispatch(int64_t n, const int64_t *rp, const int32_t *col, int32_t
   return rc;
 }
 
-int or_dp_count_kc(int64_t n, const int64_t *rp, const int32_t *col, int32_t k,
-                   const int32_t *parent, const uint8_t *colors, int32_t kc, int32_t numtype,
-                   int32_t keep_x, double *out_table, double *out_root,
-                   uint64_t *out_lo, uint64_t *out_hi, long double *out_ld) {
-  return dp_dispatch(n, rp, col, k, parent, colors, kc, numtype, keep_x, out_table, out_root, out_lo, out_hi, out_ld,
-                     NULL);
-}
-
 /* The root's count at ONE vertex v0, D_root(v0, [k]) (the summand of Eq. 3
- * at v0): the same DP, each template vertex's table evaluated only within
- * its depth of v0 (BFS distance), so that large graphs cost only the ball of
- * radius height(T) around v0.  Exact total in (out_lo, out_hi) for numtype 0,
- * else *out_ld. */
+ * at v0), for graphs too large for the whole DP: the same fold-children
+ * recurrence, where the table of a template vertex at depth d is kept only
+ * for the vertices within distance d of v0 -- exactly the rows the root at
+ * v0 reads (a child's row at u is read by its parent at a neighbour of u).
+ * Vertices are numbered in BFS order from v0, so those rows are a prefix.
+ * Exact total in (out_lo, out_hi) for numtype 0, else *out_ld. */
 int or_dp_root_at(int64_t n, const int64_t *rp, const int32_t *col, int32_t k, const int32_t *parent,
                   const uint8_t *colors, int32_t numtype, int64_t v0, uint64_t *out_lo, uint64_t *out_hi,
                   long double *out_ld) {
+  tmpl t;
+  int rc = tmpl_init(&t, k, parent);
+  if (rc) return rc;
   if (v0 < 0 || v0 >= n) return OR_EARG;
-  int32_t *dist = (int32_t *)malloc((size_t)(n + 1) * sizeof(int32_t));
-  int64_t *queue = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
-  if (!dist || !queue) { free(dist); free(queue); return OR_ENOMEM; }
-  for (int64_t v = 0; v < n; ++v) dist[v] = 1 << 30;
-  int64_t head = 0, tail = 0;
+  int h = 0;
+  for (int x = 0; x < k; ++x) h = t.depth[x] > h ? t.depth[x] : h;
+  /* BFS from v0 to depth h: queue order; end[d] = number of vertices within distance d */
+  int32_t *dist = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+  int32_t *qpos = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+  int64_t cap = 1024, len = 0;
+  int32_t *queue = (int32_t *)malloc((size_t)cap * sizeof(int32_t));
+  if (!dist || !qpos || !queue) { free(dist); free(qpos); free(queue); return OR_ENOMEM; }
+  for (int64_t v = 0; v < n; ++v) dist[v] = -1;
+  int64_t end[17] = {0};
   dist[v0] = 0;
-  queue[tail++] = v0;
-  while (head < tail) {
-    const int64_t v = queue[head++];
-    if (dist[v] >= k) continue;  /* deeper than any template vertex */
-    for (int64_t e = rp[v]; e < rp[v + 1]; ++e)
-      if (dist[col[e]] > dist[v] + 1) {
-        dist[col[e]] = dist[v] + 1;
-        queue[tail++] = col[e];
+  queue[len++] = (int32_t)v0;
+  for (int64_t head = 0; head < len; ++head) {
+    const int32_t v = queue[head];
+    if (dist[v] >= h) continue;
+    for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+      const int32_t u = col[e];
+      if (dist[u] >= 0) continue;
+      dist[u] = dist[v] + 1;
+      if (len == cap) {
+        cap *= 2;
+        int32_t *q2 = (int32_t *)realloc(queue, (size_t)cap * sizeof(int32_t));
+        if (!q2) { free(dist); free(qpos); free(queue); return OR_ENOMEM; }
+        queue = q2;
       }
+      queue[len++] = u;
+    }
   }
-  free(queue);
-  const int rc = dp_dispatch(n, rp, col, k, parent, colors, k, numtype, -1, NULL, NULL, out_lo, out_hi, out_ld, dist);
+  for (int64_t i = 0; i < len; ++i) {
+    qpos[queue[i]] = (int32_t)i;
+    end[dist[queue[i]]] = i + 1;
+  }
+  for (int d = 1; d <= h; ++d) if (end[d] < end[d - 1]) end[d] = end[d - 1];
+  subsets ss;
+  if (subsets_init(&ss, k)) { subsets_free(&ss); free(dist); free(qpos); free(queue); return OR_ENOMEM; }
+  switch (numtype) {
+    case 0: {
+      u128 x = 0;
+      rc = droot_u128(&ss, &t, rp, col, colors, queue, qpos, end, &x);
+      if (!rc) { *out_lo = (uint64_t)x; *out_hi = (uint64_t)(x >> 64); if (out_ld) *out_ld = (long double)x; }
+      break;
+    }
+    case 1: {
+      long double x = 0;
+      rc = droot_ld(&ss, &t, rp, col, colors, queue, qpos, end, &x);
+      if (!rc && out_ld) *out_ld = x;
+      break;
+    }
+    case 2: {
+      double x = 0;
+      rc = droot_f64(&ss, &t, rp, col, colors, queue, qpos, end, &x);
+      if (!rc && out_ld) *out_ld = (long double)x;
+      break;
+    }
+    default:
+      rc = OR_EARG;
+  }
+  subsets_free(&ss);
   free(dist);
+  free(qpos);
+  free(queue);
   return rc;
 }
 

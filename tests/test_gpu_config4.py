@@ -23,6 +23,13 @@ pytestmark = pytest.mark.gpu
 
 TOL_FP32 = 1e-4
 
+# k = 16: the root with two 7-vertex perfect binary subtrees and a leaf -- a
+# template whose 7-vertex subtree table alone (11.73 M rows x C(15, 6) fp32)
+# is 235 GB and whose neighbour sum is 302 GB: it runs on ONE GPU only
+# through the memory plan (row-batched tail, the subtree table recomputed per
+# batch in column chunks).
+PAR16 = [-1, 0, 0, 1, 1, 3, 3, 4, 4, 2, 2, 9, 9, 10, 10, 0]
+
 
 @pytest.fixture(scope="module")
 def graph4():
@@ -32,13 +39,19 @@ def graph4():
     return synth.CONFIGS[4].graph()
 
 
-def _ball2(g, v):
-    nb = g.neighbors(v)
-    verts = np.unique(np.concatenate([[v], nb] + [g.neighbors(int(u)) for u in nb]))
+def ball(g, v, r):
+    """Sorted vertex ids within distance r of v."""
+    verts = np.array([v], dtype=np.int64)
+    frontier = verts
+    for _ in range(r):
+        nxt = np.unique(np.concatenate([g.neighbors(int(u)) for u in frontier]))
+        frontier = np.setdiff1d(nxt, verts)
+        verts = np.union1d(verts, frontier)
     return verts
 
 
-def _induced(g, verts):
+def induced(g, verts):
+    """The subgraph induced by the sorted vertex ids `verts` (relabelled 0..)."""
     idx = -np.ones(g.n, dtype=np.int64)
     idx[verts] = np.arange(verts.size)
     eu, ev = [], []
@@ -86,8 +99,8 @@ def test_config4_full_size_one_gpu_sampled_rows(graph4):
     assert st["fused_root"] == 2
     col = oracle.color(g.n, k, seed)
     for i, v in enumerate(samples):
-        verts = _ball2(g, v)
-        sub = _induced(g, verts)
+        verts = ball(g, v, 2)
+        sub = induced(g, verts)
         pos = int(np.searchsorted(verts, v))
         ref = oracle.dp_count(sub, cfg.parent, col[verts], oracle.NUM_DOUBLE, keep_x=1).table[pos]
         assert ref.shape == rows[i].shape
