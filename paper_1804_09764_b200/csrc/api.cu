@@ -89,6 +89,7 @@ int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
   if (name == "hub_l2_pct") return &k.hub_l2_pct;
   if (name == "grid_reserve") return &k.grid_reserve;
   if (name == "tail_batches") return &k.tail_batches;
+  if (name == "layout") return &k.layout;
   if (name == "tail_recompute_cols") return &k.tail_recompute_cols;
   return nullptr;
 }
@@ -97,7 +98,7 @@ int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
 void knobs_from_env(cc::dev::Knobs &k) {
   static const char *names[] = {"fused_root", "sector_skip", "gather_impl", "narrow_impl", "narrow_split",
                                 "csort_small", "combine_impl", "acc32", "phase_events", "hub_l2_pct", "grid_reserve",
-                                "tail_batches", "tail_recompute_cols"};
+                                "tail_batches", "tail_recompute_cols", "layout"};
   for (const char *n : names) {
     std::string env = "CC_";
     for (const char *q = n; *q; ++q) env += (char)std::toupper((unsigned char)*q);
@@ -460,11 +461,12 @@ cc_status cc_get_subtree_counts(cc_ctx *c, int32_t x, double *out) {
     std::memset(out, 0, (size_t)c->n_global * Wd * sizeof(double));
     std::vector<uint32_t> sets((size_t)Wd);
     for (int64_t r = 0; r < Wd; ++r) sets[r] = cc::colex_unrank(s, r);
+    const auto &L = c->lay[s];  // storage order of the compressed columns
     for (int64_t i = 0; i < R.n_own; ++i) {
       double *row = out + (size_t)R.own_orig[i] * Wd;
       for (int64_t r = 0; r < Wd; ++r) {
         const int64_t ci = compressed_index(sets[r], col[i]);
-        if (ci >= 0) row[r] = tab[(size_t)i * Wc + ci];
+        if (ci >= 0) row[r] = tab[(size_t)i * Wc + L.pos[(size_t)ci]];
       }
     }
   }
@@ -527,7 +529,7 @@ cc_status cc_get_subtree_rows(cc_ctx *c, int32_t x, const int32_t *vertices, int
       if (inv[vertices[i]] < 0) continue;  // isolated: no embedding of a tree with >= 2 vertices
       for (int64_t r = 0; r < Wd; ++r) {
         const int64_t ci = compressed_index(sets[r], colour_of[vertices[i]]);
-        if (ci >= 0) row[r] = tab[j * Wc + ci];
+        if (ci >= 0) row[r] = tab[j * Wc + c->lay[s].pos[(size_t)ci]];
       }
       ++j;
     }
@@ -543,6 +545,11 @@ cc_status cc_set_knob(cc_ctx *c, const char *name, int32_t value) {
     return CC_ERR_ARG;
   }
   *p = value;
+  if (std::string(name) == "layout" && c->has_graph && c->has_template) {  // the tables' column order changes
+    API_BEGIN(c)
+    cc::upload_template(c);
+    API_END(c)
+  }
   return CC_OK;
 }
 

@@ -5,7 +5,9 @@
 // S_i subset of S with |S_i| = |T_i|" -- every table row holds C(k, |T_i|)
 // entries, one per colour set; Eq. 1/2 (lines 118, 167) sum over the splits
 // S = S1 u S2 with |S1| = |T_i'|, |S2| = |T_i''|.
+#include <algorithm>
 #include <cstring>
+#include <numeric>
 
 #include "common.h"
 
@@ -81,19 +83,79 @@ uint32_t unsqueeze(uint32_t mask, int c) { return (mask & ((1u << c) - 1u)) | ((
 
 int64_t gather_map_ld(int k, int p) { return (binom(k - 1, p - 1) + 7) / 8 * 8; }
 
-std::vector<uint16_t> gather_map(int k, int p) {
+std::vector<uint16_t> gather_map(int k, int p, const Layout *lin, const Layout *lout) {
   const int64_t w_in = binom(k - 1, p - 1), ld = gather_map_ld(k, p);
   std::vector<uint16_t> out((size_t)(k * k * ld), 0xFFFF);
   for (int cu = 0; cu < k; ++cu)
     for (int cv = 0; cv < k; ++cv) {
       if (cu == cv) continue;
-      for (int64_t r = 0; r < w_in; ++r) {
+      for (int64_t q = 0; q < w_in; ++q) {  // storage position q of u's row
+        const int64_t r = lin ? lin->rank[(size_t)q] : q;
         const uint32_t Y = unsqueeze(colex_unrank(p - 1, r), cu) | (1u << cu);  // u's colour set
         if (Y >> cv & 1u) continue;                                             // meets v's colour
-        out[(size_t)((cu * k + cv) * ld + r)] = (uint16_t)colex_rank(squeeze(Y, cv));
+        const int64_t y = colex_rank(squeeze(Y, cv));
+        out[(size_t)((cu * k + cv) * ld + q)] = (uint16_t)(lout ? lout->pos[(size_t)y] : y);
       }
     }
   return out;
+}
+
+// Sector-homogeneous storage order of the s-subsets of a K-colour universe
+// (build decision R-3): consecutive groups of E sets (E = entries per 32-byte
+// sector) that share as many colours as possible, so that a neighbour row's
+// sectors whose sets all contain the destination's colour -- never used by
+// it -- are as many as possible (they are not read, R-2).  Greedy over
+// shared cores of size s-1, s-2, ..., 1 (each core's remaining supersets cut
+// into groups of E), the rest in colex order; deterministic.
+Layout pack_layout(int K, int s, int E) {
+  Layout L;
+  const int64_t W = binom(K, s);
+  L.rank.resize((size_t)W);
+  L.pos.resize((size_t)W);
+  std::vector<uint32_t> sets((size_t)W);
+  for (int64_t r = 0; r < W; ++r) sets[r] = colex_unrank(s, r);
+  std::vector<char> used((size_t)W, 0);
+  int64_t n = 0;
+  uint64_t rng = 0x9E3779B97F4A7C15ULL;  // fixed-seed xorshift: the order of the cores tried
+  auto next = [&]() {
+    rng ^= rng << 13;
+    rng ^= rng >> 7;
+    rng ^= rng << 17;
+    return rng;
+  };
+  for (int c = s - 1; c >= 1 && s >= 2; --c) {
+    std::vector<uint32_t> cores;
+    for (int64_t r = 0; r < binom(K, c); ++r) cores.push_back(colex_unrank(c, r));
+    for (size_t i = cores.size(); i > 1; --i) std::swap(cores[i - 1], cores[next() % i]);
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (uint32_t core : cores) {
+        std::vector<int64_t> cand;
+        for (int64_t r = 0; r < W; ++r)
+          if (!used[r] && (sets[r] & core) == core) cand.push_back(r);
+        for (size_t i = 0; i + E <= cand.size(); i += E) {
+          for (int e = 0; e < E; ++e) {
+            used[cand[i + e]] = 1;
+            L.rank[(size_t)n++] = (int32_t)cand[i + e];
+          }
+          changed = true;
+        }
+      }
+    }
+  }
+  for (int64_t r = 0; r < W; ++r)
+    if (!used[r]) L.rank[(size_t)n++] = (int32_t)r;
+  for (int64_t q = 0; q < W; ++q) L.pos[(size_t)L.rank[q]] = (int32_t)q;
+  return L;
+}
+
+Layout identity_layout(int K, int s) {
+  Layout L;
+  const int64_t W = binom(K, s);
+  L.rank.resize((size_t)W);
+  std::iota(L.rank.begin(), L.rank.end(), 0);
+  L.pos = L.rank;
+  return L;
 }
 
 std::vector<uint16_t> complement_table(int k, int a) {
@@ -170,7 +232,7 @@ int64_t zblock_ld(int ts, int as) {
 
 namespace cc {
 
-std::vector<uint32_t> skip_table(int k, int p, int elem, int *words) {
+std::vector<uint32_t> skip_table(int k, int p, int elem, int *words, const Layout *lin) {
   const int K = k - 1, s = p - 1;
   const int64_t W = binom(K, s);
   const int vw = 16 / elem, se = 32 / elem;  // entries per 16-byte vector / 32-byte sector
@@ -178,7 +240,7 @@ std::vector<uint32_t> skip_table(int k, int p, int elem, int *words) {
   const int nw = (int)((nvec + 31) / 32) + 4;  // + slack: the kernel may address (pass, j) words past the row
   std::vector<uint32_t> out((size_t)K * nw, 0);
   std::vector<uint32_t> sets((size_t)W);
-  for (int64_t r = 0; r < W; ++r) sets[r] = colex_unrank(s, r);
+  for (int64_t q = 0; q < W; ++q) sets[q] = colex_unrank(s, lin ? lin->rank[(size_t)q] : q);  // storage order
   for (int c = 0; c < K; ++c)
     for (int64_t vi = 0; vi < nvec; ++vi) {
       const int64_t s0 = vi * vw / se * se;

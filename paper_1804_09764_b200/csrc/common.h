@@ -36,17 +36,27 @@ std::vector<uint16_t> complement_table(int k, int a);
 // from the universe (higher colours shift down), us_c re-inserts it.
 uint32_t squeeze(uint32_t mask, int c);
 uint32_t unsqueeze(uint32_t mask, int c);
+// Storage order of a table's compressed columns (build decision R-3): rank[q]
+// = colex rank of the colour set at storage position q, pos = its inverse.
+struct Layout {
+  std::vector<int32_t> rank, pos;
+};
+Layout pack_layout(int K, int s, int E);  // sector-homogeneous order (E sets per 32-byte sector)
+Layout identity_layout(int K, int s);
+
 // Gather map of a passive part of size p: for neighbour colour cu, vertex
 // colour cv and compressed index r of u's row (Y' = unrank(p-1, r) in the
 // (k-1)-universe of cu), out[(cu*k + cv) * C(k-1,p-1) + r] = rank of
 // sq_cv({cu} u us_cu(Y')) in C(k-1, p), or 0xFFFF if that set contains cv.
-std::vector<uint16_t> gather_map(int k, int p);
+// With layouts: lin = the passive table's (input positions), lout = the
+// neighbour sum's (output positions); nullptr = colex order.
+std::vector<uint16_t> gather_map(int k, int p, const Layout *lin = nullptr, const Layout *lout = nullptr);
 // Sector-skip table of a passive part of size p (rows of C(k-1, p-1) entries
 // of elem bytes): for each colour c' of the (k-1)-universe, bit (vi mod 32)
 // of word (vi / 32) marks 16-byte vector vi of a row whose whole 32-byte
 // sector holds only sets containing c' (or padding) -- entries no
 // destination of that colour can use.  *words receives the words per colour.
-std::vector<uint32_t> skip_table(int k, int p, int elem, int *words);
+std::vector<uint32_t> skip_table(int k, int p, int elem, int *words, const Layout *lin = nullptr);
 int64_t gather_map_ld(int k, int p);  // map row stride: C(k-1,p-1) rounded up to 8 (padding 0xFFFF)
 
 // Z-block cover of a combine step with outputs of size ts = t-1, actives of

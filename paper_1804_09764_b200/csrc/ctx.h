@@ -143,6 +143,7 @@ struct cc_ctx {
   std::vector<uint16_t *> d_map;      // per passive size p: gather map (p >= 2)
   std::vector<uint32_t *> d_skip;     // per passive size p: sector-skip table
   std::vector<int> skip_words;
+  std::vector<cc::Layout> lay;        // per table size t: storage order of the C(k-1, t-1) columns (R-3)
   uint16_t *d_comp = nullptr;         // root step complement table
   bool has_colors = false;
   bool sorted_valid = false;          // colour-sorted adjacency matches the colouring

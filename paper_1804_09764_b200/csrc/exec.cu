@@ -267,32 +267,58 @@ void upload_template(cc_ctx *c) {
   c->skip_words.assign(kMaxK + 1, 0);
   c->d_comp = nullptr;
   const int k = c->plan.colours();
+  // storage order of the compressed columns of every table size t (R-3):
+  // sector-homogeneous for t >= 3; colex for t <= 2 (the leaf level and its
+  // lift are written by the colour sort in colex order)
+  c->lay.assign(kMaxK + 2, Layout());
+  for (int t = 1; t <= k; ++t)
+    c->lay[t] = (t >= 3 && c->knobs.layout) ? pack_layout(k - 1, t - 1, 32 / c->elem()) : identity_layout(k - 1, t - 1);
+  const auto &L = c->lay;
   for (size_t s = 0; s < c->plan.steps.size(); ++s) {
     const Step &st = c->plan.steps[s];
     // compressed universe: k-1 colours, sets of size t-1 split into (a-1, p);
     // the root of a template with as many vertices as colours pairs each
-    // active set with its complement, otherwise the root is a full combine
+    // active set with its complement, otherwise the root is a full combine.
+    // Indices are storage positions: actives in L[a], neighbour sums of a
+    // passive of size p in L[p + 1], outputs in L[t].
     if (st.out < 0 && c->plan.k == k) {
-      if (st.a > 1) c->d_comp = c->pupload(complement_table(k - 1, st.a - 1));
+      if (st.a > 1) {
+        std::vector<uint16_t> comp = complement_table(k - 1, st.a - 1);
+        std::vector<uint16_t> cp(comp.size());
+        for (size_t q = 0; q < comp.size(); ++q) cp[q] = (uint16_t)L[st.p + 1].pos[comp[(size_t)L[st.a].rank[q]]];
+        c->d_comp = c->pupload(cp);
+      }
     } else if (st.a > 1) {
       // rows of the split table padded to a multiple of 8 outputs (16-byte
       // aligned groups of split entries for the combine kernels)
       const std::vector<uint32_t> tab = split_table(k - 1, st.t - 1, st.a - 1);
       const int64_t WO = binom(k - 1, st.t - 1), WOp = (WO + 7) / 8 * 8, nq = binom(st.t - 1, st.a - 1);
       std::vector<uint32_t> pad((size_t)(nq * WOp), 0);
-      for (int64_t q = 0; q < nq; ++q) std::copy(tab.begin() + q * WO, tab.begin() + (q + 1) * WO, pad.begin() + q * WOp);
+      for (int64_t q = 0; q < nq; ++q)
+        for (int64_t o = 0; o < WO; ++o) {
+          const uint32_t e = tab[(size_t)(q * WO + L[st.t].rank[(size_t)o])];
+          pad[(size_t)(q * WOp + o)] = (uint32_t)L[st.a].pos[e & 0xFFFF] | ((uint32_t)L[st.p + 1].pos[e >> 16] << 16);
+        }
       c->d_split[s] = c->pupload(pad);
       if (dev::combine_z_supported(c->elem(), st.t - 1, st.a - 1)) {  // Z-block cover for the register-blocked combine
         int nb = 0;
-        const std::vector<uint16_t> zt = zblock_table(k - 1, st.t - 1, st.a - 1, &nb);
+        std::vector<uint16_t> zt = zblock_table(k - 1, st.t - 1, st.a - 1, &nb);
+        const int64_t zld = zblock_ld(st.t - 1, st.a - 1), na = binom(st.t, st.a - 1), nn = binom(st.t, st.p);
+        for (int b = 0; b < nb; ++b) {
+          uint16_t *e = zt.data() + (size_t)b * zld;
+          for (int64_t i = 0; i < na; ++i) e[i] = (uint16_t)L[st.a].pos[e[i]];
+          for (int64_t i = na; i < na + nn; ++i) e[i] = (uint16_t)L[st.p + 1].pos[e[i]];
+          for (int64_t i = na + nn; i < na + nn + st.t; ++i)
+            if (e[i] != 0xFFFF) e[i] = (uint16_t)L[st.t].pos[e[i]];
+        }
         c->d_ztab[s] = c->pupload(zt);
         c->zblocks[s] = nb;
       }
     }
     if (st.p > 1 && !c->d_map[st.p]) {
-      c->d_map[st.p] = c->pupload(gather_map(k, st.p));
+      c->d_map[st.p] = c->pupload(gather_map(k, st.p, &L[st.p], &L[st.p + 1]));
       int nw = 0;
-      const std::vector<uint32_t> sk = skip_table(k, st.p, c->elem(), &nw);
+      const std::vector<uint32_t> sk = skip_table(k, st.p, c->elem(), &nw, &L[st.p]);
       c->d_skip[st.p] = c->pupload(sk);
       c->skip_words[st.p] = nw;
     }

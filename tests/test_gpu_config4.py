@@ -168,3 +168,79 @@ def test_star_closed_form_full_config4_graph(graph4):
     from gpu_util import count
     got = count(g, [-1] + [0] * (k - 1), seed=21, precision="fp64")
     assert abs(got - want) <= 1e-12 * want, (got, want)
+
+
+def _root_samples(g, n, seed=7, max_ball2=20000, max_work=20_000_000):
+    """n vertices (seeded order) of degree 4..12 whose radius-2 ball has at
+    most max_ball2 vertices and degree sum at most max_work: the oracle's
+    or_dp_root_at then costs seconds, however large the graph."""
+    deg = g.degrees()
+    cand = np.flatnonzero((deg >= 4) & (deg <= 12))
+    np.random.default_rng(seed).shuffle(cand)
+    out = []
+    for v in cand[:200000]:
+        nb = g.neighbors(int(v))
+        if 1 + nb.size + int(deg[nb].sum()) > max_ball2:
+            continue
+        b2 = np.unique(np.concatenate([nb] + [g.neighbors(int(u)) for u in nb]))
+        if int(deg[b2].sum()) > max_work:
+            continue
+        out.append(int(v))
+        if len(out) == n:
+            break
+    return out
+
+
+def _check_root_rows(got, want, what):
+    for i, (x, w) in enumerate(zip(got, want)):
+        if w == 0:
+            assert x == 0, f"{what}: X_v = {x} where the oracle has 0 (sample {i})"
+        else:
+            assert abs(x - w) <= TOL_FP32 * abs(w), f"{what}: X_v = {x} vs oracle {w} (sample {i})"
+
+
+def test_config4_full_size_root_counts(graph4):
+    """configs[4] at full size, one GPU: the per-vertex root counts X_v (the
+    summands of Eq. 3) of sampled vertices against the
+    oracle's DP evaluated at that vertex (or_dp_root_at: the depth-3 template
+    reads only the ball of radius 3), fp32 tables within 1e-4.  The fused
+    root (self dot, mode 2) produced them."""
+    cc = lib()
+    cfg = synth.CONFIGS[4]
+    g = graph4
+    samples = _root_samples(g, 4)
+    with context(g, cfg.parent, "fp32") as ctx:
+        cc.cc_color(ctx, cfg.color_seed)
+        rows = cc.cc_get_subtree_rows(ctx, 0, samples, cfg.k, cfg.k)[:, 0]
+        assert cc.cc_last_stats(ctx)["fused_root"] == 2
+    col = oracle.color(g.n, cfg.k, cfg.color_seed)
+    want = [oracle.dp_root_at(g, cfg.parent, col, v, oracle.NUM_DOUBLE) for v in samples]
+    assert any(w > 0 for w in want)
+    _check_root_rows(rows, want, "configs[4] X_v")
+
+
+def test_k16_template_with_7_vertex_subtrees_runs_on_one_gpu(graph4):
+    """A k = 16 template (PAR16: the root, two 7-vertex perfect binary
+    subtrees, a leaf) on the configs[4] graph needs a 235 GB table of the
+    7-vertex subtree and a 302 GB neighbour sum -- more than one GPU.  The
+    memory plan runs it on ONE GPU:
+    the tail of the plan in row batches, the 7-vertex subtree's table
+    recomputed per batch in column chunks by its combine.  The count is
+    finite and positive, the plan is the batched one, and sampled X_v equal
+    the oracle's DP at those vertices (fp32, 1e-4)."""
+    cc = lib()
+    g = graph4
+    k = 16
+    samples = _root_samples(g, 4)
+    with context(g, PAR16, "fp32") as ctx:
+        cc.cc_color(ctx, 2)
+        x = cc.cc_count_colorful(ctx)
+        st = cc.cc_last_stats(ctx)
+        assert math.isfinite(x) and x > 0
+        assert st["tail_batches"] >= 2 and st["recompute_cols"] > 0, st
+        assert st["peak_table_bytes"] < 180e9
+        rows = cc.cc_get_subtree_rows(ctx, 0, samples, k, k)[:, 0]
+    col = oracle.color(g.n, k, 2)
+    want = [oracle.dp_root_at(g, PAR16, col, v, oracle.NUM_DOUBLE) for v in samples]
+    assert any(w > 0 for w in want)
+    _check_root_rows(rows, want, "k = 16 X_v")
