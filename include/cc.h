@@ -112,9 +112,13 @@ typedef struct {
   int32_t segment_len;   /* neighbour-list task size s: neighbour lists longer
                             than this are split into segments of at most s
                             neighbours (Alg. 4); 0 = auto */
-  int32_t use_graphs;    /* reserved, must be 0 or 1, no effect: a colouring
-                            is ~12 launches of >= 1 ms each on configs[2-4],
-                            not launch-bound */
+  int32_t use_graphs;    /* 1: cc_count_colorful / cc_estimate (one rank)
+                            replay a CUDA graph of the count's device work,
+                            captured on first use and after any change of
+                            graph, template, knobs or profiling (a new
+                            colouring is data: the same graph); per-phase
+                            profile times are then not reported.  For the
+                            launch-bound small graphs (configs[0-1]); 0 or 1 */
   uint64_t relabel_seed; /* seed of the internal vertex permutation used to
                             balance the partition ("randomly
                             partitioned"); never changes results */
@@ -272,7 +276,8 @@ cc_status cc_get_subtree_rows(cc_ctx *ctx, int32_t x, const int32_t *vertices, i
 /* Implementation knobs (A/B switches of the launchers; every setting
  * computes the same values): name is one of fused_root, sector_skip,
  * gather_impl, narrow_impl, narrow_split, csort_small, combine_impl, acc32,
- * phase_events, hub_l2_pct, grid_reserve (meanings and defaults: DESIGN.md
+ * phase_events, hub_l2_pct, grid_reserve, tail_batches, tail_recompute_cols,
+ * layout, nvtx_mark (meanings and defaults: DESIGN.md
  * section 9a).  Each context reads CC_<NAME> from the environment ONCE, in
  * cc_create; these calls change or read the context's value.  CC_ERR_ARG on
  * an unknown name or a NULL pointer.  Not collective: set the same value on
@@ -306,7 +311,9 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * (0: none -- one rank or replicas, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING),
  * out[11] (cap >= 12) = column-chunk launches of the chunked neighbour sums
  * (0: none), out[12] = row batches of the memory plan's tail (0: none),
- * out[13] = column width of the tail's recomputed passive table (0: none).
+ * out[13] = column width of the tail's recomputed passive table (0: none),
+ * out[14] (cap >= 15) = 1-based ordinal of the longest neighbour-sum pass
+ * among the count's passes (the knob nvtx_mark selects a pass by it).
  * cap >= 5. */
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
 

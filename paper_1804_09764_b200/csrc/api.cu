@@ -90,6 +90,7 @@ int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
   if (name == "grid_reserve") return &k.grid_reserve;
   if (name == "tail_batches") return &k.tail_batches;
   if (name == "layout") return &k.layout;
+  if (name == "nvtx_mark") return &k.nvtx_mark;
   if (name == "tail_recompute_cols") return &k.tail_recompute_cols;
   return nullptr;
 }
@@ -98,7 +99,7 @@ int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
 void knobs_from_env(cc::dev::Knobs &k) {
   static const char *names[] = {"fused_root", "sector_skip", "gather_impl", "narrow_impl", "narrow_split",
                                 "csort_small", "combine_impl", "acc32", "phase_events", "hub_l2_pct", "grid_reserve",
-                                "tail_batches", "tail_recompute_cols", "layout"};
+                                "tail_batches", "tail_recompute_cols", "layout", "nvtx_mark"};
   for (const char *n : names) {
     std::string env = "CC_";
     for (const char *q = n; *q; ++q) env += (char)std::toupper((unsigned char)*q);
@@ -236,10 +237,17 @@ void cc_destroy(cc_ctx *c) {
   if (c->comm) cc::nccl().CommDestroy(c->comm);
   for (void *p : c->persistent) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  for (auto e : c->graph_ev)
+    if (e) cudaEventDestroy(e);
   for (auto e : c->ev_color)
     if (e) cudaEventDestroy(e);
   if (c->s_main) cudaStreamDestroy(c->s_main);
   if (c->s_comm) cudaStreamDestroy(c->s_comm);
+  {  // hand the stream-ordered pool's cached blocks back to the device
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->opt.device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
   delete c;
 }
 
@@ -320,7 +328,8 @@ cc_status cc_count_colorful(cc_ctx *c, double *X) {
   if (!X) throw Error(CC_ERR_ARG, "output pointer is NULL");
   if (!c->has_graph || !c->has_template || !c->has_colors)
     throw Error(CC_ERR_STATE, "cc_count_colorful needs a graph, a template and a colouring");
-  cc::run_count(c, X, -1, nullptr, nullptr);
+  if (c->opt.use_graphs && c->pworld() == 1) cc::count_graph(c, X);
+  else cc::run_count(c, X, -1, nullptr, nullptr);
   API_END(c)
 }
 
@@ -545,6 +554,7 @@ cc_status cc_set_knob(cc_ctx *c, const char *name, int32_t value) {
     return CC_ERR_ARG;
   }
   *p = value;
+  ++c->epoch;  // a captured graph no longer matches
   if (std::string(name) == "layout" && c->has_graph && c->has_template) {  // the tables' column order changes
     API_BEGIN(c)
     cc::upload_template(c);
@@ -564,6 +574,7 @@ cc_status cc_get_knob(cc_ctx *c, const char *name, int32_t *value) {
 cc_status cc_set_profiling(cc_ctx *c, int32_t on) {
   if (!c) return CC_ERR_ARG;
   c->profiling = on != 0;
+  ++c->epoch;
   return CC_OK;
 }
 

@@ -30,7 +30,7 @@
 
 namespace cc {
 
-constexpr int kNStats = 14;  // cc_last_stats entries
+constexpr int kNStats = 15;  // cc_last_stats entries
 
 // Phases reported by cc_last_profile after "total": PROFILE order.
 enum Phase { PH_COLOR = 0, PH_CSORT, PH_HIST, PH_GATHER, PH_COMBINE, PH_ROOT, PH_EXCHANGE, PH_EXPOSED, PH_N };
@@ -131,6 +131,10 @@ struct cc_ctx {
   // planner's statistic, identical on every rank (a per-rank figure could
   // pick different plans on different ranks, and their exchanges would not match)
   double avg_degree = 0;
+  // CUDA graph of a count (use_graphs): rebuilt when epoch moves past gepoch
+  int64_t epoch = 0, gepoch = -1;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t graph_ev[2] = {nullptr, nullptr};
 
   // template
   bool has_template = false;
@@ -160,6 +164,7 @@ struct cc_ctx {
   double prof[cc::PH_N + 1] = {0};
   double stats[cc::kNStats] = {0};
   std::vector<std::pair<size_t, double>> gather_log;  // (ev_log index, algorithmic bytes) per gather launch
+  int gather_ordinal = 0;                             // neighbour-sum passes launched in this count
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -265,8 +270,11 @@ void launch_colouring(cc_ctx *c, uint64_t seed);
 // owned row (dump_rows == nullptr; disables the fused root and releases) or
 // only the internal rows listed in *dump_rows (copied right after the step
 // that produces the table; nothing else changes).
+// capture: record the device work into the stream's capture (CUDA graph), no host copies
 void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, std::vector<double> *root_out,
-               const std::vector<int64_t> *dump_rows = nullptr, TableCache *cache = nullptr);
+               const std::vector<int64_t> *dump_rows = nullptr, TableCache *cache = nullptr, bool capture = false);
+// cc_count_colorful through a captured CUDA graph (use_graphs, one rank)
+void count_graph(cc_ctx *c, double *X);
 void free_cache(cc_ctx *c, TableCache &cache);
 // X_j for colourings seed0 + j, j < iterations (replica mode with world > 1:
 // iteration j on rank j mod world, then one all-reduce of the vector).

@@ -34,6 +34,8 @@ struct Knobs {
   int hub_l2_pct = 50;     // CC_HUB_L2_PCT: % of the L2 given an evict-last policy for hub rows (rings)
   int grid_reserve = -1;   // CC_GRID_RESERVE: SMs left free for NCCL while an exchange is in flight
                            //                  (-1 = auto: 8 when world > 1 over NCCL, else 0)
+  int nvtx_mark = 0;       // CC_NVTX_MARK: i > 0 = the i-th neighbour-sum pass of a count runs inside
+                           //               the NVTX range "cc_dominant" (one-launch ncu measurement)
   int layout = 1;          // CC_LAYOUT: 1 = sector-homogeneous column order of tables of >= 3 vertices
                            //            (R-3), 0 = colex order
   int tail_batches = 0;    // CC_TAIL_BATCHES: > 0 forces the memory plan's row batches (0 = by memory)
