@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-scale", type=int, default=0, help="R-MAT scale of the oracle sample (0 = auto)")
+    ap.add_argument("--graphs", type=int, default=-1,
+                    help="1: replay each count as a CUDA graph (cc_options.use_graphs); -1 = auto (configs 0-1)")
     ap.add_argument("--no-ncu", action="store_true",
                     help="skip the one-launch ncu pass that measures the dominant kernel's DRAM traffic")
     ap.add_argument("--ncu-child", type=int, default=0, help=argparse.SUPPRESS)  # internal: pass ordinal to mark
@@ -317,7 +319,8 @@ def run_ours(args, cfg, rank, world, dist):
     kw = dict(precision=cc.CC_FP64 if precision == "fp64" else cc.CC_FP32, segment_len=args.segment_len,
               exchange={"auto": cc.CC_EXCHANGE_AUTO, "grouped": cc.CC_EXCHANGE_GROUPED,
                         "ring": cc.CC_EXCHANGE_RING}[args.exchange],
-              replicas=1 if (args.replicas and world > 1) else 0)
+              replicas=1 if (args.replicas and world > 1) else 0,
+              use_graphs=int(args.graphs if args.graphs >= 0 else (cfg.idx <= 1 and world == 1)))
     if world > 1:
         opt, _idbuf = cc.distributed_options(**kw)
     else:

@@ -202,6 +202,11 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
     int l2 = 0;
     CUDA_OK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, opt->device));
     if (l2 > 0) c->l2_bytes = l2;
+    {
+      size_t fr = 0, tot = 0;
+      CUDA_OK(cudaMemGetInfo(&fr, &tot));
+      c->total_mem = (double)tot;
+    }
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
     cudaMemPool_t pool;

@@ -100,6 +100,7 @@ struct cc_ctx {
   std::string err;
   bool poisoned = false;
   int num_sms = 148;
+  double total_mem = 0;  // device memory (bytes), at cc_create
   int64_t l2_bytes = 126LL << 20;
   cudaStream_t s_main = nullptr, s_comm = nullptr;
   ncclComm_t comm = nullptr;

@@ -800,6 +800,11 @@ MemPlan plan_memory(cc_ctx *c, const Plan &pl, int64_t rows, int fuse, int defer
   MemPlan none;
   const int sr = (int)pl.steps.size() - 1, forced_nb = c->knobs.tail_batches, forced_w = c->knobs.tail_recompute_cols;
   if (c->pworld() > 1) return none;  // one rank only (the 1D partition bounds memory with chunked halo buffers)
+  // plans far below the device's memory need no query (cudaMemGetInfo costs
+  // milliseconds of host time, which launch-bound small graphs would see)
+  if (forced_nb <= 0 && forced_w <= 0 &&
+      model_peak(c, pl, rows, fuse, defer_lift, fuse_cr, last_hist_use, per_vertex, none) < 0.4 * c->total_mem)
+    return none;
   // the budget: free device memory + what the stream-ordered pool holds unused, less a margin
   size_t free_b = 0, total_b = 0;
   CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
@@ -894,8 +899,8 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
   // table rows: owned + halo (halo rows of passive tables land there), or
   // owned only when the exchange is chunked (halo rows go to chunk buffers)
   const int64_t n = c->n_own, rows = c->chunked ? c->n_own : c->n_rows;
-  cudaEvent_t t0 = capture ? c->graph_ev[0] : c->ev(), t1 = capture ? c->graph_ev[1] : c->ev();
-  CUDA_OK(cudaEventRecord(t0, c->s_main));
+  cudaEvent_t t0 = c->ev(), t1 = c->ev();
+  if (!capture) CUDA_OK(cudaEventRecord(t0, c->s_main));  // graphs are timed around their launch
 
   // world > 1: colour-sort the neighbour ranges of both passes (once per
   // colouring); world 1 sorts below, fused with the leaf level (hist)
@@ -1371,7 +1376,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     else NCCL_OK(nccl().AllReduce(c->d_result, c->d_result, 1, ncclFloat64, ncclSum, c->comm, c->s_main));
     c->end(PH_EXCHANGE, c->s_main, b);
   }
-  CUDA_OK(cudaEventRecord(t1, c->s_main));
+  if (!capture) CUDA_OK(cudaEventRecord(t1, c->s_main));
   if (capture) {  // a CUDA graph of the count's device work (use_graphs): no host copies, no syncs
     for (auto &b : bufs.pool)
       if (b.p && b.owned) c->afree(b.p, b.bytes, c->s_main);
@@ -1461,7 +1466,9 @@ void count_graph(cc_ctx *c, double *X) {
     CUDA_OK(e);
     c->gepoch = c->epoch;
   }
+  CUDA_OK(cudaEventRecord(c->graph_ev[0], c->s_main));
   CUDA_OK(cudaGraphLaunch(c->gexec, c->s_main));
+  CUDA_OK(cudaEventRecord(c->graph_ev[1], c->s_main));
   double host_x = 0;
   CUDA_OK(cudaMemcpyAsync(&host_x, c->d_result, sizeof(double), cudaMemcpyDeviceToHost, c->s_main));
   CUDA_OK(cudaStreamSynchronize(c->s_main));

@@ -638,3 +638,33 @@ def test_every_knob_setting_computes_the_same_count(ci):
             with context(g, cfg.parent) as ctx:
                 cc.cc_set_knob(ctx, "no_such_knob", 1)
         assert e.value.status == cc.CC_ERR_ARG
+
+
+def test_cuda_graph_replay_equals_direct_counts():
+    """use_graphs = 1 (configs[0] and [1], the launch-bound ones): the count's
+    device work is captured once and replayed for every new colouring (data
+    only); a knob change or a new template recaptures.  Every count equals
+    the direct path's, which equals the oracle (fp64 exact)."""
+    cc = lib()
+    for ci in (0, 1):
+        cfg = synth.CONFIGS[ci]
+        g = cfg.graph()
+        with context(g, cfg.parent) as direct, context(g, cfg.parent, use_graphs=1) as graphed:
+            for seed in (2, 3, 4):
+                cc.cc_color(direct, seed)
+                cc.cc_color(graphed, seed)
+                x = cc.cc_count_colorful(direct)
+                assert cc.cc_count_colorful(graphed) == x, (ci, seed)
+                assert cc.cc_last_profile(graphed)["total"] > 0
+            want = oracle.dp_count(g, cfg.parent, oracle.color(g.n, cfg.k, 4), oracle.NUM_EXACT).total
+            assert rel_err(x, float(want)) <= TOL_FP64  # (configs[1]'s counts pass 2^53)
+            cc.cc_set_knob(graphed, "gather_impl", 2)  # recapture
+            assert cc.cc_count_colorful(graphed) == x
+            cc.cc_set_template(graphed, [-1, 0, 1])    # new plan: recapture
+            cc.cc_set_template(direct, [-1, 0, 1])
+            cc.cc_color(direct, 9)
+            cc.cc_color(graphed, 9)
+            assert cc.cc_count_colorful(graphed) == cc.cc_count_colorful(direct)
+            e1, xs1 = cc.cc_estimate(graphed, 4, 50, per_iter=True)
+            e2, xs2 = cc.cc_estimate(direct, 4, 50, per_iter=True)
+            assert list(xs1) == list(xs2) and e1 == e2
