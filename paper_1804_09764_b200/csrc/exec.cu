@@ -277,7 +277,9 @@ void upload_template(cc_ctx *c) {
   // lift are written by the colour sort in colex order)
   c->lay.assign(kMaxK + 2, Layout());
   for (int t = 1; t <= k; ++t)
-    c->lay[t] = (t >= 3 && c->knobs.layout) ? pack_layout(k - 1, t - 1, 32 / c->elem()) : identity_layout(k - 1, t - 1);
+    c->lay[t] = (t >= 3 && c->knobs.layout > 0)
+                    ? pack_layout(k - 1, t - 1, (32 << (c->knobs.layout - 1)) / c->elem())  // groups of 32 B, 64 B, 128 B
+                    : identity_layout(k - 1, t - 1);
   const auto &L = c->lay;
   for (size_t s = 0; s < c->plan.steps.size(); ++s) {
     const Step &st = c->plan.steps[s];

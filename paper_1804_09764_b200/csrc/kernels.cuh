@@ -36,8 +36,8 @@ struct Knobs {
                            //                  (-1 = auto: 8 when world > 1 over NCCL, else 0)
   int nvtx_mark = 0;       // CC_NVTX_MARK: i > 0 = the i-th neighbour-sum pass of a count runs inside
                            //               the NVTX range "cc_dominant" (one-launch ncu measurement)
-  int layout = 0;          // CC_LAYOUT: 1 = sector-homogeneous column order of tables of >= 3 vertices
-                           //            (R-3; measured slower on configs[3]: gathers 143.6 -> 148.4 ms), 0 = colex
+  int layout = 0;          // CC_LAYOUT: column order of tables of >= 3 vertices (R-3): 0 = colex;
+                           //   L = 1, 2, 3: groups of 32 << (L-1) bytes whose sets share the most colours
   int tail_batches = 0;    // CC_TAIL_BATCHES: > 0 forces the memory plan's row batches (0 = by memory)
   int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
                                 //   per batch in column chunks of this width (0 = by memory)
