@@ -46,7 +46,7 @@ def parse():
                     help="N > 1: colouring replicas (each GPU the whole graph, different colourings; SURVEY F1) "
                          "instead of the 1D vertex partition")
     ap.add_argument("--segment-len", type=int, default=0)
-    ap.add_argument("--exchange", default="auto", choices=["auto", "grouped", "ring"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "grouped", "ring", "alltoall", "device"],
                     help="halo-exchange schedule of the 1D partition (PAPER.md Alg. 3)")
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -317,8 +317,8 @@ def run_ours(args, cfg, rank, world, dist):
     torch.cuda.set_device(local)
     g = cfg.graph()
     kw = dict(precision=cc.CC_FP64 if precision == "fp64" else cc.CC_FP32, segment_len=args.segment_len,
-              exchange={"auto": cc.CC_EXCHANGE_AUTO, "grouped": cc.CC_EXCHANGE_GROUPED,
-                        "ring": cc.CC_EXCHANGE_RING}[args.exchange],
+              exchange={"auto": cc.CC_EXCHANGE_AUTO, "grouped": cc.CC_EXCHANGE_GROUPED, "ring": cc.CC_EXCHANGE_RING,
+                        "alltoall": cc.CC_EXCHANGE_ALLTOALL, "device": cc.CC_EXCHANGE_DEVICE}[args.exchange],
               replicas=1 if (args.replicas and world > 1) else 0,
               use_graphs=int(args.graphs if args.graphs >= 0 else (cfg.idx <= 1 and world == 1)))
     if world > 1:
@@ -443,7 +443,7 @@ def run_ours(args, cfg, rank, world, dist):
                         "d2h_bytes_per_step": 8, "ms_per_step": e2e_s * 1e3,
                         "api": "cc_set_colors(host colouring) + cc_count_colorful"},
                 "gpu_launches": launches * args.steps,
-                "nvlink": ({"schedule": {1: "grouped", 2: "ring"}.get(stats["exchange"]),
+                "nvlink": ({"schedule": {1: "grouped", 2: "ring", 3: "alltoall", 4: "device"}.get(stats["exchange"]),
                             "halo_bytes_received_per_step_rank0": stats["halo_bytes"],
                             "exchange_ms_per_step_rank0": last_prof["exchange"],
                             "exposed_exchange_ms_per_step_rank0": last_prof.get("exposed_exchange"),

@@ -81,10 +81,19 @@ enum {
   CC_EXCHANGE_GROUPED = 1, /* one grouped send/recv with every peer (the
                               all-to-all branch, Alg. 3 line 15), overlapped with
                               the local neighbour sum, then one remote pass */
-  CC_EXCHANGE_RING = 2     /* world - 1 steps: step r sends to rank + r and
+  CC_EXCHANGE_RING = 2,    /* world - 1 steps: step r sends to rank + r and
                               receives from rank - r (Alg. 3 lines 2-6), the
                               remote neighbour sum over step r's rows runs while
                               step r + 1 transfers (the pipeline, lines 326-341) */
+  CC_EXCHANGE_ALLTOALL = 3, /* one ncclAlltoAll of per-peer blocks padded to the
+                               largest send count of any rank pair, then the
+                               blocks' rows moved into place */
+  CC_EXCHANGE_DEVICE = 4    /* device-initiated: the pack kernel stores each
+                               boundary row straight into the peer's halo window
+                               (NCCL >= 2.28 symmetric window, LSA pointers over
+                               NVLink, LSA barriers before and after); halo rows
+                               in double-buffered chunk windows (as chunk_cols > 0);
+                               needs a NCCL communicator (not loopback) */
 };
 
 typedef struct {
@@ -316,6 +325,14 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * among the count's passes (the knob nvtx_mark selects a pass by it).
  * cap >= 5. */
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
+
+/* Test hook: the device-initiated exchange's machinery on a one-rank NCCL
+ * communicator: a symmetric window (ncclMemAlloc + ncclCommWindowRegister),
+ * a device communicator with LSA barriers (ncclDevCommCreate), and a kernel
+ * that stores through ncclGetLsaPointer, syncs the barrier and reads the
+ * values back.  CC_ERR_NCCL when the device API is missing or a value is
+ * wrong. */
+cc_status cc_nccl_device_selftest(int32_t device);
 
 /* Test hook: a one-rank NCCL communicator on `device` runs the calls the
  * partitioned path uses -- a grouped ncclSend/ncclRecv (to itself) and an

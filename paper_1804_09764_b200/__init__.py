@@ -18,7 +18,7 @@ import numpy as np
 from . import _native
 from ._native import (CC_ERR_ARG, CC_ERR_CUDA, CC_ERR_GRAPH, CC_ERR_NCCL, CC_ERR_NONFINITE,  # noqa: F401
                       CC_ERR_OOM, CC_ERR_STATE, CC_ERR_TEMPLATE, CC_EXCHANGE_AUTO, CC_EXCHANGE_GROUPED,
-                      CC_EXCHANGE_RING, CC_FP32, CC_FP64, CC_OK, STATUS_NAMES,
+                      CC_EXCHANGE_RING, CC_EXCHANGE_ALLTOALL, CC_EXCHANGE_DEVICE, CC_FP32, CC_FP64, CC_OK, STATUS_NAMES,
                       cc_options)
 
 _lib = _native.lib
@@ -58,6 +58,11 @@ def cc_default_options(**kw) -> cc_options:
 def cc_nccl_selftest(device: int = 0) -> None:
     """Test hook: one-rank NCCL grouped send/recv + all-reduce on `device`."""
     _check(None, _lib.cc_nccl_selftest(device))
+
+
+def cc_nccl_device_selftest(device: int = 0) -> None:
+    """Test hook: NCCL device API (symmetric window, LSA pointer, LSA barrier) on one rank."""
+    _check(None, _lib.cc_nccl_device_selftest(device))
 
 
 def cc_loopback_create(world: int) -> ctypes.c_void_p:

@@ -30,7 +30,7 @@ class cc_options(ctypes.Structure):
 CC_OK, CC_ERR_ARG, CC_ERR_GRAPH, CC_ERR_TEMPLATE, CC_ERR_STATE, CC_ERR_OOM, CC_ERR_CUDA, \
     CC_ERR_NCCL, CC_ERR_NONFINITE = range(9)
 CC_FP64, CC_FP32 = 0, 1
-CC_EXCHANGE_AUTO, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING = 0, 1, 2
+CC_EXCHANGE_AUTO, CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING, CC_EXCHANGE_ALLTOALL, CC_EXCHANGE_DEVICE = 0, 1, 2, 3, 4
 STATUS_NAMES = ["CC_OK", "CC_ERR_ARG", "CC_ERR_GRAPH", "CC_ERR_TEMPLATE", "CC_ERR_STATE", "CC_ERR_OOM",
                 "CC_ERR_CUDA", "CC_ERR_NCCL", "CC_ERR_NONFINITE"]
 
@@ -39,6 +39,7 @@ SIGNATURES = {
     "cc_default_options": (c_i32, [vp]),
     "cc_nccl_unique_id": (c_i32, [vp]),
     "cc_nccl_selftest": (c_i32, [c_i32]),
+    "cc_nccl_device_selftest": (c_i32, [c_i32]),
     "cc_loopback_create": (c_i32, [c_i32, vp]),
     "cc_loopback_destroy": (None, [vp]),
     "cc_create": (c_i32, [vp, vp]),

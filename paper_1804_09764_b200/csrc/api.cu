@@ -147,6 +147,8 @@ cc_status cc_nccl_unique_id(void *out128) {
   return CC_OK;
 }
 
+cc_status cc_nccl_device_selftest(int32_t device) { return cc::device_selftest(device); }
+
 cc_status cc_nccl_selftest(int32_t device) {
   auto &api = cc::nccl();
   if (!api.ok) return CC_ERR_NCCL;
@@ -190,7 +192,8 @@ cc_status cc_create(const cc_options *opt, cc_ctx **out) {
   if (opt->world > 1 && !opt->nccl_id && !opt->loopback) return CC_ERR_ARG;
   if (opt->chunk_cols < 0 || opt->segment_len < 0 || opt->use_graphs < 0 || opt->use_graphs > 1) return CC_ERR_ARG;
   if (opt->replicas < 0 || opt->replicas > 1) return CC_ERR_ARG;
-  if (opt->exchange < CC_EXCHANGE_AUTO || opt->exchange > CC_EXCHANGE_RING) return CC_ERR_ARG;
+  if (opt->exchange < CC_EXCHANGE_AUTO || opt->exchange > CC_EXCHANGE_DEVICE) return CC_ERR_ARG;
+  if (opt->exchange == CC_EXCHANGE_DEVICE && opt->loopback) return CC_ERR_ARG;
   std::unique_ptr<cc_ctx> c(new cc_ctx());
   c->opt = *opt;
   c->opt.nccl_id = nullptr;
@@ -239,6 +242,7 @@ void cc_destroy(cc_ctx *c) {
   cudaSetDevice(c->opt.device);
   if (c->s_main) cudaStreamSynchronize(c->s_main);
   if (c->s_comm) cudaStreamSynchronize(c->s_comm);
+  cc::devx_free(c);
   if (c->comm) cc::nccl().CommDestroy(c->comm);
   for (void *p : c->persistent) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);

@@ -30,6 +30,8 @@
 
 namespace cc {
 
+struct DevX;  // device-initiated exchange state (devx.cu)
+
 constexpr int kNStats = 15;  // cc_last_stats entries
 
 // Phases reported by cc_last_profile after "total": PROFILE order.
@@ -119,7 +121,10 @@ struct cc_ctx {
   unsigned *d_bad = nullptr;
   cc::Pass p_full, p_local, p_remote;  // world 1: p_full; world > 1: p_local + p_remote (+ p_full for hist)
   std::vector<cc::Pass> p_peer;        // ring exchange: the remote pass per source peer (replaces p_remote)
-  int xmode = 0;                       // exchange schedule in use: 0 none, CC_EXCHANGE_GROUPED / _RING
+  int xmode = 0;                       // exchange schedule in use: 0 none, CC_EXCHANGE_GROUPED / _RING / ...
+  int64_t a2a_rows = 0;
+  int64_t max_halo = 0;                // halo rows of the largest rank (window size)                // CC_EXCHANGE_ALLTOALL: rows per peer block (max over all rank pairs)
+  cc::DevX *devx = nullptr;            // CC_EXCHANGE_DEVICE: device communicator + halo window
   // column chunks: chunk_cols > 0 splits every neighbour sum's
   // passive columns into launches of that width; chunked (world > 1) then
   // exchanges halo rows per chunk into double buffers and tables keep only
@@ -276,6 +281,12 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
                const std::vector<int64_t> *dump_rows = nullptr, TableCache *cache = nullptr, bool capture = false);
 // cc_count_colorful through a captured CUDA graph (use_graphs, one rank)
 void count_graph(cc_ctx *c, double *X);
+// devx.cu: the device-initiated exchange (CC_EXCHANGE_DEVICE)
+void devx_init(cc_ctx *c, const std::vector<int64_t> &dst_row);
+void devx_free(cc_ctx *c);
+void *devx_window(cc_ctx *c, size_t bytes);
+void devx_put(cc_ctx *c, const void *P, int64_t ldP, int64_t c0, int64_t w, size_t win_off, int64_t ldH);
+cc_status device_selftest(int32_t device);
 void free_cache(cc_ctx *c, TableCache &cache);
 // X_j for colourings seed0 + j, j < iterations (replica mode with world > 1:
 // iteration j on rank j mod world, then one all-reduce of the vector).

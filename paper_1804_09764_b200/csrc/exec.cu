@@ -215,6 +215,22 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
     c->xmode = c->opt.exchange != CC_EXCHANGE_AUTO ? c->opt.exchange
                : c->xmodel[1] < c->xmodel[0]        ? CC_EXCHANGE_RING
                                                     : CC_EXCHANGE_GROUPED;
+    if (c->xmode == CC_EXCHANGE_ALLTOALL || c->xmode == CC_EXCHANGE_DEVICE) {
+      // every rank's receive offsets (row q of W + 1 entries), from one all-reduce
+      std::vector<double> v((size_t)W * (W + 1), 0.0);
+      for (int q = 0; q <= W; ++q) v[(size_t)me * (W + 1) + q] = (double)R.recv_off[q];
+      allreduce_host(c, v);
+      c->max_halo = 0;
+      c->a2a_rows = 0;
+      std::vector<int64_t> dst_row(W, 0);  // where this rank's rows start in peer q's halo
+      for (int p = 0; p < W; ++p) {
+        c->max_halo = std::max<int64_t>(c->max_halo, (int64_t)v[(size_t)p * (W + 1) + W]);
+        for (int q = 0; q < W; ++q)
+          c->a2a_rows = std::max<int64_t>(c->a2a_rows, (int64_t)(v[(size_t)p * (W + 1) + q + 1] - v[(size_t)p * (W + 1) + q]));
+      }
+      for (int q = 0; q < W; ++q) dst_row[q] = (int64_t)v[(size_t)q * (W + 1) + me];
+      if (c->xmode == CC_EXCHANGE_DEVICE) devx_init(c, dst_row);
+    }
     if (c->xmode == CC_EXCHANGE_RING) {
       // one remote pass per source peer: its neighbours of each owned row
       const int64_t n = R.n_own;
@@ -239,7 +255,8 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
     c->p_full.col_sorted = nullptr;
     c->d_col_sorted_full = nullptr;
   }
-  c->chunked = c->pworld() > 1 && c->chunk_cols > 0;
+  // device-initiated exchange: halo rows always in (double-buffered) windows
+  c->chunked = c->pworld() > 1 && (c->chunk_cols > 0 || c->xmode == CC_EXCHANGE_DEVICE);
   c->d_arrive = c->pmalloc<unsigned int>((size_t)std::max<int64_t>(c->max_hv, 1));
   c->arrive_cap = std::max<int64_t>(c->max_hv, 1);
   c->has_graph = true;
@@ -539,6 +556,28 @@ cudaEvent_t exchange_halo(cc_ctx *c, const void *P, int64_t ldP, int64_t c0, int
   const ncclDataType_t dt = elem == 8 ? ncclFloat64 : ncclFloat32;
   if (c->loop) {
     loopback_exchange(c, sendbuf, H, ldH, elem, steps);
+  } else if (c->xmode == CC_EXCHANGE_ALLTOALL) {
+    // ncclAlltoAll needs equal counts: per-peer blocks padded to the largest
+    // send count of any rank pair, then each block's rows moved into place
+    const int W = c->pworld();
+    if (!api.AlltoAll) throw Error(CC_ERR_NCCL, "this NCCL has no ncclAlltoAll");
+    const size_t blk = (size_t)c->a2a_rows * ldH * elem;
+    ScopedAsync sp(c, blk * W, c->s_comm), rp(c, blk * W, c->s_comm);
+    for (int q = 0; q < W; ++q) {
+      const int64_t ns = R.send_off[q + 1] - R.send_off[q];
+      if (q != c->opt.rank && ns)
+        CUDA_OK(cudaMemcpyAsync(static_cast<char *>(sp.p) + blk * q,
+                                static_cast<char *>(sendbuf) + (size_t)R.send_off[q] * ldH * elem,
+                                (size_t)ns * ldH * elem, cudaMemcpyDeviceToDevice, c->s_comm));
+    }
+    if (blk) NCCL_OK(api.AlltoAll(sp.p, rp.p, (size_t)c->a2a_rows * ldH, dt, c->comm, c->s_comm));
+    for (int q = 0; q < W; ++q) {
+      const int64_t nr = R.recv_off[q + 1] - R.recv_off[q];
+      if (q != c->opt.rank && nr)
+        CUDA_OK(cudaMemcpyAsync(static_cast<char *>(H) + (size_t)R.recv_off[q] * ldH * elem,
+                                static_cast<char *>(rp.p) + blk * q, (size_t)nr * ldH * elem,
+                                cudaMemcpyDeviceToDevice, c->s_comm));
+    }
   } else if (c->xmode == CC_EXCHANGE_RING) {
     // Alg. 3 lines 2-6: step r sends to rank + r and receives from rank - r
     const int W = c->pworld(), me = c->opt.rank;
@@ -641,11 +680,20 @@ void aggregate(cc_ctx *c, void *P, int64_t ldP, int p, void *N) {
     CUDA_OK(cudaStreamWaitEvent(c->s_main, recvd, 0));  // the send buffer's release is ordered after every step
     return;
   }
-  // chunked: double-buffered halo buffers of the chunk width
+  // chunked: double-buffered halo buffers of the chunk width (device-initiated
+  // exchange: the two halves of the registered window)
   const int64_t ldH = c->ld_of(chunks[0].second);
-  const size_t hbytes = (size_t)std::max<int64_t>(c->n_halo, 1) * ldH * elem;
-  ScopedAsync H0(c, hbytes, c->s_main), H1(c, chunks.size() > 1 ? hbytes : 0, c->s_main);
+  const bool devx = c->xmode == CC_EXCHANGE_DEVICE;
+  const size_t hbytes = (size_t)std::max<int64_t>(devx ? c->max_halo : c->n_halo, 1) * ldH * elem;
+  ScopedAsync H0(c, devx ? 0 : hbytes, c->s_main), H1(c, !devx && chunks.size() > 1 ? hbytes : 0, c->s_main);
   void *H[2] = {H0.p, H1.p ? H1.p : H0.p};
+  size_t hoff[2] = {0, 0};
+  if (devx) {
+    char *w = static_cast<char *>(devx_window(c, 2 * hbytes));
+    H[0] = w;
+    H[1] = w + hbytes;
+    hoff[1] = hbytes;
+  }
   cudaEvent_t hfree[2] = {nullptr, nullptr};
   comm_after_main(c);  // P produced and the halo buffers allocated
   cudaEvent_t recvd = nullptr;
@@ -653,7 +701,17 @@ void aggregate(cc_ctx *c, void *P, int64_t ldP, int p, void *N) {
     const int c0 = chunks[i].first, w = chunks[i].second;
     if (hfree[i % 2]) CUDA_OK(cudaStreamWaitEvent(c->s_comm, hfree[i % 2], 0));  // chunk i - 2 summed
     std::vector<std::pair<int, cudaEvent_t>> steps;
-    recvd = exchange_halo(c, P, ldP, c0, w, H[i % 2], ldH, ring ? &steps : nullptr);
+    if (devx) {  // the pack kernel stores into the peers' windows (LSA barriers inside)
+      cudaEvent_t xb = c->begin(c->s_comm);
+      devx_put(c, P, ldP, c0, w, hoff[i % 2], ldH);
+      c->end(PH_EXCHANGE, c->s_comm, xb);
+      recvd = c->ev();
+      CUDA_OK(cudaEventRecord(recvd, c->s_comm));
+      c->stats[1] += (double)c->part.send_off[c->pworld()] * w * elem * 2;
+      c->stats[9] += (double)c->part.recv_off[c->pworld()] * w * elem;
+    } else {
+      recvd = exchange_halo(c, P, ldP, c0, w, H[i % 2], ldH, ring ? &steps : nullptr);
+    }
     gather_pass(c, c->p_local, table_src(P, ldP, c0, w, elem), p, N, i > 0, nullptr, c->gather_sms(true));
     if (!ring) steps.push_back({-1, recvd});
     // the remote rows of this chunk: halo row j at H + j * ldH, i.e. table row n_own + j

@@ -1,5 +1,6 @@
 // nccl_dl.cpp -- dlopen/dlsym of the NCCL entry points used by the halo
-// exchange (grouped ncclSend/ncclRecv) and the final 1-double all-reduce.
+// exchange (grouped ncclSend/ncclRecv, ncclAlltoAll, the device API's
+// symmetric windows) and the final 1-double all-reduce.
 #include "nccl_dl.h"
 
 #include <dlfcn.h>
@@ -35,6 +36,11 @@ NcclApi &nccl() {
               sym(h, "ncclRecv", api.Recv) && sym(h, "ncclGroupStart", api.GroupStart) &&
               sym(h, "ncclGroupEnd", api.GroupEnd) && sym(h, "ncclAllReduce", api.AllReduce) &&
               sym(h, "ncclGetErrorString", api.GetErrorString);
+    sym(h, "ncclAlltoAll", api.AlltoAll);
+    api.dev_ok = sym(h, "ncclMemAlloc", api.MemAlloc) && sym(h, "ncclMemFree", api.MemFree) &&
+                 sym(h, "ncclCommWindowRegister", api.CommWindowRegister) &&
+                 sym(h, "ncclCommWindowDeregister", api.CommWindowDeregister) &&
+                 sym(h, "ncclDevCommCreate", api.DevCommCreate) && sym(h, "ncclDevCommDestroy", api.DevCommDestroy);
     api.ok = ok;
     api.why = ok ? "" : "libnccl.so.2 lacks a required symbol";
   });

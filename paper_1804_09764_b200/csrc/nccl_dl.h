@@ -6,6 +6,9 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+struct ncclDevComm;              // nccl_device/core.h (device API, NCCL >= 2.28)
+struct ncclDevCommRequirements;
+
 namespace cc {
 
 struct NcclApi {
@@ -22,6 +25,16 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*AlltoAll)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  // device API (NCCL >= 2.28): symmetric windows + device communicator; dev_ok
+  // when every entry point below resolved
+  bool dev_ok = false;
+  ncclResult_t (*MemAlloc)(void **, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void *) = nullptr;
+  ncclResult_t (*CommWindowRegister)(ncclComm_t, void *, size_t, ncclWindow_t *, int) = nullptr;
+  ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+  ncclResult_t (*DevCommCreate)(ncclComm_t, const struct ncclDevCommRequirements *, struct ncclDevComm *) = nullptr;
+  ncclResult_t (*DevCommDestroy)(ncclComm_t, const struct ncclDevComm *) = nullptr;
 };
 
 NcclApi &nccl();

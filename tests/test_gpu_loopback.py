@@ -199,7 +199,7 @@ def test_ranks_plan_from_the_global_degree():
         assert rel_err(got[0], want) <= 1e-12, (world, got[0], want)
 
 
-@pytest.mark.parametrize("world,exchange", [(2, 1), (3, 1), (3, 2), (4, 2)])
+@pytest.mark.parametrize("world,exchange", [(2, 1), (3, 1), (3, 2), (4, 2), (3, 3)])
 def test_chunked_exchange_equals_the_oracle(world, exchange):
     """chunk_cols > 0 with the 1D partition: per column chunk the boundary
     rows are packed, exchanged into one of two chunk-wide halo buffers and

@@ -108,7 +108,7 @@ def _worlds():
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 CUDA devices (one rank per GPU)")
 @pytest.mark.parametrize("case", list(CASES))
-@pytest.mark.parametrize("exchange", [1, 2])  # CC_EXCHANGE_GROUPED, CC_EXCHANGE_RING
+@pytest.mark.parametrize("exchange", [1, 2, 3, 4])  # grouped, ring, ncclAlltoAll, device-initiated stores
 def test_nccl_partitioned_counts_equal_the_oracle(case, exchange):
     want = _want(case)
     tol = TOL_FP64 if CASES[case][2] == "fp64" else TOL_FP32
@@ -121,3 +121,16 @@ def test_nccl_partitioned_counts_equal_the_oracle(case, exchange):
                 for j, (x, w) in enumerate(zip(xs, want)):
                     assert abs(x - w) <= tol * abs(w), (case, world, exchange, chunk, rank, j, x, w)
             assert all(o[1] == out[0][1] for o in out), "ranks disagree"
+
+
+def test_nccl_device_api_one_rank_selftest():
+    """The device-initiated exchange's machinery (NCCL >= 2.28 device API) on a
+    one-rank communicator: symmetric window, device communicator with LSA
+    barriers, stores through ncclGetLsaPointer, barrier, read back.  Runs on
+    one GPU (no second rank is emulated)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_09764_b200 as cc
+    cc.cc_nccl_device_selftest(0)
+    cc.cc_nccl_selftest(0)
