@@ -922,6 +922,141 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
   }
 }
 
+// ------------------------------------------------------------------ gather, wide rows, short lists
+// The items with <= 32 neighbours (most items of an R-MAT graph; measured:
+// 78% of configs[3]'s items, 14.7 of the p = 5 gather's 69 ms for 7% of its
+// DRAM bytes): the lean kernel waits for every colour group in turn (its ids,
+// then its rows), several dependent round trips per item.  Here a warp
+// loads the whole stream's ids at once (one coalesced load; <= 32 rows), then
+// issues the rows B at a time ACROSS colour-group boundaries and walks them
+// in order, expanding a group's sum into N'' when the colour changes.  Same
+// sums in the same order as the lean kernel (fp32 blocks of one colour group,
+// then the N'' row); no sector skipping (whole rows).
+template <typename T, int NV, int B, typename AccT>
+__global__ void __launch_bounds__(128) k_gather_short(GatherArgs a, int nch) {
+  using V = typename Vec<T>::type;
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = 32 * NV * VW;  // columns per pass
+  extern __shared__ __align__(16) unsigned char sacc_raw[];
+  const int lane = threadIdx.x & 31;
+  AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)a.W_out;
+  const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const char *__restrict__ srcb = static_cast<const char *>(a.src);
+  const uint32_t ld_bytes = (uint32_t)(a.ld_src * sizeof(T));
+
+  int64_t it = a.item_from + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int4 dx = make_int4(0, 0, 0, 0), dy = make_int4(0, 0, 0, 0);
+  int go_n = 0;
+  if (it < n_items) load_desc(a, it, lane, dx, dy, go_n);
+  for (; it < n_items; it += nw) {
+    const int64_t b = (int64_t)(((uint64_t)(uint32_t)dx.y << 32) | (uint32_t)dx.x);
+    const int32_t v = dx.z;
+    const int n_s = dx.w, cv_lo = dy.x, skip = dy.y, cv = dy.z;
+    const int go = go_n;  // lane j < 16: end of colour group j (item positions)
+    if (it + nw < n_items) load_desc(a, it + nw, lane, dx, dy, go_n);  // prefetch the next item
+    // the stream (the item's neighbours minus v's own colour group): ids and colours, one lane each
+    const int ip = lane < cv_lo ? lane : lane + skip;  // item position of stream position lane
+    const int32_t my_u = lane < n_s ? __ldg(a.col + b + ip) : 0;
+    int my_cu = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) my_cu += (j < a.k) && (__shfl_sync(0xffffffffu, go, j) <= ip);
+    for (int j = lane; j < a.W_out; j += 32) sacc[j] = (AccT)0;
+    __syncwarp();
+    for (int ch = 0; ch < nch; ++ch) {
+      const int c0 = ch * CAP + lane * VW;
+      bool valid[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) valid[j] = c0 + j * 32 * VW < a.W_in;
+      const char *lbase = srcb + (size_t)c0 * sizeof(T);
+      int cur = -1;
+      uint16_t m[NV][VW];
+      V blk[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) zero_vec(blk[j]);
+      auto flush = [&]() {  // the colour group's block sum into N'' (fp32 block, then the N'' row)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const double e[4] = {(double)vec_at(blk[j], 0), (double)vec_at(blk[j], 1), (double)vec_at(blk[j], 2 % VW),
+                               (double)vec_at(blk[j], 3 % VW)};
+#pragma unroll
+          for (int q = 0; q < VW; ++q)
+            if (m[j][q] != 0xFFFF) sacc[m[j][q]] += (AccT)(e[q] * AccScale<AccT>::in);
+          zero_vec(blk[j]);
+        }
+      };
+      for (int r0 = 0; r0 < n_s; r0 += B) {
+        V x[B][NV];
+#pragma unroll
+        for (int bb = 0; bb < B; ++bb) {  // B rows in flight, whatever their colour groups
+          const int r = r0 + bb;
+          const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, r & 31);
+          const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            if (r < n_s && valid[j]) x[bb][j] = __ldg(row + 32 * j);
+            else zero_vec(x[bb][j]);
+          }
+        }
+#pragma unroll
+        for (int bb = 0; bb < B; ++bb) {
+          const int r = r0 + bb;
+          const int cu = __shfl_sync(0xffffffffu, my_cu, r & 31);
+          if (r < n_s && cu != cur) {  // warp-uniform: a new colour group
+            if (cur >= 0) flush();
+            __syncwarp();  // groups of different colours may map to the same N'' entries
+            cur = cu;
+            const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              if (valid[j]) {
+                if constexpr (VW == 4) {
+                  const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + c0 + j * 32 * VW));
+                  m[j][0] = w.x & 0xFFFF;
+                  m[j][1 % VW] = w.x >> 16;
+                  m[j][2 % VW] = w.y & 0xFFFF;
+                  m[j][3 % VW] = w.y >> 16;
+                } else {
+                  const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + c0 + j * 32 * VW));
+                  m[j][0] = w & 0xFFFF;
+                  m[j][1 % VW] = w >> 16;
+                }
+              } else {
+#pragma unroll
+                for (int q = 0; q < VW; ++q) m[j][q] = 0xFFFF;
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < NV; ++j) add_same(blk[j], x[bb][j]);
+        }
+      }
+      if (cur >= 0) flush();
+      __syncwarp();
+    }
+    if (a.root_mode) root_epilogue<T, AccT>(a, sacc, it, v, false, lane);
+    else gather_epilogue<T, 32, AccT>(a, sacc, it, v, false, lane, 0xffffffffu);
+    __syncwarp();
+  }
+}
+
+template <typename T, int NV, int B>
+void short_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int CAP = 32 * NV * VW;
+  const bool acc32 = sizeof(T) == 4 && (a.W_out > 1600 || (kn.acc32 && !a.root_mode));
+  auto kern = acc32 ? k_gather_short<T, NV, B, float> : k_gather_short<T, NV, B, double>;
+  const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
+  int warps = 4;
+  while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
+  const int threads = warps * 32;
+  const size_t smem = row * warps;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, threads, smem, num_sms);
+  const int nch = (a.W_in + CAP - 1) / CAP;
+  kern<<<grid, threads, smem, s>>>(a, nch);
+}
+
 template <typename T, int G, int NV, int U>
 void rows_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
@@ -994,6 +1129,53 @@ int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t
   // exists in the lean kernel only.
   const bool lean = kn.gather_impl ? kn.gather_impl == 2 : wvec > 16;
   if (lean || a.root_mode) {
+    const int64_t to = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
+    if (a.lean_split > a.item_from && a.lean_split < to) {  // two launches: long lists, short tail
+      GatherArgs h = a, t = a;
+      h.item_to = a.lean_split;
+      h.lean_split = -1;
+      t.item_from = a.lean_split;
+      t.lean_split = -1;
+      return gather_typed<T>(h, kn, num_sms, s) + gather_typed<T>(t, kn, num_sms, s);
+    }
+    // the items with <= 32 neighbours on the short-list kernel (knob short_lists)
+    if (kn.short_lists && a.short_from < to) {
+      const int64_t sf = std::max(a.short_from, a.item_from);
+      int launches = 0;
+      if (a.item_from < sf) {
+        GatherArgs h = a;
+        h.item_to = sf;
+        h.short_from = to;  // (no further split)
+        launches += gather_typed<T>(h, kn, num_sms, s);
+      }
+      GatherArgs t = a;
+      t.item_from = sf;
+      t.item_to = to;
+      if (kn.short_lists == 1) {
+        if (wvec <= 32) short_go<T, 1, 8>(t, kn, num_sms, s);
+        else if (wvec <= 64) short_go<T, 2, 8>(t, kn, num_sms, s);
+        else if (wvec <= 96) short_go<T, 3, 6>(t, kn, num_sms, s);
+        else short_go<T, 4, 4>(t, kn, num_sms, s);
+      } else if (kn.short_lists == 2) {  // the lean kernel, fewer rows in flight, more warps
+        // (configs[3]: 155.8 -> 149.0 ms per colouring with the tail at <= 128 neighbours;
+        // rows of > 96 vectors keep the long-list kernel: 3 CTAs would spill)
+        if (wvec <= 32) ldg_go<T, 1, 2, 3>(t, kn, num_sms, s);
+        else if (wvec <= 64) ldg_go<T, 2, 2, 3>(t, kn, num_sms, s);
+        else if (wvec <= 96) ldg_go<T, 3, 2, 3>(t, kn, num_sms, s);
+        else ldg_go<T, 4, 2>(t, kn, num_sms, s);
+      } else if (kn.short_lists == 4) {  // U = 3 at 3 CTAs/SM
+        if (wvec <= 32) ldg_go<T, 1, 3, 3>(t, kn, num_sms, s);
+        else if (wvec <= 64) ldg_go<T, 2, 3, 3>(t, kn, num_sms, s);
+        else if (wvec <= 96) ldg_go<T, 3, 3, 3>(t, kn, num_sms, s);
+        else ldg_go<T, 4, 2, 3>(t, kn, num_sms, s);
+      } else {
+        if (wvec <= 32) ldg_go<T, 1, 1, 4>(t, kn, num_sms, s);
+        else if (wvec <= 64) ldg_go<T, 2, 1, 4>(t, kn, num_sms, s);
+        else if (wvec <= 96) ldg_go<T, 3, 1, 4>(t, kn, num_sms, s);
+        else ldg_go<T, 4, 1, 4>(t, kn, num_sms, s);
+      }
+      return launches + 1;
+    }
     if (wvec <= 32) ldg_go<T, 1, 8>(a, kn, num_sms, s);
     else if (wvec <= 64) ldg_go<T, 2, 8>(a, kn, num_sms, s);
     else if (wvec <= 96) ldg_go<T, 3, 4>(a, kn, num_sms, s);

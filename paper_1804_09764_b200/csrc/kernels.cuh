@@ -36,6 +36,12 @@ struct Knobs {
                            //                  (-1 = auto: 8 when world > 1 over NCCL, else 0)
   int nvtx_mark = 0;       // CC_NVTX_MARK: i > 0 = the i-th neighbour-sum pass of a count runs inside
                            //               the NVTX range "cc_dominant" (one-launch ncu measurement)
+  int short_lists = 2;     // CC_SHORT_LISTS: the short tail of wide-row gathers: 0 = with the long lists,
+                           //   1 = k_gather_short, 2 = lean kernel U = 2 at 3 CTAs/SM (measured best),
+                           //   3 = U = 1 at 4 CTAs/SM, 4 = U = 3 at 3 CTAs/SM
+  int short_split = 4;     // CC_SHORT_SPLIT: q, the short tail = light items with <= 8 << q neighbours
+  int lean_split = -1;     // CC_LEAN_SPLIT: q >= 0 = wide-row gathers run as two launches, the items with
+                           //   more than 8 << q neighbours and the rest (measurement of the short tail)
   int layout = 0;          // CC_LAYOUT: column order of tables of >= 3 vertices (R-3): 0 = colex;
                            //   L = 1, 2, 3: groups of 32 << (L-1) bytes whose sets share the most colours
   int tail_batches = 0;    // CC_TAIL_BATCHES: > 0 forces the memory plan's row batches (0 = by memory)
@@ -87,6 +93,8 @@ struct GatherArgs {
   int64_t item_from = 0;  // this launch takes items [item_from, item_to) (a row batch, or the
   int64_t item_to = -1;   // narrow kernels' split of the list); -1: all items
   int64_t item_split = 0; // first light item with <= 32 neighbours (items are in degree order)
+  int64_t lean_split = -1; // knob lean_split: the lean kernel runs as two launches split at this item
+  int64_t short_from = -1; // first light item with <= 32 neighbours (wide rows: the short-list kernel); -1: none
   const uint16_t *map;    // [c_u][c_v][map_ld] -> rank of Y'' in C(k-1, p), 0xFFFF = unusable
   int64_t map_ld;         // map row stride (multiple of 8 entries, padding = 0xFFFF)
   const uint32_t *skip = nullptr;  // [k-1][skip_words]: bit v of word w set = 16-byte vector 32 w + v of a

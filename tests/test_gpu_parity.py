@@ -607,7 +607,7 @@ def test_fp32_overflow_is_reported_nonfinite():
 KNOB_SETTINGS = [("gather_impl", 1), ("gather_impl", 2), ("narrow_impl", 0), ("narrow_impl", 1),
                  ("narrow_split", 0), ("narrow_split", 7), ("csort_small", 0), ("sector_skip", 0),
                  ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("acc32", 0),
-                 ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1)]
+                 ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1), ("short_lists", 0), ("short_lists", 1), ("short_lists", 3), ("short_split", 1), ("lean_split", 2)]
 
 
 @pytest.mark.parametrize("ci", [2, 3, 4])
