@@ -1057,7 +1057,7 @@ void short_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s)
   kern<<<grid, threads, smem, s>>>(a, nch);
 }
 
-template <typename T, int G, int NV, int U>
+template <typename T, int G, int NV, int U, int MINB = 3>
 void rows_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
@@ -1065,7 +1065,7 @@ void rows_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) 
   // configs[3] -1 to -2% against 2 CTAs (profiles/r1/SUMMARY.md)
   // fp32 tables: fp32 shared-memory rows as in the lean gather (C-6)
   const bool acc32 = sizeof(T) == 4 && kn.acc32;
-  auto kern = acc32 ? k_gather_rows<T, G, NV, U, 3, float> : k_gather_rows<T, G, NV, U, 3, double>;
+  auto kern = acc32 ? k_gather_rows<T, G, NV, U, MINB, float> : k_gather_rows<T, G, NV, U, MINB, double>;
   const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
@@ -1194,9 +1194,19 @@ int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t
     t.item_to = to;
     int launches = 0;
     if (h.item_from < h.item_to) {
-      if (wvec <= 4) rows_go<T, 4, 1, 4>(h, kn, num_sms, s);
-      else if (wvec <= 8) rows_go<T, 8, 1, 4>(h, kn, num_sms, s);
-      else rows_go<T, 8, 2, 4>(h, kn, num_sms, s);
+      if (kn.rows_variant == 1) {  // fewer rows in flight, more warps
+        if (wvec <= 4) rows_go<T, 4, 1, 2, 4>(h, kn, num_sms, s);
+        else if (wvec <= 8) rows_go<T, 8, 1, 2, 4>(h, kn, num_sms, s);
+        else rows_go<T, 8, 2, 2, 4>(h, kn, num_sms, s);
+      } else if (kn.rows_variant == 2) {  // more rows in flight
+        if (wvec <= 4) rows_go<T, 4, 1, 8, 2>(h, kn, num_sms, s);
+        else if (wvec <= 8) rows_go<T, 8, 1, 8, 2>(h, kn, num_sms, s);
+        else rows_go<T, 8, 2, 8, 2>(h, kn, num_sms, s);
+      } else {
+        if (wvec <= 4) rows_go<T, 4, 1, 4>(h, kn, num_sms, s);
+        else if (wvec <= 8) rows_go<T, 8, 1, 4>(h, kn, num_sms, s);
+        else rows_go<T, 8, 2, 4>(h, kn, num_sms, s);
+      }
       ++launches;
     }
     if (t.item_from < t.item_to) {

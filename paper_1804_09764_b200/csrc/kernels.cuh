@@ -39,6 +39,8 @@ struct Knobs {
   int short_lists = 2;     // CC_SHORT_LISTS: the short tail of wide-row gathers: 0 = with the long lists,
                            //   1 = k_gather_short, 2 = lean kernel U = 2 at 3 CTAs/SM (measured best),
                            //   3 = U = 1 at 4 CTAs/SM, 4 = U = 3 at 3 CTAs/SM
+  int rows_variant = 0;    // CC_ROWS_VARIANT: row-parallel narrow kernel: 0 = U 4 at 3 CTAs/SM,
+                           //   1 = U 2 at 4 CTAs/SM, 2 = U 8 at 2 CTAs/SM
   int short_split = 4;     // CC_SHORT_SPLIT: q, the short tail = light items with <= 8 << q neighbours
   int lean_split = -1;     // CC_LEAN_SPLIT: q >= 0 = wide-row gathers run as two launches, the items with
                            //   more than 8 << q neighbours and the rest (measurement of the short tail)
