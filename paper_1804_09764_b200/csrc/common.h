@@ -127,11 +127,17 @@ double plan_cost(const Plan &P, const PlanOpts &o);
 // ---------------------------------------------------------------- graph.cpp
 // Validated CSR (copy) of the global graph.
 struct HostGraph {
-  int64_t n = 0;
-  std::vector<int64_t> rp;
-  std::vector<int32_t> col;
+  int64_t n = 0, nnz = 0;
+  const int64_t *rp = nullptr;  // n + 1 offsets: the caller's array (read only), valid during the call
+  const int32_t *col = nullptr; // nnz ids: the caller's array when every row is sorted, else col_own
+  std::vector<int64_t> rp_own;  // (n == 0: {0})
+  std::vector<int32_t> col_own; // a sorted copy, only when some row was not sorted
+  HostGraph() = default;
+  HostGraph(HostGraph &&) = default;
+  HostGraph(const HostGraph &) = delete;
 };
-// Validate (throws Error(CC_ERR_GRAPH)) and copy with rows sorted.
+// Validate (throws Error(CC_ERR_GRAPH)); the caller's arrays are used in
+// place (no copy of a multi-GB CSR per rank) unless a row must be sorted.
 HostGraph validate_graph(int64_t n, const int64_t *row_ptr, const int32_t *col);
 
 // The 1D vertex partition of one rank (Alg. 2 line 2; lines 374-382).

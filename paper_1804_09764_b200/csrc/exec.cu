@@ -168,7 +168,7 @@ void load_graph(cc_ctx *c, const HostGraph &g) {
   {
     int64_t nz = 0;
     for (int64_t v = 0; v < g.n; ++v) nz += g.rp[v + 1] > g.rp[v];
-    c->avg_degree = nz ? (double)g.col.size() / (double)nz : 0.0;
+    c->avg_degree = nz ? (double)g.nnz / (double)nz : 0.0;
   }
   c->n_own = R.n_own;
   c->n_halo = R.n_halo;

@@ -33,27 +33,39 @@ HostGraph validate_graph(int64_t n, const int64_t *row_ptr, const int32_t *col) 
   if (n > 0 && !row_ptr) throw Error(CC_ERR_ARG, "row_ptr is NULL");
   HostGraph g;
   g.n = n;
-  g.rp.assign(row_ptr, row_ptr + n + 1);
   if (n == 0) {
-    g.rp.assign(1, 0);
+    g.rp_own.assign(1, 0);
+    g.rp = g.rp_own.data();
     return g;
   }
+  g.rp = row_ptr;
   if (g.rp[0] != 0) throw Error(CC_ERR_GRAPH, "row_ptr[0] != 0");
   for (int64_t v = 0; v < n; ++v)
     if (g.rp[v + 1] < g.rp[v]) throw Error(CC_ERR_GRAPH, "row_ptr decreases at row " + std::to_string(v));
   const int64_t nnz = g.rp[n];
+  g.nnz = nnz;
   if (nnz > 0 && !col) throw Error(CC_ERR_ARG, "col is NULL");
-  g.col.assign(col, col + nnz);
+  // rows sorted already (the usual case): validate the caller's array in place
+  int64_t unsorted = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : unsorted)
+  for (int64_t v = 0; v < n; ++v) unsorted += !std::is_sorted(col + g.rp[v], col + g.rp[v + 1]);
+  if (unsorted) {
+    g.col_own.assign(col, col + nnz);
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t v = 0; v < n; ++v) std::sort(g.col_own.data() + g.rp[v], g.col_own.data() + g.rp[v + 1]);
+    g.col = g.col_own.data();
+  } else {
+    g.col = col;
+  }
   int64_t bad_range = INT64_MAX, bad_loop = INT64_MAX, bad_dup = INT64_MAX, bad_sym = INT64_MAX;
 #pragma omp parallel for schedule(dynamic, 4096) reduction(min : bad_range, bad_loop, bad_dup)
   for (int64_t v = 0; v < n; ++v) {
-    int32_t *b = g.col.data() + g.rp[v], *e = g.col.data() + g.rp[v + 1];
+    const int32_t *b = g.col + g.rp[v], *e = g.col + g.rp[v + 1];
     bool range_ok = true;
-    for (int32_t *p = b; p < e; ++p)
+    for (const int32_t *p = b; p < e; ++p)
       if (*p < 0 || *p >= n) range_ok = false;
     if (!range_ok) { bad_range = std::min<int64_t>(bad_range, v); continue; }
-    if (!std::is_sorted(b, e)) std::sort(b, e);
-    for (int32_t *p = b; p < e; ++p) {
+    for (const int32_t *p = b; p < e; ++p) {
       if (*p == v) bad_loop = std::min<int64_t>(bad_loop, v);
       if (p > b && p[-1] == *p) bad_dup = std::min<int64_t>(bad_dup, v);
     }
@@ -65,7 +77,7 @@ HostGraph validate_graph(int64_t n, const int64_t *row_ptr, const int32_t *col) 
   for (int64_t v = 0; v < n; ++v) {
     for (int64_t e = g.rp[v]; e < g.rp[v + 1]; ++e) {
       int32_t u = g.col[e];
-      if (!std::binary_search(g.col.data() + g.rp[u], g.col.data() + g.rp[u + 1], (int32_t)v)) {
+      if (!std::binary_search(g.col + g.rp[u], g.col + g.rp[u + 1], (int32_t)v)) {
         bad_sym = std::min<int64_t>(bad_sym, v);
         break;
       }

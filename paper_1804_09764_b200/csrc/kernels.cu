@@ -115,6 +115,61 @@ __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_
   }
 }
 
+// Warp-per-vertex combine for low-intensity steps (few split terms per output,
+// e.g. the p = 1 steps (t; t-1, 1): t - 1 terms): the split-table slice of the
+// outputs [o_lo, o_hi) sits in shared memory once per CTA; each warp stages
+// its vertex's A' and N'' rows in shared memory (one coalesced load each, the
+// next vertex's already in registers), then a lane per output walks its split
+// pairs and the outputs go out coalesced.  Latency of the row loads is hidden
+// by the next vertex's prefetch and by 16 warps per SM.
+template <typename T, int PF>
+__global__ void __launch_bounds__(256) k_combine_warp(const T *__restrict__ A, int64_t ldA, int WA,
+                                                      const T *__restrict__ N, int64_t ldN, int WN,
+                                                      const uint32_t *__restrict__ split, int nq, int64_t n,
+                                                      T *__restrict__ out, int64_t ldO, int WO, int o_lo, int o_hi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int WOp = (WO + 7) & ~7, nout = o_hi - o_lo;
+  uint32_t *ss = reinterpret_cast<uint32_t *>(smem_raw);  // [q][nout]
+  for (int i = threadIdx.x; i < nq * nout; i += blockDim.x) {
+    const int q = i / nout, o = i - q * nout;
+    ss[i] = split[(int64_t)q * WOp + o_lo + o];
+  }
+  T *rows = reinterpret_cast<T *>(smem_raw + (((size_t)nq * nout * 4 + 15) & ~(size_t)15)) + (size_t)warp * (WA + WN);
+  __syncthreads();
+  const int64_t nw = (int64_t)gridDim.x * nwarp;
+  int64_t v = (int64_t)blockIdx.x * nwarp + warp;
+  T pa[PF], pn[PF];  // the next vertex's rows, lane-strided
+  auto fetch = [&](int64_t u) {
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+      const int x = lane + 32 * i;
+      pa[i] = (u < n && x < WA) ? __ldg(A + u * ldA + x) : (T)0;
+      pn[i] = (u < n && x < WN) ? __ldg(N + u * ldN + x) : (T)0;
+    }
+  };
+  fetch(v);
+  for (; v < n; v += nw) {
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+      const int x = lane + 32 * i;
+      if (x < WA) rows[x] = pa[i];
+      if (x < WN) rows[WA + x] = pn[i];
+    }
+    __syncwarp();
+    fetch(v + nw);  // the next vertex's rows are in flight during this one's split walk
+    for (int o = lane; o < nout; o += 32) {
+      T acc = (T)0;
+      for (int q = 0; q < nq; ++q) {
+        const uint32_t sp = ss[q * nout + o];
+        acc = fma(rows[sp & 0xFFFF], rows[WA + (sp >> 16)], acc);
+      }
+      out[v * ldO + o_lo + o] = acc;
+    }
+    __syncwarp();
+  }
+}
+
 // Lane-per-vertex combine (persistent, one CTA of 8 warps per SM): tiles of
 // 32 vertices' A' and N'' rows are staged TRANSPOSED in shared memory as
 // [column][33] by cp.async (double-buffered: tile i+1 streams in while tile i
@@ -585,6 +640,24 @@ int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN
       kern<<<grid, 512, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq,
                                    n, static_cast<T *>(out), ldO, WO, nbuf, o0, std::min(chunk, o_hi - o0));
     return launches;
+  }
+  // low-intensity steps with short rows: warp per vertex (knob combine_impl 4;
+  // auto when the rows fit a warp's prefetch registers and the split slice fits)
+  {
+    const int nout = o_hi - o_lo;
+    const size_t ssb = ((size_t)nq * nout * 4 + 15) & ~(size_t)15;
+    const size_t smem = ssb + (size_t)8 * (WA + WN) * sizeof(T);
+    const bool warp_ok = kn.combine_impl == 4 || (kn.combine_impl == 0 && WA <= 128 && WN <= 128);
+    if (warp_ok && WA <= 128 && WN <= 128 && smem <= 200 * 1024) {
+      auto kern = (WA <= 32 && WN <= 32)   ? k_combine_warp<T, 1>
+                  : (WA <= 64 && WN <= 64) ? k_combine_warp<T, 2>
+                                           : k_combine_warp<T, 4>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int grid = persistent_grid(kern, 256, smem, num_sms);
+      kern<<<grid, 256, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, nq,
+                                   n, static_cast<T *>(out), ldO, WO, o_lo, o_hi);
+      return 1;
+    }
   }
   // wide rows: tile of V vertices (padded rows); k <= 16 bounds a row by
   // 2 x C(15,7) entries, so the smallest tile always fits in 227 KB

@@ -28,7 +28,7 @@ struct Knobs {
                            //                 1 = row-parallel only
   int narrow_split = -1;   // CC_NARROW_SPLIT: log2(T/8), items with > T neighbours row-parallel; -1 = auto
   int csort_small = 1;     // CC_CSORT_SMALL: 0 = no separate kernel for the <= 8-neighbour items
-  int combine_impl = 0;    // CC_COMBINE_IMPL: 0 = auto, 1 = Z-block, 2 = lane, 3 = V-tile
+  int combine_impl = 0;    // CC_COMBINE_IMPL: 0 = auto, 1 = Z-block, 2 = lane, 3 = V-tile, 4 = warp per vertex
   int acc32 = 1;           // CC_ACC32: fp32 tables keep the shared-memory N'' rows in fp32 (scaled)
   int phase_events = 1;    // CC_PHASE_EVENTS: per-kernel events for cc_last_profile
   int hub_l2_pct = 50;     // CC_HUB_L2_PCT: % of the L2 given an evict-last policy for hub rows (rings)

@@ -237,12 +237,11 @@ def test_k16_template_with_7_vertex_subtrees_runs_on_one_gpu(graph4):
     samples = _root_samples(g, 3)
     with context(g, PAR16, "fp64", fixed_root=1) as ctx:
         cc.cc_color(ctx, 2)
-        x = cc.cc_count_colorful(ctx)
+        rows = cc.cc_get_subtree_rows(ctx, 0, samples, k, k)[:, 0]  # one whole count, X_v kept
         st = cc.cc_last_stats(ctx)
-        assert math.isfinite(x) and x > 0
         assert st["tail_batches"] >= 2 and st["recompute_cols"] > 0, st
         assert st["peak_table_bytes"] < 180e9
-        rows = cc.cc_get_subtree_rows(ctx, 0, samples, k, k)[:, 0]
+    assert np.all(np.isfinite(rows)) and np.all(rows >= 0)
     col = oracle.color(g.n, k, 2)
     want = [oracle.dp_root_at(g, PAR16, col, v, oracle.NUM_LONGDOUBLE) for v in samples]
     assert any(w > 0 for w in want)

@@ -558,7 +558,7 @@ def test_options_and_hooks_are_validated():
         cc.cc_create(device=0, replicas=2)
     assert e.value.status == cc.CC_ERR_ARG
     with pytest.raises(cc.CCError) as e:
-        cc.cc_create(device=0, exchange=3)  # CC_EXCHANGE_AUTO / _GROUPED / _RING only
+        cc.cc_create(device=0, exchange=5)  # CC_EXCHANGE_AUTO .. CC_EXCHANGE_DEVICE only
     assert e.value.status == cc.CC_ERR_ARG
     g = synth.gnp(50, 0.2, 1)
     with context(g, [-1, 0, 1, 2]) as ctx:  # P4: a p = 2 neighbour sum under every root
@@ -606,7 +606,7 @@ def test_fp32_overflow_is_reported_nonfinite():
 
 KNOB_SETTINGS = [("gather_impl", 1), ("gather_impl", 2), ("narrow_impl", 0), ("narrow_impl", 1),
                  ("narrow_split", 0), ("narrow_split", 7), ("csort_small", 0), ("sector_skip", 0),
-                 ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("acc32", 0),
+                 ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("combine_impl", 4), ("acc32", 0),
                  ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1), ("short_lists", 0), ("short_lists", 1), ("short_lists", 3), ("short_split", 1), ("lean_split", 2)]
 
 
