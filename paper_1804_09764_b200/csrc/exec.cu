@@ -428,7 +428,8 @@ void gather_pass(cc_ctx *c, Pass &w, const Src &src, int p, void *N, int accumul
     if (c->knobs.narrow_split >= 0) q = std::min(7, c->knobs.narrow_split);
     a.item_split = w.seg_len > (8 << q) ? w.split[q] : 0;
     if (c->knobs.lean_split >= 0) a.lean_split = w.split[std::min(7, c->knobs.lean_split)];
-    a.short_from = w.split[std::min(7, std::max(0, c->knobs.short_split))];  // first light item of the short tail
+    // first light item of the short tail (k_gather_short takes <= 32 neighbours: one id per lane)
+    a.short_from = w.split[std::min(c->knobs.short_lists == 1 ? 2 : 7, std::max(0, c->knobs.short_split))];
   }
   a.map = c->d_map[p];
   a.map_ld = gather_map_ld(k, p);
