@@ -322,7 +322,9 @@ cc_status cc_last_profile(cc_ctx *ctx, double *ms, int32_t cap, int32_t *n);
  * (0: none), out[12] = row batches of the memory plan's tail (0: none),
  * out[13] = column width of the tail's recomputed passive table (0: none),
  * out[14] (cap >= 15) = 1-based ordinal of the longest neighbour-sum pass
- * among the count's passes (the knob nvtx_mark selects a pass by it).
+ * among the count's passes (the knob nvtx_mark selects a pass by it),
+ * out[15] (cap >= 16) = sibling pairs: narrow neighbour sums taken along in
+ * the traversal of another (one rank; knob pair_gather).
  * cap >= 5. */
 cc_status cc_last_stats(cc_ctx *ctx, double *out, int32_t cap);
 

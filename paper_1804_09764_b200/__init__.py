@@ -219,12 +219,12 @@ def cc_get_subtree_rows(ctx, x: int, vertices, k: int, s: int) -> np.ndarray:
 
 
 def cc_last_stats(ctx) -> dict:
-    buf = np.zeros(15, dtype=np.float64)
-    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 15))
+    buf = np.zeros(16, dtype=np.float64)
+    _check(ctx, _lib.cc_last_stats(ctx, _p(buf), 16))
     return dict(updates=buf[0], model_bytes=buf[1], agg_bytes=buf[2], launches=buf[3], peak_table_bytes=buf[4],
                 fused_root=int(buf[5]), top_gather_bytes=buf[6], top_gather_ms=buf[7], gather_launches=int(buf[8]),
                 halo_bytes=buf[9], exchange=int(buf[10]), column_chunks=int(buf[11]), tail_batches=int(buf[12]),
-                recompute_cols=int(buf[13]), top_gather_ordinal=int(buf[14]))
+                recompute_cols=int(buf[13]), top_gather_ordinal=int(buf[14]), sibling_pairs=int(buf[15]))
 
 
 # ------------------------------------------------------------------ host-only

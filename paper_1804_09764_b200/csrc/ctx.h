@@ -32,7 +32,7 @@ namespace cc {
 
 struct DevX;  // device-initiated exchange state (devx.cu)
 
-constexpr int kNStats = 15;  // cc_last_stats entries
+constexpr int kNStats = 16;  // cc_last_stats entries
 
 // Phases reported by cc_last_profile after "total": PROFILE order.
 enum Phase { PH_COLOR = 0, PH_CSORT, PH_HIST, PH_GATHER, PH_COMBINE, PH_ROOT, PH_EXCHANGE, PH_EXPOSED, PH_N };

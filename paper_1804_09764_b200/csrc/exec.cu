@@ -399,10 +399,19 @@ Src table_src(const void *base, int64_t ld, int c0, int w, int elem) {
 // items [from, to) of one pass (to < 0: all).  N is the base of the N'' rows
 // (row v at N + v * ldN; a row batch passes a virtual base).  sms: the SMs
 // the launch may fill (c->gather_sms).
+// A sibling passive summed in the same traversal (one rank, narrow rows):
+// its whole table, size p, and its N'' base.
+struct PairSrc {
+  Src src;
+  int p;
+  void *N;
+};
+
 void gather_pass(cc_ctx *c, Pass &w, const Src &src, int p, void *N, int accumulate, const RootFuse *rf, int sms,
-                 int64_t from = 0, int64_t to = -1) {
+                 int64_t from = 0, int64_t to = -1, const PairSrc *pr = nullptr) {
   const int k = c->plan.colours(), elem = c->elem();
-  const int W_out = (int)binom(k - 1, p);
+  const int W_out1 = (int)binom(k - 1, p);
+  const int W_out = W_out1 + (pr ? (int)binom(k - 1, pr->p) : 0);
   if (to < 0) to = w.items();
   if (from >= to) return;
   dev::GatherArgs a;
@@ -440,9 +449,26 @@ void gather_pass(cc_ctx *c, Pass &w, const Src &src, int p, void *N, int accumul
   // hub rows kept in L2: a fraction of the L2 (rows are degree-ordered, hubs first)
   a.hub_rows = (int64_t)(c->knobs.hub_l2_pct / 100.0 * (double)c->l2_bytes / (double)(a.ld_src * elem));
   a.dst = N;
-  a.ld_dst = c->ld_of(W_out);
+  a.ld_dst = c->ld_of(W_out1);
   a.W_out = W_out;
   a.k = k;
+  if (pr) {  // the virtual row: part 1's whole 16-byte vectors, then part 2
+    const int vw = 16 / elem;
+    a.nvec1 = (src.w + vw - 1) / vw;
+    a.W_in = a.nvec1 * vw + pr->src.w;
+    a.src2 = pr->src.P;
+    a.ld_src2 = pr->src.ld;
+    a.W_in2 = pr->src.w;
+    a.map2 = c->d_map[pr->p];
+    a.map_ld2 = gather_map_ld(k, pr->p);
+    if (c->knobs.sector_skip) {
+      a.skip2 = c->d_skip[pr->p];
+      a.skip_words2 = c->skip_words[pr->p];
+    }
+    a.dst2 = pr->N;
+    a.ld_dst2 = c->ld_of(W_out - W_out1);
+    a.o2 = W_out1;
+  }
   a.accumulate = accumulate;
   a.work = w.view();
   a.ld_scratch = W_out;
@@ -475,12 +501,13 @@ void gather_pass(cc_ctx *c, Pass &w, const Src &src, int p, void *N, int accumul
   const double nnz = (double)(w.pref[(size_t)to] - w.pref[(size_t)from]);
   const double rows_out = (double)(to - from) - (segs ? (double)(std::min(to, w.n_seg) - from) : 0.0) +
                           (segs ? (double)w.n_hv : 0.0);
-  const double rows = nnz * (double)(k - 1) / k * src.w * elem;
+  const double rows = nnz * (double)(k - 1) / k * (src.w + (pr ? pr->src.w : 0)) * elem;
   const double out_bytes = rf ? rows_out * (8.0 + (rf->mode == 1 ? (double)rf->WA * elem : 0.0))
                               : rows_out * W_out * elem * (1 + accumulate);
   const double bytes = nnz * 4.0 + rows + out_bytes;
   if (!c->ev_log.empty()) c->gather_log.push_back({c->ev_log.size() - 1, bytes});
   c->stats[0] += nnz * (double)src.w / (double)binom(k - 1, p - 1) * (double)binom(k, p);  // U
+  if (pr) c->stats[0] += nnz * (double)binom(k, pr->p);
   c->stats[1] += bytes;
   c->stats[2] += bytes;
 }
@@ -1127,12 +1154,89 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
     mark_passive(pl.steps.back().passive);
   }
 
+  auto release_dead = [&](int s) {  // release the tables / neighbour sums whose last use is step s
+    if (dump_table >= 0 && !dump_rows) return;
+    for (int id = 0; id < nt; ++id) {
+      if (T[id] >= 0 && last_use[id] == s) {
+        bufs.unref(T[id]);
+        T[id] = -1;
+      }
+      if (Nb[id] >= 0 && n_last[id] == s) {
+        bufs.unref(Nb[id]);
+        Nb[id] = -1;
+      }
+    }
+    if (hist >= 0 && s == last_hist_use) {
+      bufs.unref(hist);
+      hist = -2;  // computed and released
+    }
+  };
+
+  // Sibling pairs (one rank): a narrow passive P2 of a later step whose
+  // table is ready -- or is made by a row-local step (its passive the leaf
+  // level, its active table alive) that can run now -- is summed in the SAME
+  // traversal of the colour-sorted lists as this step's narrow passive (the
+  // index stream, colour groups, item setup and N'' row writes paid once).
+  // configs[3]: the p = 2 gather takes B3's neighbour sum along (B3 = the
+  // (3;2,1) combine, run ahead of its turn).  Off when the tables approach
+  // the device size (N''(P2) is allocated earlier than planned).
+  std::vector<char> early(pl.steps.size(), 0);  // row-local steps run ahead of their turn
+  const bool pair_ok = c->knobs.pair_gather && c->pworld() == 1 && c->chunk_cols == 0 && !cache && mp.tail < 0 &&
+                       (dump_table < 0 || dump_rows) &&
+                       model_peak(c, pl, rows, fuse, defer_lift, fuse_cr, last_hist_use, root_out != nullptr, mp) <
+                           0.4 * c->total_mem;
+  auto vecs = [&](int p) { return (int)((binom(k - 1, p - 1) * elem + 15) / 16); };  // 16-byte vectors of a row
+  auto pair_partner = [&](int s) -> std::pair<int, int> {  // (step s2 of the sibling, producer to run early or -1)
+    const Step &st = pl.steps[s];
+    if (!pair_ok || st.p < 2 || vecs(st.p) > 16) return {-1, -1};
+    for (int s2 = s + 1; s2 <= sr; ++s2) {
+      const Step &q = pl.steps[s2];
+      if (q.p < 2 || q.passive == st.passive || Nb[q.passive] >= 0 || pl.n_first_use[q.passive] != s2) continue;
+      if ((s2 == sr && fuse) || vecs(st.p) + vecs(q.p) > 24) continue;
+      if (T[q.passive] >= 0) return {s2, -1};
+      int sp = -1;
+      for (int x = s + 1; x < s2; ++x)
+        if (pl.steps[x].out == q.passive) sp = x;
+      if (sp < 0) continue;
+      const Step &ps = pl.steps[sp];
+      if (ps.p != 1 || hist < 0 || early[sp] || sp == defer_lift || sp == fuse_cr) continue;
+      if (dump_table >= 0 && ps.out == dump_table) continue;  // its sampled rows are copied in its own turn
+      if (ps.active >= 0 && T[ps.active] < 0) continue;
+      return {s2, sp};
+    }
+    return {-1, -1};
+  };
+  auto run_early = [&](int sp) {  // a row-local step over the leaf level, ahead of its turn
+    const Step &ps = pl.steps[sp];
+    const int Wa = (int)binom(k - 1, ps.a - 1), Wp = k - 1, Wt = (int)binom(k - 1, ps.t - 1);
+    early[sp] = 1;
+    if (ps.a == 1) {  // lift: T' = N''(leaf)
+      T[ps.out] = hist;
+      bufs.ref(hist);
+      return;
+    }
+    T[ps.out] = bufs.make((size_t)rows * c->ld_of(Wt) * elem);
+    cudaEvent_t b = c->begin(c->s_main);
+    c->stats[3] += dev::launch_combine(elem, bufs.ptr(T[ps.active]), c->ld_of(Wa), Wa, bufs.ptr(hist), c->ld_of(Wp), Wp,
+                                       c->d_split[sp], (int)binom(ps.t - 1, ps.a - 1), n, bufs.ptr(T[ps.out]),
+                                       c->ld_of(Wt), Wt, c->d_ztab[sp], c->zblocks[sp],
+                                       (int)zblock_ld(ps.t - 1, ps.a - 1), ps.t - 1, ps.a - 1, c->knobs, c->num_sms,
+                                       c->s_main);
+    c->check_launch();
+    c->end(PH_COMBINE, c->s_main, b);
+    c->stats[1] += (double)n * (Wa + Wp + Wt) * elem;
+  };
+
   for (int s = 0; s < (int)pl.steps.size(); ++s) {
     const Step &st = pl.steps[s];
     const int Wa = (int)binom(k - 1, st.a - 1), Wp = (int)binom(k - 1, st.p), Wt = (int)binom(k - 1, st.t - 1);
     if (mp.tail >= 0 && s >= mp.tail) break;  // the batched tail (below)
     if (s == mp.rc) continue;                  // recomputed per batch in column chunks
     if (s == defer_lift) continue;  // T_out = N''(P) is evaluated inside the fused root
+    if (early[s]) {  // ran ahead of its turn for a sibling pair
+      release_dead(s);
+      continue;
+    }
     if (cache && st.out >= 0) {
       if (!need[st.out]) continue;  // only feeds tables this template finds cached
       if (need[st.out] == 2) {      // computed by an earlier template of this colouring
@@ -1202,7 +1306,20 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
           ++cache->reused;
         } else {
           Nb[P] = bufs.make((size_t)rows * c->ld_of(Wp) * elem);
-          aggregate(c, bufs.ptr(T[P]), c->ld_of(binom(k - 1, st.p - 1)), st.p, bufs.ptr(Nb[P]));
+          const auto pp = pair_partner(s);
+          if (pp.first >= 0) {  // one traversal for P and its sibling
+            const Step &q = pl.steps[pp.first];
+            if (pp.second >= 0) run_early(pp.second);
+            const int P2 = q.passive, Win2 = (int)binom(k - 1, q.p - 1);
+            Nb[P2] = bufs.make((size_t)rows * c->ld_of(binom(k - 1, q.p)) * elem);
+            const PairSrc pr{table_src(bufs.ptr(T[P2]), c->ld_of(Win2), 0, Win2, elem), q.p, bufs.ptr(Nb[P2])};
+            const int Win = (int)binom(k - 1, st.p - 1);
+            gather_pass(c, c->p_full, table_src(bufs.ptr(T[P]), c->ld_of(Win), 0, Win, elem), st.p, bufs.ptr(Nb[P]), 0,
+                        nullptr, c->num_sms, 0, -1, &pr);
+            c->stats[15] += 1;  // sibling pairs
+          } else {
+            aggregate(c, bufs.ptr(T[P]), c->ld_of(binom(k - 1, st.p - 1)), st.p, bufs.ptr(Nb[P]));
+          }
           Buf &bb = bufs.pool[Nb[P]];
           if (cache && cache->bytes + bb.bytes <= cache->budget) {
             cache->tables[nkey] = {bb.p, bb.bytes};
@@ -1303,22 +1420,7 @@ void run_count(cc_ctx *c, double *X, int dump_table, std::vector<double> *dump, 
       for (size_t i = 0; i < dump->size(); ++i)
         (*dump)[i] = elem == 8 ? reinterpret_cast<double *>(raw.data())[i] : reinterpret_cast<float *>(raw.data())[i];
     }
-    if (dump_table < 0 || dump_rows) {  // release dead tables / neighbour sums
-      for (int id = 0; id < nt; ++id) {
-        if (T[id] >= 0 && last_use[id] == s) {
-          bufs.unref(T[id]);
-          T[id] = -1;
-        }
-        if (Nb[id] >= 0 && n_last[id] == s) {
-          bufs.unref(Nb[id]);
-          Nb[id] = -1;
-        }
-      }
-      if (hist >= 0 && s == last_hist_use) {
-        bufs.unref(hist);
-        hist = -2;  // computed and released
-      }
-    }
+    release_dead(s);
   }
   if (mp.tail >= 0) {
     // The batched tail (memory plan): for each batch of rows [r0, r1), the

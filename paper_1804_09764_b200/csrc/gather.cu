@@ -368,11 +368,14 @@ template <typename T, int G, typename AccT = double>
 __device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const AccT *sacc, int64_t it, int32_t v,
                                                 bool heavy, int lane, unsigned gmask) {
   T *drow = static_cast<T *>(a.dst) + (int64_t)v * a.ld_dst;
+  // a sibling pair's part 2 goes to its own N'' table (entries o2.. of the virtual row)
+  T *drow2 = a.src2 ? static_cast<T *>(a.dst2) + (int64_t)v * a.ld_dst2 - a.o2 : drow;
   if (!heavy) {
     for (int j = lane; j < a.W_out; j += G) {
+      T *d = j < a.o2 ? drow + j : drow2 + j;
       double x = (double)sacc[j] * AccScale<AccT>::out;
-      if (a.accumulate) x += (double)drow[j];
-      drow[j] = (T)x;
+      if (a.accumulate) x += (double)*d;
+      *d = (T)x;
     }
     return;
   }
@@ -388,12 +391,66 @@ __device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const AccT 
     __threadfence();
     const int32_t s0 = a.work.hv_first[hv], ns = a.work.hv_nseg[hv];
     for (int j = lane; j < a.W_out; j += G) {
+      T *d = j < a.o2 ? drow + j : drow2 + j;
       double x = 0.0;
       for (int s = 0; s < ns; ++s) x += __ldcg(a.scratch + (int64_t)(s0 + s) * a.ld_scratch + j);
-      if (a.accumulate) x += (double)drow[j];
-      drow[j] = (T)x;
+      if (a.accumulate) x += (double)*d;
+      *d = (T)x;
     }
   }
+}
+
+// Sibling pair: row base / stride of virtual 16-byte vector q and whether it
+// holds columns of its part (ring kernel: no sector skip).
+template <typename T, int VW>
+__device__ __forceinline__ bool pair_base(const GatherArgs &a, int q, const char *&base, uint32_t &ld_bytes) {
+  const bool second = q >= a.nvec1;
+  const int qq = second ? q - a.nvec1 : q;
+  base = static_cast<const char *>(second ? a.src2 : a.src) + (size_t)qq * 16;
+  ld_bytes = (uint32_t)((second ? a.ld_src2 : a.ld_src) * sizeof(T));
+  return qq * VW < (second ? a.W_in2 : a.nvec1 * VW);
+}
+// Sibling pair: the colour-pair map entries of virtual vector q as virtual N'' indices.
+template <int VW>
+__device__ __forceinline__ void pair_map(const GatherArgs &a, int q, int cu, int cv, uint16_t (&m)[VW]) {
+  const bool second = q >= a.nvec1;
+  const int qq = second ? q - a.nvec1 : q;
+#pragma unroll
+  for (int i = 0; i < VW; ++i) m[i] = 0xFFFF;
+  if (qq * VW >= (second ? a.W_in2 : a.nvec1 * VW)) return;
+  const uint16_t *mrow = second ? a.map2 + (int64_t)(cu * a.k + cv) * a.map_ld2 : a.map + (int64_t)(cu * a.k + cv) * a.map_ld;
+  if constexpr (VW == 4) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + qq * VW));
+    m[0] = w.x & 0xFFFF;
+    m[1 % VW] = w.x >> 16;
+    m[2 % VW] = w.y & 0xFFFF;
+    m[3 % VW] = w.y >> 16;
+  } else {
+    const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + qq * VW));
+    m[0] = w & 0xFFFF;
+    m[1 % VW] = w >> 16;
+  }
+  const int off = second ? a.o2 : 0;
+#pragma unroll
+  for (int i = 0; i < VW; ++i)
+    if (m[i] != 0xFFFF) m[i] = (uint16_t)(m[i] + off);
+}
+
+// Sibling pair: the part of virtual 16-byte vector q (a lane's vector of the
+// pass), its row base and stride, whether the destination colour can use it
+// (sector skip) and its colour-pair map entries as virtual N'' indices.
+template <typename T, int VW>
+__device__ __forceinline__ void pair_vector(const GatherArgs &a, int q, int cu, int cv, const char *&base,
+                                            uint32_t &ld_bytes, bool &use, uint16_t (&m)[VW]) {
+  use = pair_base<T, VW>(a, q, base, ld_bytes);
+  const bool second = q >= a.nvec1;
+  const uint32_t *sk = second ? a.skip2 : a.skip;
+  if (sk && use) {
+    const int qq = second ? q - a.nvec1 : q;
+    const int cvu = cv < cu ? cv : cv - 1;  // sq_{c_u}(c_v)
+    use = !((__ldg(sk + (int64_t)cvu * (second ? a.skip_words2 : a.skip_words) + (qq >> 5)) >> (qq & 31)) & 1u);
+  }
+  pair_map<VW>(a, q, cu, cv, m);
 }
 
 // Fused root epilogue (root_mode 1 / 2): X_v = sum_{X'} A'(v, X') N''(v, comp X')
@@ -467,6 +524,22 @@ __device__ __forceinline__ void expand(const GatherArgs &a, int cu, int cv, int 
   }
 }
 
+// the same for a sibling pair (virtual vectors lane + j G)
+template <int NV, int VW, int G>
+__device__ __forceinline__ void expand_pair(const GatherArgs &a, int cu, int cv, int lane, double (&acc)[NV][VW],
+                                            double *sacc) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    uint16_t m[VW];
+    pair_map<VW>(a, lane + j * G, cu, cv, m);
+#pragma unroll
+    for (int q = 0; q < VW; ++q) {
+      if (m[q] != 0xFFFF) sacc[m[q]] += acc[j][q];
+      acc[j][q] = 0.0;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ gather, cp.async ring
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes, uint64_t policy) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -495,7 +568,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // fp32 rows are summed in blocks of up to 8 consecutive rows in fp32 and the
 // blocks in fp64 (relative error <= 7 u32 + O(n u64) per entry; DESIGN.md
 // reading C-6); fp64 rows are summed in fp64.
-template <typename T, int G, int NV, int D, int MINB>
+template <typename T, int G, int NV, int D, int MINB, bool PAIR = false>
 __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
@@ -530,8 +603,13 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
     for (int ch = 0; ch < nch; ++ch) {
       const int c0 = ch * CAP + lane * VW;
       int nbytes[NV];
+      const char *jb[NV];  // sibling pair: per-vector row base and stride
+      uint32_t jld[NV];
 #pragma unroll
-      for (int j = 0; j < NV; ++j) nbytes[j] = c0 + j * G * VW < a.W_in ? 16 : 0;
+      for (int j = 0; j < NV; ++j) {
+        if constexpr (PAIR) nbytes[j] = pair_base<T, VW>(a, lane + j * G, jb[j], jld[j]) ? 16 : 0;
+        else nbytes[j] = c0 + j * G * VW < a.W_in ? 16 : 0;
+      }
       // neighbour ids: a window of G stream positions per lane, one window ahead
       auto load_idx = [&](int r) -> int32_t {
         return r < n_s ? __ldg(a.col + b + (r < cv_lo ? r : r + skip)) : 0;
@@ -546,12 +624,19 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
         }
         const int32_t u = __shfl_sync(gmask, idx_cur, r - win, G);
         if (r < n_s) {
-          const T *row = src + (int64_t)u * a.ld_src + c0;
           V *slot = ring + (r % D) * NV * G + lane;
           const uint64_t pol = u < a.hub_rows ? pol_keep : pol_stream;
+          if constexpr (PAIR) {
 #pragma unroll
-          for (int j = 0; j < NV; ++j)
-            cp_async16(slot + j * G, nbytes[j] ? row + j * G * VW : row, nbytes[j], pol);
+            for (int j = 0; j < NV; ++j)
+              cp_async16(slot + j * G, nbytes[j] ? jb[j] + (uint64_t)u * jld[j] : jb[0] + (uint64_t)u * jld[0],
+                         nbytes[j], pol);
+          } else {
+            const T *row = src + (int64_t)u * a.ld_src + c0;
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+              cp_async16(slot + j * G, nbytes[j] ? row + j * G * VW : row, nbytes[j], pol);
+          }
         }
         cp_async_commit();
       };
@@ -606,7 +691,8 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
           for (int j = 0; j < NV; ++j) add_vec(acc[j], slot[j * G]);
         }
         if (i + 1 == gend_s) {  // end of a colour group: expand into N''
-          expand<NV, VW, G>(a, gc, cv, c0, acc, sacc);
+          if constexpr (PAIR) expand_pair<NV, VW, G>(a, gc, cv, lane, acc, sacc);
+          else expand<NV, VW, G>(a, gc, cv, c0, acc, sacc);
           __syncwarp(gmask);
           ++gc;
           next_group();
@@ -790,7 +876,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
 // of a chunk of <= 32 rows the RG slot sums are combined by XOR shuffles
 // (fp32 block of <= 32 rows, then fp64: DESIGN.md C-6) and expanded into the
 // fp64 N'' row through the colour-pair map, vector j by slot j mod RG.
-template <typename T, int G, int NV, int U, int MINB = 2, typename AccT = double>
+template <typename T, int G, int NV, int U, int MINB = 2, typename AccT = double, bool PAIR = false>
 __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
@@ -830,7 +916,19 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
         const int lo = cu == 0 ? 0 : __shfl_sync(0xffffffffu, hi_l, cu - 1);
         const int hi = __shfl_sync(0xffffffffu, hi_l, cu);
         bool use[NV];
-        {
+        uint16_t m[NV][VW];
+        // sibling pair: per-vector row base and stride (part 1 or part 2)
+        const char *jb[NV];
+        uint32_t jld[NV];
+        if constexpr (PAIR) {
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            uint16_t mm[VW];
+            pair_vector<T, VW>(a, vl + j * G, cu, cv, jb[j], jld[j], use[j], mm);
+#pragma unroll
+            for (int q = 0; q < VW; ++q) m[j][q] = rs == j % RG ? mm[q] : (uint16_t)0xFFFF;
+          }
+        } else {
           const int cvu = cv < cu ? cv : cv - 1;  // sq_{c_u}(c_v)
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
@@ -840,11 +938,11 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
               use[j] = !((__ldg(a.skip + (int64_t)cvu * a.skip_words + (vi >> 5)) >> (vi & 31)) & 1u);
             }
           }
-        }
-        uint16_t m[NV][VW];
         const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
+          jb[j] = lbase + (size_t)j * G * 16;
+          jld[j] = ld_bytes;
           if (valid[j] && rs == j % RG) {
             if constexpr (VW == 4) {
               const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + c0 + j * G * VW));
@@ -862,6 +960,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
             for (int q = 0; q < VW; ++q) m[j][q] = 0xFFFF;
           }
         }
+        }
         int32_t u_next = lane < hi - lo ? __ldg(a.col + b + lo + lane) : 0;
         for (int p = lo; p < hi; p += 32) {
           const int cnt = min(32, hi - p);
@@ -876,11 +975,19 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
             for (int uu = 0; uu < U; ++uu) {
               const int rr = r + uu * RG + rs;
               const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, rr & 31);
-              const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
+              if constexpr (PAIR) {
 #pragma unroll
-              for (int j = 0; j < NV; ++j) {
-                if (rr < cnt && use[j]) x[uu][j] = __ldg(row + G * j);
-                else zero_vec(x[uu][j]);
+                for (int j = 0; j < NV; ++j) {
+                  if (rr < cnt && use[j]) x[uu][j] = __ldg(reinterpret_cast<const V *>(jb[j] + (uint64_t)u * jld[j]));
+                  else zero_vec(x[uu][j]);
+                }
+              } else {
+                const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                  if (rr < cnt && use[j]) x[uu][j] = __ldg(row + G * j);
+                  else zero_vec(x[uu][j]);
+                }
               }
             }
 #pragma unroll
@@ -1057,7 +1164,7 @@ void short_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s)
   kern<<<grid, threads, smem, s>>>(a, nch);
 }
 
-template <typename T, int G, int NV, int U, int MINB = 3>
+template <typename T, int G, int NV, int U, int MINB = 3, bool PAIR = false>
 void rows_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
@@ -1065,7 +1172,7 @@ void rows_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) 
   // configs[3] -1 to -2% against 2 CTAs (profiles/r1/SUMMARY.md)
   // fp32 tables: fp32 shared-memory rows as in the lean gather (C-6)
   const bool acc32 = sizeof(T) == 4 && kn.acc32;
-  auto kern = acc32 ? k_gather_rows<T, G, NV, U, MINB, float> : k_gather_rows<T, G, NV, U, MINB, double>;
+  auto kern = acc32 ? k_gather_rows<T, G, NV, U, MINB, float, PAIR> : k_gather_rows<T, G, NV, U, MINB, double, PAIR>;
   const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
@@ -1104,14 +1211,15 @@ void ldg_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <typename T, int G, int NV, int D, int MINB = 1>
+template <typename T, int G, int NV, int D, int MINB = 1, bool PAIR = false>
 void ring_go(const GatherArgs &a, const Knobs &, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
-  auto kern = k_gather_ring<T, G, NV, D, MINB>;
+  auto kern = k_gather_ring<T, G, NV, D, MINB, PAIR>;
   const size_t per_group = (size_t)D * NV * G * 16 + (size_t)a.W_out * sizeof(double);
   int groups = 256 / G;
-  while (groups > 1 && per_group * groups > 100 * 1024) groups /= 2;
+  // (sibling pairs: as many groups as MINB CTAs per SM allow)
+  while (groups > 1 && (PAIR ? per_group * groups * MINB > 224 * 1024 : per_group * groups > 100 * 1024)) groups /= 2;
   const int threads = groups * G;
   const size_t smem = per_group * groups;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1120,10 +1228,40 @@ void ring_go(const GatherArgs &a, const Knobs &, int num_sms, cudaStream_t s) {
   kern<<<grid, threads, smem, s>>>(a, nch);
 }
 
+// A sibling pair of narrow passives (GatherArgs::src2): one traversal, the
+// long lists row-parallel and the short tail on rings as for one narrow
+// table, over the virtual row of both parts (<= 24 vectors).
+template <typename T>
+int pair_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
+  constexpr int VW = Vec<T>::W;
+  const int wvec = (a.W_in + VW - 1) / VW;
+  const int64_t from = a.item_from, to = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
+  const int64_t split = std::min(std::max(a.item_split, from), to);
+  GatherArgs h = a, t = a;
+  h.item_to = split;
+  t.item_from = split;
+  int launches = 0;
+  if (h.item_from < h.item_to) {
+    if (wvec <= 8) rows_go<T, 8, 1, 4, 3, true>(h, kn, num_sms, s);
+    else if (wvec <= 16) rows_go<T, 8, 2, 4, 3, true>(h, kn, num_sms, s);
+    else if (kn.rows_variant == 2) rows_go<T, 8, 3, 4, 2, true>(h, kn, num_sms, s);  // more rows in flight
+    else rows_go<T, 8, 3, 3, 3, true>(h, kn, num_sms, s);
+    ++launches;
+  }
+  if (t.item_from < t.item_to) {
+    if (wvec <= 8) ring_go<T, 8, 1, 4, 2, true>(t, kn, num_sms, s);
+    else if (wvec <= 16) ring_go<T, 8, 2, 4, 3, true>(t, kn, num_sms, s);
+    else ring_go<T, 8, 3, 4, 2, true>(t, kn, num_sms, s);
+    ++launches;
+  }
+  return launches;
+}
+
 template <typename T>
 int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {  // returns the launches
   constexpr int VW = Vec<T>::W;
   const int wvec = (a.W_in + VW - 1) / VW;
+  if (a.src2) return pair_typed<T>(a, kn, num_sms, s);
   // default: rows of <= 16 vectors go to the narrow kernels, wider rows to
   // the lean kernel (measured, profiles/r1/SUMMARY.md).  The fused root
   // exists in the lean kernel only.

@@ -47,6 +47,8 @@ struct Knobs {
   int layout = 0;          // CC_LAYOUT: column order of tables of >= 3 vertices (R-3): 0 = colex;
                            //   L = 1, 2, 3: groups of 32 << (L-1) bytes whose sets share the most colours
   int tail_batches = 0;    // CC_TAIL_BATCHES: > 0 forces the memory plan's row batches (0 = by memory)
+  int pair_gather = 1;     // CC_PAIR_GATHER: 0 = every narrow passive gets its own traversal (one rank: sibling
+                           //   narrow passives ready at the same time are summed in one pass)
   int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
                                 //   per batch in column chunks of this width (0 = by memory)
 };
@@ -120,6 +122,25 @@ struct GatherArgs {
   int WA = 0;
   const uint16_t *comp = nullptr;  // comp[X'] = rank of [k-1] \ X' in C(k-1, p)
   double *per_vertex = nullptr;
+  // Sibling pair (one rank, narrow rows; src2 != nullptr): a second passive
+  // table summed in the SAME traversal of the colour-sorted lists (the two
+  // neighbour sums of Eq. 1 over the same N(v)).  The
+  // launch sees a virtual row of nvec1 16-byte vectors of part 1 (src, map,
+  // skip) followed by part 2's (src2, map2, skip2); W_in = nvec1 x the vector
+  // width + W_in2.  The virtual N'' row is part 1's o2 entries (written to
+  // dst) followed by part 2's W_out - o2 entries (written to dst2).  No
+  // column chunks, no fused root.
+  const void *src2 = nullptr;
+  int64_t ld_src2 = 0;
+  int W_in2 = 0;
+  int nvec1 = 0;
+  const uint16_t *map2 = nullptr;
+  int64_t map_ld2 = 0;
+  const uint32_t *skip2 = nullptr;
+  int skip_words2 = 0;
+  void *dst2 = nullptr;
+  int64_t ld_dst2 = 0;
+  int o2 = 1 << 30;  // first N'' entry of part 2 (virtual row); unpaired: never reached
 };
 
 int launch_color(const int32_t *orig, int64_t n, uint64_t seed, int k, uint8_t *out, cudaStream_t s);

@@ -287,6 +287,49 @@ def test_subtree_rows_match_the_full_dump_and_the_oracle():
         assert np.array_equal(got[7][-2:].sum(axis=1), [1.0, 1.0])  # ... but the single vertex maps
 
 
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_sibling_pair_gather_every_row(prec):
+    """Sibling pairs (knob pair_gather, one rank): configs[3]'s plan sums the
+    p = 2 passive (the lifted leaf level, 11 columns) and B3 (the (3;2,1)
+    combine, run ahead of its turn, 55 columns) in ONE traversal of the
+    colour-sorted lists (Eq. 1's inner sum, for both).
+    Every full-subtree row of every template vertex equals the oracle (fp64:
+    1e-12 per entry, zero entries exactly zero) and the count equals the
+    unpaired run's bit for bit in fp64 (same sums in the same order); with
+    forced heavy segments too (the segments' partial rows of both parts)."""
+    cc = lib()
+    cfg = synth.scaled_twin(synth.CONFIGS[3], 12, 32)
+    g = cfg.graph()
+    k = cfg.k
+    col = oracle.color(g.n, k, 5)
+    sizes = subtree_sizes(cfg.parent)
+    verts = np.arange(g.n, dtype=np.int32)
+    want = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE, want_root=True)
+    tol = TOL_FP64 if prec == "fp64" else TOL_FP32
+    for seg in (0, 64):
+        with context(g, cfg.parent, prec, segment_len=seg) as ctx:
+            cc.cc_set_colors(ctx, col)
+            x1 = cc.cc_count_colorful(ctx)
+            assert cc.cc_last_stats(ctx)["sibling_pairs"] >= 1
+            cc.cc_set_knob(ctx, "pair_gather", 0)
+            x0 = cc.cc_count_colorful(ctx)
+            assert cc.cc_last_stats(ctx)["sibling_pairs"] == 0
+            cc.cc_set_knob(ctx, "pair_gather", 1)
+            assert rel_err(x1, float(want.total)) <= tol
+            if prec == "fp64":
+                assert x1 == x0, (seg, x1, x0)
+                for x in range(k):
+                    if cfg.parent[x] == -1:
+                        rows = cc.cc_get_subtree_rows(ctx, x, verts, k, k)[:, 0]
+                        ref = want.root
+                    else:
+                        rows = cc.cc_get_subtree_rows(ctx, x, verts, k, sizes[x])
+                        ref = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE, keep_x=x).table
+                    assert_close_entries(rows, ref, TOL_FP64, f"pair x={x} seg={seg}")
+            else:
+                assert rel_err(x1, x0) <= tol
+
+
 # ------------------------------------------------------------------ configs[1]: fp64 1e-12 per entry, fp32 1e-4
 def test_config1_fp64_every_entry_and_fp32_total():
     cfg = synth.CONFIGS[1]
@@ -607,7 +650,8 @@ def test_fp32_overflow_is_reported_nonfinite():
 KNOB_SETTINGS = [("gather_impl", 1), ("gather_impl", 2), ("narrow_impl", 0), ("narrow_impl", 1),
                  ("narrow_split", 0), ("narrow_split", 7), ("csort_small", 0), ("sector_skip", 0),
                  ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("combine_impl", 4), ("acc32", 0),
-                 ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1), ("short_lists", 0), ("short_lists", 1), ("short_lists", 3), ("short_split", 1), ("lean_split", 2)]
+                 ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1), ("short_lists", 0), ("short_lists", 1), ("short_lists", 3), ("short_split", 1), ("lean_split", 2),
+                 ("pair_gather", 0), ("rows_variant", 2)]
 
 
 @pytest.mark.parametrize("ci", [2, 3, 4])
