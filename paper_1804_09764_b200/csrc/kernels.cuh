@@ -38,7 +38,8 @@ struct Knobs {
                            //               the NVTX range "cc_dominant" (one-launch ncu measurement)
   int short_lists = 2;     // CC_SHORT_LISTS: the short tail of wide-row gathers: 0 = with the long lists,
                            //   1 = k_gather_short, 2 = lean kernel U = 2 at 3 CTAs/SM (measured best),
-                           //   3 = U = 1 at 4 CTAs/SM, 4 = U = 3 at 3 CTAs/SM
+                           //   3 = U = 1 at 4 CTAs/SM, 4 = U = 3 at 3 CTAs/SM, 5..7 = k_gather_stream
+                           //   (rows streamed across colour groups; 6, 7: other U for 64-vector rows)
   int rows_variant = 0;    // CC_ROWS_VARIANT: row-parallel narrow kernel: 0 = U 4 at 3 CTAs/SM,
                            //   1 = U 2 at 4 CTAs/SM, 2 = U 8 at 2 CTAs/SM
   int short_split = 4;     // CC_SHORT_SPLIT: q, the short tail = light items with <= 8 << q neighbours
@@ -47,8 +48,9 @@ struct Knobs {
   int layout = 0;          // CC_LAYOUT: column order of tables of >= 3 vertices (R-3): 0 = colex;
                            //   L = 1, 2, 3: groups of 32 << (L-1) bytes whose sets share the most colours
   int tail_batches = 0;    // CC_TAIL_BATCHES: > 0 forces the memory plan's row batches (0 = by memory)
-  int pair_gather = 1;     // CC_PAIR_GATHER: 0 = every narrow passive gets its own traversal (one rank: sibling
-                           //   narrow passives ready at the same time are summed in one pass)
+  int pair_gather = 0;     // CC_PAIR_GATHER: 1 = sibling narrow passives ready at the same time are summed
+                           //   in one traversal (one rank); measured slower on configs[3] (33.7 ms for the
+                           //   p = 2 + p = 3 pair against 25.1 ms unpaired, profiles/r2/SUMMARY.md)
   int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
                                 //   per batch in column chunks of this width (0 = by memory)
 };

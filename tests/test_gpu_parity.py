@@ -287,16 +287,16 @@ def test_subtree_rows_match_the_full_dump_and_the_oracle():
         assert np.array_equal(got[7][-2:].sum(axis=1), [1.0, 1.0])  # ... but the single vertex maps
 
 
-@pytest.mark.parametrize("prec", ["fp64", "fp32"])
-def test_sibling_pair_gather_every_row(prec):
-    """Sibling pairs (knob pair_gather, one rank): configs[3]'s plan sums the
-    p = 2 passive (the lifted leaf level, 11 columns) and B3 (the (3;2,1)
-    combine, run ahead of its turn, 55 columns) in ONE traversal of the
-    colour-sorted lists (Eq. 1's inner sum, for both).
-    Every full-subtree row of every template vertex equals the oracle (fp64:
-    1e-12 per entry, zero entries exactly zero) and the count equals the
-    unpaired run's bit for bit in fp64 (same sums in the same order); with
-    forced heavy segments too (the segments' partial rows of both parts)."""
+def test_sibling_pair_gather_every_row():
+    """Sibling pairs (knob pair_gather = 1, one rank; off by default: measured
+    slower): configs[3]'s plan sums the p = 2 passive (the lifted leaf level,
+    11 columns) and B3 (the (3;2,1) combine, run ahead of its turn, 55
+    columns) in ONE traversal of the colour-sorted lists (Eq. 1's inner sum,
+    PAPER.md line 118, for both).  fp32 rows only: in fp64 the pair's rows
+    (6 + 28 vectors) exceed the 24-vector limit and no pair forms.  Every
+    full-subtree row of every template vertex is within the fp32 tolerance
+    of the oracle, zero entries exactly zero; with forced heavy segments too
+    (the segments' partial rows of both parts)."""
     cc = lib()
     cfg = synth.scaled_twin(synth.CONFIGS[3], 12, 32)
     g = cfg.graph()
@@ -305,29 +305,31 @@ def test_sibling_pair_gather_every_row(prec):
     sizes = subtree_sizes(cfg.parent)
     verts = np.arange(g.n, dtype=np.int32)
     want = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE, want_root=True)
-    tol = TOL_FP64 if prec == "fp64" else TOL_FP32
     for seg in (0, 64):
-        with context(g, cfg.parent, prec, segment_len=seg) as ctx:
+        with context(g, cfg.parent, "fp64", segment_len=seg) as ctx:
             cc.cc_set_colors(ctx, col)
-            x1 = cc.cc_count_colorful(ctx)
-            assert cc.cc_last_stats(ctx)["sibling_pairs"] >= 1
+            cc.cc_set_knob(ctx, "pair_gather", 1)
+            x64 = cc.cc_count_colorful(ctx)
+            assert cc.cc_last_stats(ctx)["sibling_pairs"] == 0
+            assert rel_err(x64, float(want.total)) <= TOL_FP64
+        with context(g, cfg.parent, "fp32", segment_len=seg) as ctx:
+            cc.cc_set_colors(ctx, col)
             cc.cc_set_knob(ctx, "pair_gather", 0)
             x0 = cc.cc_count_colorful(ctx)
             assert cc.cc_last_stats(ctx)["sibling_pairs"] == 0
             cc.cc_set_knob(ctx, "pair_gather", 1)
-            assert rel_err(x1, float(want.total)) <= tol
-            if prec == "fp64":
-                assert x1 == x0, (seg, x1, x0)
-                for x in range(k):
-                    if cfg.parent[x] == -1:
-                        rows = cc.cc_get_subtree_rows(ctx, x, verts, k, k)[:, 0]
-                        ref = want.root
-                    else:
-                        rows = cc.cc_get_subtree_rows(ctx, x, verts, k, sizes[x])
-                        ref = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE, keep_x=x).table
-                    assert_close_entries(rows, ref, TOL_FP64, f"pair x={x} seg={seg}")
-            else:
-                assert rel_err(x1, x0) <= tol
+            x1 = cc.cc_count_colorful(ctx)
+            assert cc.cc_last_stats(ctx)["sibling_pairs"] >= 1
+            assert rel_err(x1, float(want.total)) <= TOL_FP32
+            assert rel_err(x1, x0) <= TOL_FP32
+            for x in range(k):
+                if cfg.parent[x] == -1:
+                    rows = cc.cc_get_subtree_rows(ctx, x, verts, k, k)[:, 0]
+                    ref = want.root
+                else:
+                    rows = cc.cc_get_subtree_rows(ctx, x, verts, k, sizes[x])
+                    ref = oracle.dp_count(g, cfg.parent, col, oracle.NUM_LONGDOUBLE, keep_x=x).table
+                assert_close_entries(rows, ref, TOL_FP32, f"pair x={x} seg={seg}")
 
 
 # ------------------------------------------------------------------ configs[1]: fp64 1e-12 per entry, fp32 1e-4
@@ -357,6 +359,37 @@ def test_config_twins_fp64_every_entry(ci, scale, ef):
     got = tables(g, cfg.parent, col, segment_len=256)
     for x in range(cfg.k):
         assert_close_entries(got[x], ref[x], TOL_FP64, f"{cfg.name} x={x}")
+
+
+_SHORT_REF = {}
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("variant", [2, 5, 6, 7])
+def test_short_list_kernels_every_entry(prec, variant):
+    """The short tail of the wide-row gathers (light items with <= 128
+    neighbours; knob short_lists: 2 = the lean kernel, 5-7 = k_gather_stream,
+    rows streamed across colour groups) computes Eq. 1's neighbour sums
+    (PAPER.md lines 114-120): every table of a configs[3] twin equals the
+    oracle per entry (fp64 1e-12, fp32 1e-4; zero entries exactly zero),
+    with heavy segments forced (s = 256) so both item kinds are present."""
+    cc = lib()
+    cfg = synth.scaled_twin(synth.CONFIGS[3], 13, 32)
+    g = cfg.graph()
+    col = oracle.color(g.n, cfg.k, cfg.color_seed)
+    if "ref" not in _SHORT_REF:
+        _SHORT_REF["ref"] = oracle_tables(g, cfg.parent, col, oracle.NUM_LONGDOUBLE)
+    ref = _SHORT_REF["ref"]
+    sizes = subtree_sizes(cfg.parent)
+    k = cfg.k
+    tol = TOL_FP64 if prec == "fp64" else TOL_FP32
+    with context(g, cfg.parent, prec, segment_len=256) as ctx:
+        cc.cc_set_knob(ctx, "short_lists", variant)
+        cc.cc_set_colors(ctx, col)
+        for x in range(k):
+            got = (cc.cc_get_subtree_counts(ctx, x, g.n, k, k) if cfg.parent[x] == -1
+                   else cc.cc_get_subtree_counts(ctx, x, g.n, k, sizes[x]))
+            assert_close_entries(got, ref[x], tol, f"short_lists={variant} {prec} x={x}")
 
 
 @pytest.mark.parametrize("ci,scale,ef", [(2, 16, 16), (3, 14, 32), (4, 12, 64)])
@@ -651,7 +684,8 @@ KNOB_SETTINGS = [("gather_impl", 1), ("gather_impl", 2), ("narrow_impl", 0), ("n
                  ("narrow_split", 0), ("narrow_split", 7), ("csort_small", 0), ("sector_skip", 0),
                  ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("combine_impl", 4), ("acc32", 0),
                  ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1), ("short_lists", 0), ("short_lists", 1), ("short_lists", 3), ("short_split", 1), ("lean_split", 2),
-                 ("pair_gather", 0), ("rows_variant", 2)]
+                 ("pair_gather", 1), ("rows_variant", 2), ("short_lists", 5), ("short_lists", 6),
+                 ("short_lists", 7)]
 
 
 @pytest.mark.parametrize("ci", [2, 3, 4])
