@@ -495,33 +495,38 @@ __device__ __forceinline__ void root_epilogue(const GatherArgs &a, AccT *sacc, i
 template <int NV, int VW, int G>
 __device__ __forceinline__ void expand(const GatherArgs &a, int cu, int cv, int c0, double (&acc)[NV][VW],
                                        double *sacc) {
+  // 0xFFFF entries land in the discard slot sacc[W_out] (no branches); all
+  // loads before the stores: the map is injective per colour pair
   const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
+  const uint32_t discard = (uint32_t)a.W_out;
+  uint32_t m[NV][VW];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int y0 = c0 + j * G * VW;
-    uint16_t m[VW];
     if (y0 < a.W_in) {
       if (VW == 4) {
         const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + y0));
-        m[0] = w.x & 0xFFFF;
-        m[1] = w.x >> 16;
-        m[2 % VW] = w.y & 0xFFFF;
-        m[3 % VW] = w.y >> 16;
+        m[j][0] = w.x & 0xFFFF;
+        m[j][1] = w.x >> 16;
+        m[j][2 % VW] = w.y & 0xFFFF;
+        m[j][3 % VW] = w.y >> 16;
       } else {
         const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + y0));
-        m[0] = w & 0xFFFF;
-        m[1 % VW] = w >> 16;
+        m[j][0] = w & 0xFFFF;
+        m[j][1 % VW] = w >> 16;
       }
     } else {
 #pragma unroll
-      for (int q = 0; q < VW; ++q) m[q] = 0xFFFF;
-    }
-#pragma unroll
-    for (int q = 0; q < VW; ++q) {
-      if (m[q] != 0xFFFF) sacc[m[q]] += acc[j][q];
-      acc[j][q] = 0.0;
+      for (int q = 0; q < VW; ++q) m[j][q] = 0xFFFF;
     }
   }
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int q = 0; q < VW; ++q) {
+      if (m[j][q] != 0xFFFF) sacc[m[j][q]] += acc[j][q];
+      acc[j][q] = 0.0;
+    }
 }
 
 // the same for a sibling pair (virtual vectors lane + j G)
@@ -583,7 +588,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
   const int groups_per_block = blockDim.x / G;
   V *ring = reinterpret_cast<V *>(smem_ring) + (int64_t)grp * D * NV * G;  // [D][NV][G]
   double *sacc = reinterpret_cast<double *>(reinterpret_cast<V *>(smem_ring) + (int64_t)groups_per_block * D * NV * G) +
-                 (int64_t)grp * a.W_out;
+                 (int64_t)grp * (a.W_out + 1);  // + the discard slot
   const T *__restrict__ src = static_cast<const T *>(a.src);
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
 
@@ -881,7 +886,8 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
   constexpr int CAP = G * NV * VW;  // columns per pass
   extern __shared__ __align__(16) unsigned char sacc_raw[];
   const int lane = threadIdx.x & 31, vl = lane % G, rs = lane / G;
-  AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)a.W_out;
+  AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)(a.W_out + 1);  // + discard slot
+  const uint32_t discard = (uint32_t)a.W_out;
   const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const char *__restrict__ srcb = static_cast<const char *>(a.src);
@@ -926,37 +932,35 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
             for (int q = 0; q < VW; ++q) m[j][q] = rs == j % RG ? mm[q] : (uint16_t)0xFFFF;
           }
         } else {
-          const int cvu = cv < cu ? cv : cv - 1;  // sq_{c_u}(c_v)
+          // every lane loads its vectors' map entries (lanes of one vector
+          // share the address); a vector whose entries are all 0xFFFF holds
+          // only colour sets containing v's colour: not read (16-byte sector
+          // skipping; knob sector_skip = 0 reads it).  Only the row slot
+          // rs == j mod RG adds vector j into N'' (the others: discard slot)
+          const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
-            use[j] = valid[j];
-            if (a.skip && valid[j]) {
-              const int vi = (a.col_base + c0) / VW + j * G;  // the lane's 16-byte vector of the row
-              use[j] = !((__ldg(a.skip + (int64_t)cvu * a.skip_words + (vi >> 5)) >> (vi & 31)) & 1u);
+            jb[j] = lbase + (size_t)j * G * 16;
+            jld[j] = ld_bytes;
+            uint32_t w0 = 0xFFFFFFFFu, w1 = 0xFFFFFFFFu;
+            if (valid[j]) {
+              if constexpr (VW == 4) {
+                const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + c0 + j * G * VW));
+                w0 = w.x;
+                w1 = w.y;
+              } else {
+                w0 = __ldg(reinterpret_cast<const uint32_t *>(mrow + c0 + j * G * VW));
+              }
             }
-          }
-        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          jb[j] = lbase + (size_t)j * G * 16;
-          jld[j] = ld_bytes;
-          if (valid[j] && rs == j % RG) {
+            use[j] = valid[j] && (!a.skip || w0 != 0xFFFFFFFFu || w1 != 0xFFFFFFFFu);
+            const bool mine = rs == j % RG;
+            m[j][0] = mine ? (uint16_t)(w0 & 0xFFFF) : (uint16_t)0xFFFF;
+            m[j][1 % VW] = mine ? (uint16_t)(w0 >> 16) : (uint16_t)0xFFFF;
             if constexpr (VW == 4) {
-              const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + c0 + j * G * VW));
-              m[j][0] = w.x & 0xFFFF;
-              m[j][1 % VW] = w.x >> 16;
-              m[j][2 % VW] = w.y & 0xFFFF;
-              m[j][3 % VW] = w.y >> 16;
-            } else {
-              const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + c0 + j * G * VW));
-              m[j][0] = w & 0xFFFF;
-              m[j][1 % VW] = w >> 16;
+              m[j][2 % VW] = mine ? (uint16_t)(w1 & 0xFFFF) : (uint16_t)0xFFFF;
+              m[j][3 % VW] = mine ? (uint16_t)(w1 >> 16) : (uint16_t)0xFFFF;
             }
-          } else {
-#pragma unroll
-            for (int q = 0; q < VW; ++q) m[j][q] = 0xFFFF;
           }
-        }
         }
         int32_t u_next = lane < hi - lo ? __ldg(a.col + b + lo + lane) : 0;
         for (int p = lo; p < hi; p += 32) {
@@ -1009,14 +1013,20 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
               }
               add_same(blk[j], o);
             }
+          // into N'' (0xFFFF: the discard slot; all loads before the stores)
+          AccT *d[NV][VW];
+          AccT old[NV][VW];
 #pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            const double e[4] = {(double)vec_at(blk[j], 0), (double)vec_at(blk[j], 1), (double)vec_at(blk[j], 2 % VW),
-                                 (double)vec_at(blk[j], 3 % VW)};
+          for (int j = 0; j < NV; ++j)
 #pragma unroll
-            for (int q = 0; q < VW; ++q)
-              if (m[j][q] != 0xFFFF) sacc[m[j][q]] += (AccT)(e[q] * AccScale<AccT>::in);
-          }
+            for (int q = 0; q < VW; ++q) {
+              d[j][q] = sacc + min((uint32_t)m[j][q], discard);
+              old[j][q] = *d[j][q];
+            }
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int q = 0; q < VW; ++q) *d[j][q] = old[j][q] + (AccT)((double)vec_at(blk[j], q) * AccScale<AccT>::in);
         }
         __syncwarp();  // groups of different colours may map to the same N'' entries
       }
@@ -1336,7 +1346,7 @@ void rows_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) 
   // fp32 tables: fp32 shared-memory rows as in the lean gather (C-6)
   const bool acc32 = sizeof(T) == 4 && kn.acc32;
   auto kern = acc32 ? k_gather_rows<T, G, NV, U, MINB, float, PAIR> : k_gather_rows<T, G, NV, U, MINB, double, PAIR>;
-  const size_t row = (size_t)a.W_out * (acc32 ? sizeof(float) : sizeof(double));
+  const size_t row = (size_t)(a.W_out + 1) * (acc32 ? sizeof(float) : sizeof(double));  // + the discard slot
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
   const int threads = warps * 32;
@@ -1379,7 +1389,7 @@ void ring_go(const GatherArgs &a, const Knobs &, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
   auto kern = k_gather_ring<T, G, NV, D, MINB, PAIR>;
-  const size_t per_group = (size_t)D * NV * G * 16 + (size_t)a.W_out * sizeof(double);
+  const size_t per_group = (size_t)D * NV * G * 16 + (size_t)(a.W_out + 1) * sizeof(double);  // + discard slot
   int groups = 256 / G;
   // (sibling pairs: as many groups as MINB CTAs per SM allow)
   while (groups > 1 && (PAIR ? per_group * groups * MINB > 224 * 1024 : per_group * groups > 100 * 1024)) groups /= 2;
