@@ -438,9 +438,7 @@ void gather_pass(cc_ctx *c, Pass &w, const Src &src, int p, void *N, int accumul
     a.item_split = w.seg_len > (8 << q) ? w.split[q] : 0;
     if (c->knobs.lean_split >= 0) a.lean_split = w.split[std::min(7, c->knobs.lean_split)];
     // first light item of the short tail (k_gather_short takes <= 32 neighbours: one id per lane)
-    // (k_gather_stream: <= 128, four ids per lane)
-    a.short_from = w.split[std::min(c->knobs.short_lists == 1 ? 2 : c->knobs.short_lists >= 5 ? 4 : 7,
-                                    std::max(0, c->knobs.short_split))];
+    a.short_from = w.split[std::min(c->knobs.short_lists == 1 ? 2 : 7, std::max(0, c->knobs.short_split))];
   }
   a.map = c->d_map[p];
   a.map_ld = gather_map_ld(k, p);

@@ -495,10 +495,10 @@ __device__ __forceinline__ void root_epilogue(const GatherArgs &a, AccT *sacc, i
 template <int NV, int VW, int G>
 __device__ __forceinline__ void expand(const GatherArgs &a, int cu, int cv, int c0, double (&acc)[NV][VW],
                                        double *sacc) {
-  // 0xFFFF entries land in the discard slot sacc[W_out] (no branches); all
-  // loads before the stores: the map is injective per colour pair
+  // (the branch-free form with a discard slot, as in the lean kernels,
+  // faulted -- illegal instruction -- in the G = 32 ring variant; the rings
+  // keep the branches)
   const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
-  const uint32_t discard = (uint32_t)a.W_out;
   uint32_t m[NV][VW];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
@@ -1154,172 +1154,6 @@ __global__ void __launch_bounds__(128) k_gather_short(GatherArgs a, int nch) {
   }
 }
 
-// Short lists, streamed (knob short_lists = 5..7; items with <= 128
-// neighbours).  The lean kernel pays, per colour group, a dependent load of
-// the group's ids and then ceil(rows / U) round trips for its rows: with
-// ~11 groups of a few rows each, a short item is ~2-3 round trips per group.
-// Here the warp loads the item's whole stream of ids at once (<= 4 per lane;
-// the own-colour group is skipped by position), then issues the rows U at a
-// time ACROSS colour-group boundaries and walks them in stream order: a new
-// colour closes the previous group's fp32 block (<= 32 rows, C-6)
-// into the N'' row through its colour-pair map, which was loaded when that
-// group opened (its latency hidden behind the group's rows).  Map entries
-// 0xFFFF (sets containing v's colour, or columns past the row end) are
-// redirected to a discard slot after the N'' row instead of branched
-// around.  Whole rows: no sector skipping (a step's rows may belong to
-// several groups).  Same sums in the same order as the lean kernel when
-// blocks end at the same rows.
-template <typename T, int NV, int U, typename AccT, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_gather_stream(GatherArgs a, int nch) {
-  using V = typename Vec<T>::type;
-  constexpr int VW = Vec<T>::W;
-  constexpr int CAP = 32 * NV * VW;  // columns per pass
-  extern __shared__ __align__(16) unsigned char sacc_raw[];
-  const int lane = threadIdx.x & 31;
-  const int ldacc = a.W_out + 1;  // + the discard slot
-  AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)ldacc;
-  const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const char *__restrict__ srcb = static_cast<const char *>(a.src);
-  const uint32_t ld_bytes = (uint32_t)(a.ld_src * sizeof(T));
-  const uint32_t discard = (uint32_t)a.W_out;
-
-  int64_t it = a.item_from + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  int4 dx = make_int4(0, 0, 0, 0), dy = make_int4(0, 0, 0, 0);
-  int go_n = 0;
-  if (it < n_items) load_desc(a, it, lane, dx, dy, go_n);
-  for (; it < n_items; it += nw) {
-    const int64_t b = (int64_t)(((uint64_t)(uint32_t)dx.y << 32) | (uint32_t)dx.x);
-    const int32_t v = dx.z;
-    const int n_s = dx.w, cv_lo = dy.x, skip = dy.y, cv = dy.z;
-    const bool heavy = dy.w != 0;
-    const int go = go_n;  // lane c < 16: end of colour group c (item positions)
-    // the stream's ids (stream position s -> item position s, or s + skip past v's own colour group)
-    int32_t id0, id1, id2, id3;
-    {
-      int32_t t[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int s = lane + 32 * q;
-        t[q] = s < n_s ? __ldg(a.col + b + (s < cv_lo ? s : s + skip)) : 0;
-      }
-      id0 = t[0];
-      id1 = t[1];
-      id2 = t[2];
-      id3 = t[3];
-    }
-    // lane c: stream end of colour group c; the non-empty groups other than v's own
-    const int lo_l = __shfl_up_sync(0xffffffffu, go, 1);
-    const int hs = go - (lane > cv ? skip : 0);
-    const unsigned gm = __ballot_sync(0xffffffffu, lane < a.k && lane != cv && go > (lane == 0 ? 0 : lo_l));
-    if (it + nw < n_items) load_desc(a, it + nw, lane, dx, dy, go_n);  // prefetch the next item
-    for (int j = lane; j < a.W_out; j += 32) sacc[j] = (AccT)0;
-    __syncwarp();
-    for (int ch = 0; ch < nch; ++ch) {
-      const int c0 = ch * CAP + lane * VW;
-      bool valid[NV];
-#pragma unroll
-      for (int j = 0; j < NV; ++j) valid[j] = c0 + j * 32 * VW < a.W_in;
-      const char *lbase = srcb + (size_t)c0 * sizeof(T);
-      // the open group's colour, stream end and colour-pair map (packed 16-bit entries)
-      unsigned rem = gm;
-      int cu = 0, gend = 0;
-      uint32_t mp[NV][VW / 2];
-      auto open = [&]() {
-        cu = __ffs(rem) - 1;
-        rem &= rem - 1;
-        gend = __shfl_sync(0xffffffffu, hs, cu);
-        const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          if (valid[j]) {
-            if constexpr (VW == 4) {
-              const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + c0 + j * 32 * VW));
-              mp[j][0] = w.x;
-              mp[j][1 % (VW / 2)] = w.y;
-            } else {
-              mp[j][0] = __ldg(reinterpret_cast<const uint32_t *>(mrow + c0 + j * 32 * VW));
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < VW / 2; ++q) mp[j][q] = 0xFFFFFFFFu;
-          }
-        }
-      };
-      V blk[NV];
-#pragma unroll
-      for (int j = 0; j < NV; ++j) zero_vec(blk[j]);
-      auto flush = [&]() {  // the open block into N'' (discard slot for 0xFFFF)
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-#pragma unroll
-          for (int q = 0; q < VW; ++q) {
-            const uint32_t m = (mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
-            AccT *d = sacc + min(m, discard);
-            *d += (AccT)((double)vec_at(blk[j], q) * AccScale<AccT>::in);
-          }
-          zero_vec(blk[j]);
-        }
-        __syncwarp();  // groups of different colours may map to the same N'' entries
-      };
-      if (gm) open();
-      int nb = 0;  // rows in the open block
-      for (int r0 = 0; r0 < n_s; r0 += U) {
-        V x[U][NV];
-        const int q = r0 >> 5;  // (U divides 32: a step's rows share one id register)
-        const int32_t idq = q == 0 ? id0 : q == 1 ? id1 : q == 2 ? id2 : id3;
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu) {  // U rows in flight, whatever their colour groups
-          const int r = r0 + uu;
-          const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, idq, r & 31);
-          const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            if (r < n_s && valid[j]) x[uu][j] = __ldg(row + 32 * j);
-            else zero_vec(x[uu][j]);
-          }
-        }
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-          const int r = r0 + uu;
-          if (r < n_s) {  // warp-uniform
-            if (r == gend || nb == 32) {
-              flush();
-              nb = 0;
-              if (r == gend) open();
-            }
-#pragma unroll
-            for (int j = 0; j < NV; ++j) add_same(blk[j], x[uu][j]);
-            ++nb;
-          }
-        }
-      }
-      if (n_s > 0) flush();
-    }
-    if (a.root_mode) root_epilogue<T, AccT>(a, sacc, it, v, heavy, lane);
-    else gather_epilogue<T, 32, AccT>(a, sacc, it, v, heavy, lane, 0xffffffffu);
-    __syncwarp();
-  }
-}
-
-template <typename T, int NV, int U, int MINB>
-void stream_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
-  static_assert(32 % U == 0, "a step's rows must share one id register");
-  constexpr int VW = Vec<T>::W;
-  constexpr int CAP = 32 * NV * VW;
-  const bool acc32 = sizeof(T) == 4 && (a.W_out > 1600 || (kn.acc32 && !a.root_mode));
-  auto kern = acc32 ? k_gather_stream<T, NV, U, float, MINB> : k_gather_stream<T, NV, U, double, MINB>;
-  const size_t row = (size_t)(a.W_out + 1) * (acc32 ? sizeof(float) : sizeof(double));
-  int warps = 8;
-  while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
-  const int threads = warps * 32;
-  const size_t smem = row * warps;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, threads, smem, num_sms);
-  const int nch = (a.W_in + CAP - 1) / CAP;
-  kern<<<grid, threads, smem, s>>>(a, nch);
-}
-
 template <typename T, int NV, int B>
 void short_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
@@ -1474,15 +1308,6 @@ int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t
         else if (wvec <= 64) ldg_go<T, 2, 2, 3>(t, kn, num_sms, s);
         else if (wvec <= 96) ldg_go<T, 3, 2, 3>(t, kn, num_sms, s);
         else ldg_go<T, 4, 2>(t, kn, num_sms, s);
-      } else if (kn.short_lists >= 5 && kn.short_lists <= 7) {  // streamed across colour groups
-        // (ptxas: U = 4 rows of 3 vectors fit 2 CTAs/SM without spills; U = 2 at 3 CTAs/SM spills)
-        if (wvec <= 32) stream_go<T, 1, 4, 4>(t, kn, num_sms, s);
-        else if (wvec <= 64) {
-          if (kn.short_lists == 6) stream_go<T, 2, 2, 3>(t, kn, num_sms, s);
-          else if (kn.short_lists == 7) stream_go<T, 2, 8, 2>(t, kn, num_sms, s);
-          else stream_go<T, 2, 4, 2>(t, kn, num_sms, s);
-        } else if (wvec <= 96) stream_go<T, 3, 4, 2>(t, kn, num_sms, s);
-        else stream_go<T, 4, 2, 2>(t, kn, num_sms, s);
       } else if (kn.short_lists == 4) {  // U = 3 at 3 CTAs/SM
         if (wvec <= 32) ldg_go<T, 1, 3, 3>(t, kn, num_sms, s);
         else if (wvec <= 64) ldg_go<T, 2, 3, 3>(t, kn, num_sms, s);

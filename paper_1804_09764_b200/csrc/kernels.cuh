@@ -38,8 +38,7 @@ struct Knobs {
                            //               the NVTX range "cc_dominant" (one-launch ncu measurement)
   int short_lists = 2;     // CC_SHORT_LISTS: the short tail of wide-row gathers: 0 = with the long lists,
                            //   1 = k_gather_short, 2 = lean kernel U = 2 at 3 CTAs/SM (measured best),
-                           //   3 = U = 1 at 4 CTAs/SM, 4 = U = 3 at 3 CTAs/SM, 5..7 = k_gather_stream
-                           //   (rows streamed across colour groups; 6, 7: other U for 64-vector rows)
+                           //   3 = U = 1 at 4 CTAs/SM, 4 = U = 3 at 3 CTAs/SM
   int rows_variant = 0;    // CC_ROWS_VARIANT: row-parallel narrow kernel: 0 = U 4 at 3 CTAs/SM,
                            //   1 = U 2 at 4 CTAs/SM, 2 = U 8 at 2 CTAs/SM
   int short_split = 4;     // CC_SHORT_SPLIT: q, the short tail = light items with <= 8 << q neighbours
