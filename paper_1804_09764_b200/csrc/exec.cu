@@ -277,10 +277,7 @@ void replan(cc_ctx *c, bool fixed) {
 void upload_template(cc_ctx *c) {
   ++c->epoch;
   for (auto *p : c->d_split) c->pfree(p);
-  for (auto *p : c->d_ztab) {
-    if (p) dev::unregister_zcover(p);
-    c->pfree(p);
-  }
+  for (auto *p : c->d_ztab) c->pfree(p);
   for (auto *p : c->d_map) c->pfree(p);
   for (auto *p : c->d_skip) c->pfree(p);
   c->pfree(c->d_comp);
@@ -339,7 +336,6 @@ void upload_template(cc_ctx *c) {
             if (e[i] != 0xFFFF) e[i] = (uint16_t)L[st.t].pos[e[i]];
         }
         c->d_ztab[s] = c->pupload(zt);
-        dev::register_zcover(c->d_ztab[s], zt);
         c->zblocks[s] = nb;
       }
     }

@@ -1308,9 +1308,6 @@ int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t
         else if (wvec <= 64) ldg_go<T, 2, 2, 3>(t, kn, num_sms, s);
         else if (wvec <= 96) ldg_go<T, 3, 2, 3>(t, kn, num_sms, s);
         else ldg_go<T, 4, 2>(t, kn, num_sms, s);
-      } else if (kn.short_lists == 5 && wvec <= 96) {  // half a warp per row, two rows per load instruction
-        if (wvec <= 48) rows_go<T, 16, 3, 2, 3>(t, kn, num_sms, s);
-        else rows_go<T, 16, 6, 2, 2>(t, kn, num_sms, s);
       } else if (kn.short_lists == 4) {  // U = 3 at 3 CTAs/SM
         if (wvec <= 32) ldg_go<T, 1, 3, 3>(t, kn, num_sms, s);
         else if (wvec <= 64) ldg_go<T, 2, 3, 3>(t, kn, num_sms, s);

@@ -22,9 +22,6 @@
 // A step whose active part is the single root vertex (a = 1) needs no kernel:
 // in the compressed layout its table IS the neighbour sum N''.
 #include <algorithm>
-#include <mutex>
-#include <unordered_map>
-#include <vector>
 
 #include "dev_common.cuh"
 
@@ -358,33 +355,19 @@ struct ZTab {
   }
 };
 
-// The cover as a kernel parameter (configs[3]'s (9;6,3): 25 blocks x 219
-// entries = 21.9 KB): entries read with a warp-uniform index land in uniform
-// registers (LDCU), so every staged-tile load is one LDS [R + UR] -- no
-// address add, no shared-memory table.  Entries as in the shared-memory
-// table: byte offsets of the active / passive sets, then the output columns.
-constexpr int kZParamMax = 7900;  // 31.6 KB of the 32 KB kernel-parameter space
-struct alignas(16) ZParam {
-  uint32_t e[kZParamMax];
-};
-
-template <typename T, int ZS, int AS, int V, bool PT = false>
+template <typename T, int ZS, int AS, int V>
 __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, int64_t ldA, int WA,
                                                       const T *__restrict__ N, int64_t ldN, int WN,
                                                       const uint16_t *__restrict__ ztab, int nblocks, int zld, int64_t n,
                                                       T *__restrict__ out, int64_t ldO, int nbuf,
-                                                      const uint16_t *__restrict__ comp, double *__restrict__ per_vertex,
-                                                      const __grid_constant__ ZParam zp) {
+                                                      const uint16_t *__restrict__ comp, double *__restrict__ per_vertex) {
   constexpr ZTab<ZS, AS> tab{};
   constexpr int PS = ZS - 1 - AS, NA = ZTab<ZS, AS>::NA, NN = ZTab<ZS, AS>::NN;
   constexpr int S = 33;
   constexpr int TV = 32 * V;
   using LV = typename LaneVec<T, V>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // (the warp index through a shuffle from lane 0: provably warp-uniform, so
-  // the cover entries of the warp's blocks are uniform loads)
-  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0),
-            nwarp = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int W = WA + WN;
   const size_t bstride = ((size_t)S * V * W * sizeof(T) + 15) / 16 * 16 / sizeof(T);
   T *bufs = reinterpret_cast<T *>(smem_raw);
@@ -393,8 +376,7 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
   // columns -- one LDS.128 gives 4 ready addresses
   constexpr uint32_t CB = S * sizeof(LV);
   uint32_t *zs = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * bstride);
-  const int zsn = PT ? 0 : nblocks * zld;  // shared-memory table entries
-  for (int i = threadIdx.x; i < zsn; i += blockDim.x) {
+  for (int i = threadIdx.x; i < nblocks * zld; i += blockDim.x) {
     const uint32_t x = ztab[i];
     zs[i] = (i % zld) < NA + NN ? x * CB : x;
   }
@@ -403,7 +385,7 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
   // be) is multiplied in fp64 by the staged N''(v, comp X') -- the root step
   // (Eq. 2 at the root) shares this step's passive -- and the per-warp sums
   // are added in warp order into X_v (Eq. 3's summand)
-  double *red = reinterpret_cast<double *>(smem_raw + ((size_t)nbuf * bstride * sizeof(T) + (size_t)zsn * 4 + 7) / 8 * 8);
+  double *red = reinterpret_cast<double *>(smem_raw + ((size_t)nbuf * bstride * sizeof(T) + (size_t)nblocks * zld * 4 + 7) / 8 * 8);
   const int64_t ntiles = (n + TV - 1) / TV;
   auto stage = [&](int64_t tile, T *b) {
     const int64_t v0 = tile * TV;
@@ -436,15 +418,11 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
 #pragma unroll
     for (int i = 0; i < V; ++i) rsum[i] = 0.0;
     for (int zb = warp; zb < nblocks; zb += nwarp) {
-      const uint32_t *e = PT ? zp.e + zb * zld : zs + (size_t)zb * zld;
-      // shared-memory table: entries read 4 at a time (one 16-byte broadcast
-      // load per 4 ready byte offsets); parameter table: uniform loads
+      const uint32_t *e = zs + (size_t)zb * zld;
+      // block entries read 4 at a time (one 16-byte broadcast load per 4
+      // ready byte offsets)
       const uint4 *e4 = reinterpret_cast<const uint4 *>(e);
       auto off = [&](int i) -> uint32_t {
-        if constexpr (PT) {  // (zld padded to a multiple of 4: 8-byte uniform loads)
-          const uint2 w = reinterpret_cast<const uint2 *>(zp.e)[(zb * zld >> 1) + (i >> 1)];
-          return (i & 1) ? w.y : w.x;
-        }
         const uint4 w = e4[i >> 2];
         return (i & 3) == 0 ? w.x : (i & 3) == 1 ? w.y : (i & 3) == 2 ? w.z : w.w;
       };
@@ -468,7 +446,7 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
       }
 #pragma unroll
       for (int zz = 0; zz < ZS; ++zz) {
-        const uint32_t oc = off(NA + NN + zz);
+        const uint32_t oc = e[NA + NN + zz];
         if (oc != 0xFFFFu) {
           if (per_vertex) {
             const LV ny = *reinterpret_cast<const LV *>(Nb + (uint32_t)__ldg(comp + oc) * CB);
@@ -719,50 +697,15 @@ bool combine_z_supported(int elem, int ts, int as) {
   return ts == 6 && as == 3;
 }
 
-// Host copies of the Z-block cover tables, by device pointer (the launcher
-// passes the cover to k_combine_z as a kernel parameter when it fits).
-namespace {
-std::mutex g_zcover_mu;
-std::unordered_map<const uint16_t *, std::vector<uint16_t>> g_zcover;
-}  // namespace
-void register_zcover(const uint16_t *dev, const std::vector<uint16_t> &host) {
-  std::lock_guard<std::mutex> l(g_zcover_mu);
-  g_zcover[dev] = host;
-}
-void unregister_zcover(const uint16_t *dev) {
-  std::lock_guard<std::mutex> l(g_zcover_mu);
-  g_zcover.erase(dev);
-}
-std::vector<uint16_t> zcover_host(const uint16_t *dev) {
-  std::lock_guard<std::mutex> l(g_zcover_mu);
-  auto it = g_zcover.find(dev);
-  return it == g_zcover.end() ? std::vector<uint16_t>() : it->second;
-}
-
 namespace {
 template <typename T, int ZS, int AS>
 int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint16_t *ztab, int nblocks,
-         int zld, int64_t n, void *out, int64_t ldO, int num_sms, cudaStream_t s, bool zparam,
-         const uint16_t *comp = nullptr, double *per_vertex = nullptr) {
+         int zld, int64_t n, void *out, int64_t ldO, int num_sms, cudaStream_t s, const uint16_t *comp = nullptr,
+         double *per_vertex = nullptr) {
   const size_t cap = 227 * 1024;
   const size_t tile = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
-  // the cover as a kernel parameter when it fits (and its host copy is known)
-  ZParam zp;  // host staging (the launch copies the parameters)
-  const std::vector<uint16_t> host = zparam ? zcover_host(ztab) : std::vector<uint16_t>();
-  const int zldp = (zld + 3) / 4 * 4;  // the parameter table's row stride
-  const bool pt = (int64_t)host.size() == (int64_t)nblocks * zld && (int64_t)nblocks * zldp <= kZParamMax;
-  if (pt) {
-    using LV = typename LaneVec<T, 1>::type;
-    const uint32_t CB = 33 * sizeof(LV);
-    const int NA = cbinom(ZS, AS), NN = cbinom(ZS, ZS - 1 - AS);
-    for (int b = 0; b < nblocks; ++b)
-      for (int i = 0; i < zldp; ++i) {
-        const uint32_t x = i < zld ? host[(size_t)b * zld + i] : 0xFFFFu;
-        zp.e[(size_t)b * zldp + i] = i < NA + NN ? x * CB : x;
-      }
-  }
   // (+ the fused root's per-warp vertex sums: 16 warps x 32 doubles)
-  const size_t zbytes = (pt ? 0 : ((size_t)nblocks * zld * 4 + 7) / 8 * 8) + (per_vertex ? 16 * 32 * 8 : 0);
+  const size_t zbytes = ((size_t)nblocks * zld * 4 + 7) / 8 * 8 + (per_vertex ? 16 * 32 * 8 : 0);
   if (tile + zbytes > cap) return 0;
   // two single-buffered CTAs of 8 warps per SM when they fit (one computes
   // while the other stages or waits at its barrier; measured 5% faster on
@@ -773,11 +716,11 @@ int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN,
     threads = 256;
   }
   const size_t smem = nbuf * tile + zbytes;
-  auto kern = pt ? k_combine_z<T, ZS, AS, 1, true> : k_combine_z<T, ZS, AS, 1, false>;
+  auto kern = k_combine_z<T, ZS, AS, 1>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = persistent_grid(kern, threads, smem, num_sms);
   kern<<<grid, threads, smem, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, ztab,
-                                   nblocks, pt ? zldp : zld, n, static_cast<T *>(out), ldO, nbuf, comp, per_vertex, zp);
+                                   nblocks, zld, n, static_cast<T *>(out), ldO, nbuf, comp, per_vertex);
   return 1;
 }
 }  // namespace
@@ -788,11 +731,11 @@ int launch_combine_root(int elem, const void *A, int64_t ldA, int WA, const void
   if (n == 0 || !ztab || !comp || !per_vertex) return 0;
   if (kn.combine_impl >= 2) return 0;
   if (elem == 4 && ts == 8 && as == 5)
-    return z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, kn.zparam != 0, comp, per_vertex);
+    return z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
   if (elem == 4 && ts == 6 && as == 3)
-    return z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, kn.zparam != 0, comp, per_vertex);
+    return z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
   if (elem == 8 && ts == 6 && as == 3)
-    return z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, kn.zparam != 0, comp, per_vertex);
+    return z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
   return 0;
 }
 
@@ -802,9 +745,9 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
   if (n == 0) return 0;
   if (ztab && kn.combine_impl <= 1) {  // the Z-block kernel when the shape has one
     int l = 0;
-    if (elem == 4 && ts == 8 && as == 5) l = z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s, kn.zparam != 0);
-    else if (elem == 4 && ts == 6 && as == 3) l = z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s, kn.zparam != 0);
-    else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s, kn.zparam != 0);
+    if (elem == 4 && ts == 8 && as == 5) l = z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
+    else if (elem == 4 && ts == 6 && as == 3) l = z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
+    else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
     if (l) return l;
   }
   if (elem == 8)

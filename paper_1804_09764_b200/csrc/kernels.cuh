@@ -11,7 +11,6 @@
 #pragma once
 
 #include <cstdint>
-#include <vector>
 #include <cuda_runtime.h>
 
 namespace cc {
@@ -51,8 +50,6 @@ struct Knobs {
   int pair_gather = 0;     // CC_PAIR_GATHER: 1 = sibling narrow passives ready at the same time are summed
                            //   in one traversal (one rank); measured slower on configs[3] (33.7 ms for the
                            //   p = 2 + p = 3 pair against 25.1 ms unpaired, profiles/r2/SUMMARY.md)
-  int zparam = 1;          // CC_ZPARAM: 1 = the Z-block combine reads its cover from the kernel parameters
-                           //   (uniform loads) when it fits in 31.6 KB; 0 = from shared memory
   int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
                                 //   per batch in column chunks of this width (0 = by memory)
 };
@@ -173,11 +170,6 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
                    int nblocks, int zld, int ts, int as, const Knobs &kn, int num_sms, cudaStream_t s);
 bool combine_z_supported(int elem, int ts, int as);
-// Host copy of a Z-block cover uploaded at `dev` (k_combine_z then takes the
-// cover as a kernel parameter when it fits); unregister before freeing dev.
-void register_zcover(const uint16_t *dev, const std::vector<uint16_t> &host);
-void unregister_zcover(const uint16_t *dev);
-std::vector<uint16_t> zcover_host(const uint16_t *dev);
 // The combine restricted to the output columns [o_lo, o_hi) (a column chunk
 // of the output table): out is the chunk's virtual base (column o
 // of row v at out[v * ldO + o]); lane or V-tile kernel.
