@@ -594,17 +594,18 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
 
   for (int64_t it = a.item_from + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items;
        it += ngroups) {
-    int32_t v;
-    int64_t b, e;
-    const bool heavy = item_range(a.work, a.beg, a.end, it, v, b, e);
-    const int cv = a.colors[v];
+    // the item's descriptor (one 32-byte load): first neighbour position,
+    // vertex, stream length (the neighbours minus v's own colour group),
+    // that group's start and size, v's colour, heavy segment or not
+    const int4 dx = __ldg(reinterpret_cast<const int4 *>(a.desc + it));
+    const int4 dy = __ldg(reinterpret_cast<const int4 *>(a.desc + it) + 1);
+    const int64_t b = (int64_t)(((uint64_t)(uint32_t)dx.y << 32) | (uint32_t)dx.x);
+    const int32_t v = dx.z;
+    const int n_s = dx.w, cv_lo = dy.x, skip = dy.y, cv = dy.z;
+    const bool heavy = dy.w != 0;
     for (int j = lane; j < a.W_out; j += G) sacc[j] = 0.0;
     __syncwarp(gmask);
     const uint16_t *go = a.goff + it * 16;
-    // the stream = the item's neighbours minus the group of v's own colour
-    const int cv_lo = cv == 0 ? 0 : go[cv - 1], cv_hi = go[cv];
-    const int skip = cv_hi - cv_lo;
-    const int n_s = (int)(e - b) - skip;
     for (int ch = 0; ch < nch; ++ch) {
       const int c0 = ch * CAP + lane * VW;
       int nbytes[NV];
@@ -647,17 +648,31 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
       };
 #pragma unroll
       for (int r = 0; r < D - 1; ++r) issue(r);
-      // current colour group (stream coordinates)
-      int gc = 0, gend_s = 0;
-      auto next_group = [&]() {
-        while (gc < a.k) {
-          const int lo = gc == 0 ? 0 : go[gc - 1], hi = go[gc];
-          if (gc != cv && hi > lo) {
-            gend_s = hi - (gc > cv ? skip : 0);
-            return;
-          }
-          ++gc;
+      // current colour group (stream coordinates): the non-empty groups
+      // other than v's own as a bit mask from the item's 16 group ends (two
+      // 16-byte loads), so that the walk skips empty colours without loads
+      int gc = 0, gend_s = -1;
+      unsigned gleft = 0;
+      {
+        const uint4 ga = __ldg(reinterpret_cast<const uint4 *>(go)), gb = __ldg(reinterpret_cast<const uint4 *>(go) + 1);
+        const uint32_t gw[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        int prev = 0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int hi = (int)((gw[c >> 1] >> (16 * (c & 1))) & 0xFFFFu);
+          if (c < a.k && c != cv && hi > prev) gleft |= 1u << c;
+          prev = hi;
         }
+      }
+      auto next_group = [&]() {
+        if (!gleft) {
+          gc = a.k;
+          gend_s = -1;
+          return;
+        }
+        gc = __ffs(gleft) - 1;
+        gleft &= gleft - 1;
+        gend_s = (int)go[gc] - (gc > cv ? skip : 0);
       };
       next_group();
       double acc[NV][VW];
@@ -699,7 +714,6 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
           if constexpr (PAIR) expand_pair<NV, VW, G>(a, gc, cv, lane, acc, sacc);
           else expand<NV, VW, G>(a, gc, cv, c0, acc, sacc);
           __syncwarp(gmask);
-          ++gc;
           next_group();
         }
       }
