@@ -491,42 +491,60 @@ __device__ __forceinline__ void root_epilogue(const GatherArgs &a, AccT *sacc, i
   if (lane == 0) a.per_vertex[v] = d;
 }
 
-// expand one colour group's column sums into N'' (map injective per colour pair)
+// expand with the group's colour-pair map already in registers (packed
+// 16-bit entries, loaded when the group opened, so that its latency hides
+// behind the group's rows); rings of G <= 8 lanes send 0xFFFF entries to the
+// discard slot sacc[W_out] (all loads before the stores), G = 32 branches
 template <int NV, int VW, int G>
-__device__ __forceinline__ void expand(const GatherArgs &a, int cu, int cv, int c0, double (&acc)[NV][VW],
-                                       double *sacc) {
-  // (the branch-free form with a discard slot, as in the lean kernels,
-  // faulted -- illegal instruction -- in the G = 32 ring variant; the rings
-  // keep the branches)
+__device__ __forceinline__ void expand_map(const GatherArgs &a, const uint32_t (&mp)[NV][2], double (&acc)[NV][VW],
+                                           double *sacc) {
+  if constexpr (G <= 8) {
+    const uint32_t discard = (uint32_t)a.W_out;
+    double *d[NV][VW];
+    double old[NV][VW];
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int q = 0; q < VW; ++q) {
+        d[j][q] = sacc + min((mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu, discard);
+        old[j][q] = *d[j][q];
+      }
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int q = 0; q < VW; ++q) {
+        *d[j][q] = old[j][q] + acc[j][q];
+        acc[j][q] = 0.0;
+      }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int q = 0; q < VW; ++q) {
+        const uint32_t m = (mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+        if (m != 0xFFFFu) sacc[m] += acc[j][q];
+        acc[j][q] = 0.0;
+      }
+  }
+}
+// the group's map entries for the lane's vectors (0xFFFF past the row end)
+template <int NV, int VW, int G>
+__device__ __forceinline__ void load_map(const GatherArgs &a, int cu, int cv, int c0, uint32_t (&mp)[NV][2]) {
   const uint16_t *mrow = a.map + (int64_t)(cu * a.k + cv) * a.map_ld + a.col_base;
-  uint32_t m[NV][VW];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int y0 = c0 + j * G * VW;
+    mp[j][0] = mp[j][1] = 0xFFFFFFFFu;
     if (y0 < a.W_in) {
-      if (VW == 4) {
+      if constexpr (VW == 4) {
         const uint2 w = __ldg(reinterpret_cast<const uint2 *>(mrow + y0));
-        m[j][0] = w.x & 0xFFFF;
-        m[j][1] = w.x >> 16;
-        m[j][2 % VW] = w.y & 0xFFFF;
-        m[j][3 % VW] = w.y >> 16;
+        mp[j][0] = w.x;
+        mp[j][1] = w.y;
       } else {
-        const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(mrow + y0));
-        m[j][0] = w & 0xFFFF;
-        m[j][1 % VW] = w >> 16;
+        mp[j][0] = __ldg(reinterpret_cast<const uint32_t *>(mrow + y0));
       }
-    } else {
-#pragma unroll
-      for (int q = 0; q < VW; ++q) m[j][q] = 0xFFFF;
     }
   }
-#pragma unroll
-  for (int j = 0; j < NV; ++j)
-#pragma unroll
-    for (int q = 0; q < VW; ++q) {
-      if (m[j][q] != 0xFFFF) sacc[m[j][q]] += acc[j][q];
-      acc[j][q] = 0.0;
-    }
 }
 
 // the same for a sibling pair (virtual vectors lane + j G)
@@ -664,6 +682,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
           prev = hi;
         }
       }
+      uint32_t mp[NV][2];  // the open group's colour-pair map (non-pair rings)
       auto next_group = [&]() {
         if (!gleft) {
           gc = a.k;
@@ -673,6 +692,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
         gc = __ffs(gleft) - 1;
         gleft &= gleft - 1;
         gend_s = (int)go[gc] - (gc > cv ? skip : 0);
+        if constexpr (!PAIR) load_map<NV, VW, G>(a, gc, cv, c0, mp);
       };
       next_group();
       double acc[NV][VW];
@@ -712,7 +732,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
         }
         if (i + 1 == gend_s) {  // end of a colour group: expand into N''
           if constexpr (PAIR) expand_pair<NV, VW, G>(a, gc, cv, lane, acc, sacc);
-          else expand<NV, VW, G>(a, gc, cv, c0, acc, sacc);
+          else expand_map<NV, VW, G>(a, mp, acc, sacc);
           __syncwarp(gmask);
           next_group();
         }
