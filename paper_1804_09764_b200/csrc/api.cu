@@ -95,6 +95,7 @@ int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
   if (name == "short_split") return &k.short_split;
   if (name == "rows_variant") return &k.rows_variant;
   if (name == "pair_gather") return &k.pair_gather;
+  if (name == "combine_wreg") return &k.combine_wreg;
   if (name == "nvtx_mark") return &k.nvtx_mark;
   if (name == "tail_recompute_cols") return &k.tail_recompute_cols;
   return nullptr;
@@ -105,7 +106,7 @@ void knobs_from_env(cc::dev::Knobs &k) {
   static const char *names[] = {"fused_root", "sector_skip", "gather_impl", "narrow_impl", "narrow_split",
                                 "csort_small", "combine_impl", "acc32", "phase_events", "hub_l2_pct", "grid_reserve",
                                 "tail_batches", "tail_recompute_cols", "layout", "nvtx_mark", "lean_split", "short_lists", "short_split", "rows_variant",
-                                "pair_gather"};
+                                "pair_gather", "combine_wreg"};
   for (const char *n : names) {
     std::string env = "CC_";
     for (const char *q = n; *q; ++q) env += (char)std::toupper((unsigned char)*q);

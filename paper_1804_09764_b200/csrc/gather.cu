@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) k_csort(const int64_t *__restrict__ beg, 
 // N''(v, {y}) (heavy segments add their counts atomically into zeroed rows:
 // small integers, exact in fp32/fp64).
 template <typename T>
-__global__ void __launch_bounds__(256) k_csort2(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+__global__ void __launch_bounds__(256, 5) k_csort2(const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
                                                 const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
                                                 AggWork work, int k, int32_t *__restrict__ col_out,
                                                 uint16_t *__restrict__ goff, ItemDesc *__restrict__ desc,
@@ -122,16 +122,36 @@ __global__ void __launch_bounds__(256) k_csort2(const int64_t *__restrict__ beg,
   auto vertex_of = [&](int64_t it) -> int32_t {
     return it < work.n_seg ? work.seg_v[it] : (it < n_items ? work.light[it - work.n_seg] : 0);
   };
+  // three-stage prefetch across the warp's items: the vertex of item
+  // it + 2 nw, the neighbour range and the first 32 neighbour ids of item
+  // it + nw are in flight while item it is sorted (78% of configs[3]'s
+  // items have <= 32 neighbours: their sort then starts with the colour
+  // loads)
   int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  int32_t v_next = vertex_of(it);             // stage 1 of item it
-  int32_t v_next2 = vertex_of(it + nwarps);   // stage 1 of item it + nw
+  auto range_of = [&](int64_t i, int32_t vv, int64_t &bb, int64_t &ee) {
+    if (i >= n_items) {
+      bb = ee = 0;
+    } else if (i < work.n_seg) {
+      bb = work.seg_b[i];
+      ee = work.seg_e[i];
+    } else {
+      bb = beg[vv];
+      ee = end[vv];
+    }
+  };
+  int32_t v_next = vertex_of(it);
+  int64_t b_next, e_next;
+  range_of(it, v_next, b_next, e_next);
+  int32_t u_next = lane < e_next - b_next ? __ldg(col + b_next + lane) : 0;
+  int32_t v_next2 = vertex_of(it + nwarps);
   for (; it < n_items; it += nwarps) {
     const int32_t v = v_next;
     const bool heavy = it < work.n_seg;
-    const int64_t b = heavy ? work.seg_b[it] : beg[v];
-    const int64_t e = heavy ? work.seg_e[it] : end[v];
+    const int64_t b = b_next, e = e_next;
     const int cv = colors[v];
+    const int32_t u0 = u_next;
     v_next = v_next2;
+    range_of(it + nwarps, v_next, b_next, e_next);
     v_next2 = vertex_of(it + 2 * nwarps);
     const int d = (int)(e - b);
     cs[lane] = 0;
@@ -141,9 +161,10 @@ __global__ void __launch_bounds__(256) k_csort2(const int64_t *__restrict__ beg,
 #pragma unroll
     for (int ci = 0; ci < R; ++ci) {
       const bool ok = ci * 32 + lane < d;
-      ur[ci] = ok ? __ldg(col + b + ci * 32 + lane) : 0;
+      ur[ci] = ok ? (ci == 0 ? u0 : __ldg(col + b + ci * 32 + lane)) : 0;
       cr[ci] = ok ? (int)colors[ur[ci]] : 16 + lane % 16;  // invalid lanes: own groups, never counted
     }
+    u_next = lane < e_next - b_next ? __ldg(col + b_next + lane) : 0;  // the next item's first ids
 #pragma unroll
     for (int ci = 0; ci < R; ++ci) {
       if (ci * 32 < d) {

@@ -122,6 +122,63 @@ __global__ void __launch_bounds__(256) k_combine(const T *__restrict__ A, int64_
 // next vertex's already in registers), then a lane per output walks its split
 // pairs and the outputs go out coalesced.  Latency of the row loads is hidden
 // by the next vertex's prefetch and by 16 warps per SM.
+// The same walk with the split pairs in registers (nq = NQ splits per
+// output, <= 256 outputs): a lane owns outputs lane + 32 i for the whole
+// launch, so its split entries are loaded once; per vertex an output costs
+// NQ x (two shared-memory reads + FMA).  Same sums in the same order as
+// k_combine_warp.
+template <typename T, int PF, int NQ, int NO>
+__global__ void __launch_bounds__(256) k_combine_wreg(const T *__restrict__ A, int64_t ldA, int WA,
+                                                     const T *__restrict__ N, int64_t ldN, int WN,
+                                                     const uint32_t *__restrict__ split, int64_t n,
+                                                     T *__restrict__ out, int64_t ldO, int WO, int o_lo, int o_hi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int WOp = (WO + 7) & ~7, nout = o_hi - o_lo;
+  uint32_t sp[NO][NQ];
+#pragma unroll
+  for (int i = 0; i < NO; ++i)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int o = lane + 32 * i;
+      sp[i][q] = o < nout ? __ldg(split + (int64_t)q * WOp + o_lo + o) : 0u;
+    }
+  T *rows = reinterpret_cast<T *>(smem_raw) + (size_t)warp * (WA + WN);
+  const int64_t nw = (int64_t)gridDim.x * nwarp;
+  int64_t v = (int64_t)blockIdx.x * nwarp + warp;
+  T pa[PF], pn[PF];
+  auto fetch = [&](int64_t u) {
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+      const int x = lane + 32 * i;
+      pa[i] = (u < n && x < WA) ? __ldg(A + u * ldA + x) : (T)0;
+      pn[i] = (u < n && x < WN) ? __ldg(N + u * ldN + x) : (T)0;
+    }
+  };
+  fetch(v);
+  for (; v < n; v += nw) {
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+      const int x = lane + 32 * i;
+      if (x < WA) rows[x] = pa[i];
+      if (x < WN) rows[WA + x] = pn[i];
+    }
+    __syncwarp();
+    fetch(v + nw);  // the next vertex's rows are in flight during this one's walk
+#pragma unroll
+    for (int i = 0; i < NO; ++i) {
+      if (32 * i < nout) {  // warp-uniform
+        const int o = lane + 32 * i;
+        T acc = (T)0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc = fma(rows[sp[i][q] & 0xFFFF], rows[WA + (sp[i][q] >> 16)], acc);
+        if (o < nout) out[v * ldO + o_lo + o] = acc;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <typename T, int PF>
 __global__ void __launch_bounds__(256) k_combine_warp(const T *__restrict__ A, int64_t ldA, int WA,
                                                       const T *__restrict__ N, int64_t ldN, int WN,
@@ -648,6 +705,24 @@ int combine_typed(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN
     const size_t ssb = ((size_t)nq * nout * 4 + 15) & ~(size_t)15;
     const size_t smem = ssb + (size_t)8 * (WA + WN) * sizeof(T);
     const bool warp_ok = kn.combine_impl == 4 || (kn.combine_impl == 0 && WA <= 128 && WN <= 128);
+    if (warp_ok && WA <= 128 && WN <= 128 && (nq == 2 || nq == 3) && nout <= 256 && kn.combine_wreg) {
+      const size_t rsm = (size_t)8 * (WA + WN) * sizeof(T);
+      // (outputs per lane NO = 2, 6 or 8; rows per lane PF = 1, 2 or 4)
+      const int pf = (WA <= 32 && WN <= 32) ? 1 : (WA <= 64 && WN <= 64) ? 2 : 4;
+      const int no = nout <= 64 ? 2 : nout <= 192 ? 6 : 8;
+      using KW = decltype(&k_combine_wreg<T, 1, 2, 2>);
+      KW tab[3][2][3] = {{{k_combine_wreg<T, 1, 2, 2>, k_combine_wreg<T, 1, 2, 6>, k_combine_wreg<T, 1, 2, 8>},
+                          {k_combine_wreg<T, 1, 3, 2>, k_combine_wreg<T, 1, 3, 6>, k_combine_wreg<T, 1, 3, 8>}},
+                         {{k_combine_wreg<T, 2, 2, 2>, k_combine_wreg<T, 2, 2, 6>, k_combine_wreg<T, 2, 2, 8>},
+                          {k_combine_wreg<T, 2, 3, 2>, k_combine_wreg<T, 2, 3, 6>, k_combine_wreg<T, 2, 3, 8>}},
+                         {{k_combine_wreg<T, 4, 2, 2>, k_combine_wreg<T, 4, 2, 6>, k_combine_wreg<T, 4, 2, 8>},
+                          {k_combine_wreg<T, 4, 3, 2>, k_combine_wreg<T, 4, 3, 6>, k_combine_wreg<T, 4, 3, 8>}}};
+      KW kern = tab[pf == 1 ? 0 : pf == 2 ? 1 : 2][nq - 2][no == 2 ? 0 : no == 6 ? 1 : 2];
+      const int grid = persistent_grid(kern, 256, rsm, num_sms);
+      kern<<<grid, 256, rsm, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, split, n,
+                                  static_cast<T *>(out), ldO, WO, o_lo, o_hi);
+      return 1;
+    }
     if (warp_ok && WA <= 128 && WN <= 128 && smem <= 200 * 1024) {
       auto kern = (WA <= 32 && WN <= 32)   ? k_combine_warp<T, 1>
                   : (WA <= 64 && WN <= 64) ? k_combine_warp<T, 2>

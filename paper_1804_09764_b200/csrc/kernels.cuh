@@ -50,6 +50,8 @@ struct Knobs {
   int pair_gather = 0;     // CC_PAIR_GATHER: 1 = sibling narrow passives ready at the same time are summed
                            //   in one traversal (one rank); measured slower on configs[3] (33.7 ms for the
                            //   p = 2 + p = 3 pair against 25.1 ms unpaired, profiles/r2/SUMMARY.md)
+  int combine_wreg = 1;    // CC_COMBINE_WREG: warp-per-vertex combines with 2-3 splits per output keep the
+                           //   split pairs in registers (0: read them from shared memory per vertex)
   int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
                                 //   per batch in column chunks of this width (0 = by memory)
 };
