@@ -1264,6 +1264,8 @@ void ldg_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   const size_t row = (size_t)(a.W_out + 1) * (acc32 ? sizeof(float) : sizeof(double));  // + the discard slot
   int warps = 8;
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
+  // knob wide_warps: fewer warps per CTA for N'' rows of > 8 KB (more L1 left for the rows in flight)
+  if (kn.wide_warps > 0 && row > 8 * 1024) warps = std::min(warps, kn.wide_warps);
   const int threads = warps * 32;
   const size_t smem = row * warps;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1379,6 +1381,7 @@ int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t
     if (wvec <= 32) ldg_go<T, 1, 8>(a, kn, num_sms, s);
     else if (wvec <= 64) ldg_go<T, 2, 8>(a, kn, num_sms, s);
     else if (wvec <= 96) ldg_go<T, 3, 4>(a, kn, num_sms, s);
+    else if (kn.wide_nv == 6 && wvec > 128) ldg_go<T, 6, 2>(a, kn, num_sms, s);  // (knob wide_nv: fewer passes)
     else ldg_go<T, 4, 2>(a, kn, num_sms, s);
     return 1;
   }

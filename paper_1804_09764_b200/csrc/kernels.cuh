@@ -52,6 +52,8 @@ struct Knobs {
                            //   p = 2 + p = 3 pair against 25.1 ms unpaired, profiles/r2/SUMMARY.md)
   int combine_wreg = 1;    // CC_COMBINE_WREG: warp-per-vertex combines with 2-3 splits per output keep the
                            //   split pairs in registers (0: read them from shared memory per vertex)
+  int wide_warps = 0;      // CC_WIDE_WARPS: > 0 = warps per CTA of the lean gather for N'' rows of > 8 KB
+  int wide_nv = 4;         // CC_WIDE_NV: 16-byte vectors per lane per pass for rows of > 128 vectors (4 or 6)
   int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
                                 //   per batch in column chunks of this width (0 = by memory)
 };
