@@ -45,15 +45,30 @@ def headers():
                   + [os.path.join(ROOT, "include", "cc.h")])
 
 
+GEN = os.path.join(ROOT, "build", "gen")
+GENERATORS = [os.path.join(CSRC, "gen_combine_s.py")]
+
+
+def generate() -> None:
+    """Emit the generated headers (straight-line combine code) into build/gen."""
+    os.makedirs(GEN, exist_ok=True)
+    for g in GENERATORS:
+        out = os.path.join(GEN, os.path.basename(g).replace("gen_", "").replace(".py", "_gen.cuh"))
+        if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(g):
+            subprocess.run([sys.executable, g, out + ".tmp"], check=True)
+            os.replace(out + ".tmp", out)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sources()
-    newest = max(os.path.getmtime(p) for p in srcs + headers() + [__file__])
+    newest = max(os.path.getmtime(p) for p in srcs + headers() + GENERATORS + [__file__])
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
         return OUT
     os.makedirs(OBJ, exist_ok=True)
+    generate()
     nvcc = _nvcc()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp,-O3",
-              "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
+              "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(), "-I", GEN]
 
     def compile_one(src):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")

@@ -412,7 +412,10 @@ struct ZTab {
   }
 };
 
-template <typename T, int ZS, int AS, int V>
+// GT (global table): the cover stays in global memory (L1-cached, warp-uniform
+// 16-byte loads at each block's start) when it does not fit next to the tile --
+// configs[4]'s (7;4,3) at k = 15: 627 blocks x 160 B = 100 KB.
+template <typename T, int ZS, int AS, int V, bool GT = false>
 __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, int64_t ldA, int WA,
                                                       const T *__restrict__ N, int64_t ldN, int WN,
                                                       const uint16_t *__restrict__ ztab, int nblocks, int zld, int64_t n,
@@ -433,17 +436,33 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
   // columns -- one LDS.128 gives 4 ready addresses
   constexpr uint32_t CB = S * sizeof(LV);
   uint32_t *zs = reinterpret_cast<uint32_t *>(bufs + (size_t)nbuf * bstride);
-  for (int i = threadIdx.x; i < nblocks * zld; i += blockDim.x) {
-    const uint32_t x = ztab[i];
-    zs[i] = (i % zld) < NA + NN ? x * CB : x;
-  }
+  if constexpr (!GT)
+    for (int i = threadIdx.x; i < nblocks * zld; i += blockDim.x) {
+      const uint32_t x = ztab[i];
+      zs[i] = (i % zld) < NA + NN ? x * CB : x;
+    }
   // fused root (per_vertex != nullptr): the outputs are not stored; each
   // output T'(v, X') (rounded to the storage type, as the stored table would
   // be) is multiplied in fp64 by the staged N''(v, comp X') -- the root step
   // (Eq. 2 at the root) shares this step's passive -- and the per-warp sums
   // are added in warp order into X_v (Eq. 3's summand)
-  double *red = reinterpret_cast<double *>(smem_raw + ((size_t)nbuf * bstride * sizeof(T) + (size_t)nblocks * zld * 4 + 7) / 8 * 8);
+  double *red = reinterpret_cast<double *>(smem_raw + ((size_t)nbuf * bstride * sizeof(T) + (GT ? 0 : (size_t)nblocks * zld * 4) + 7) / 8 * 8);
   const int64_t ntiles = (n + TV - 1) / TV;
+  // GT: each warp's next cover block is prefetched by cp.async into a
+  // per-warp double buffer of zld raw entries, then turned into the ready
+  // 32-bit byte offsets of the shared-memory path (behind the fused root's sums)
+  uint16_t *wtab = reinterpret_cast<uint16_t *>(red + (per_vertex ? nwarp * TV : 0)) + (size_t)warp * 4 * zld;
+  uint32_t *woff = reinterpret_cast<uint32_t *>(wtab + 2 * zld);
+  int jt = 0;  // this warp's running block count (buffer parity)
+  auto tprefetch = [&](int zb, int buf) {
+    if (lane * 8 < zld) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(wtab + (size_t)buf * zld + lane * 8);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(ztab + (size_t)zb * zld + lane * 8)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (GT && warp < nblocks) tprefetch(warp, 0);
   auto stage = [&](int64_t tile, T *b) {
     const int64_t v0 = tile * TV;
     for (int r = warp; r < TV; r += nwarp) {
@@ -474,8 +493,26 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
     double rsum[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) rsum[i] = 0.0;
+    T *orow[V];  // the stored outputs' rows (nullptr past n)
+#pragma unroll
+    for (int i = 0; i < V; ++i) orow[i] = vb + i < n && out ? out + (vb + i) * ldO : nullptr;
     for (int zb = warp; zb < nblocks; zb += nwarp) {
       const uint32_t *e = zs + (size_t)zb * zld;
+      if constexpr (GT) {
+        const int nxt = zb + nwarp < nblocks ? zb + nwarp : warp;  // wraps to the next tile's first block
+        __syncwarp();  // the previous block's offsets are read
+        tprefetch(nxt, (jt + 1) & 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncwarp();
+        const uint16_t *raw = wtab + (size_t)(jt & 1) * zld;
+        for (int i = lane; i < zld; i += 32) {
+          const uint32_t x = raw[i];
+          woff[i] = i < NA + NN ? x * CB : x;
+        }
+        __syncwarp();
+        e = woff;
+        ++jt;
+      }
       // block entries read 4 at a time (one 16-byte broadcast load per 4
       // ready byte offsets)
       const uint4 *e4 = reinterpret_cast<const uint4 *>(e);
@@ -512,7 +549,7 @@ __global__ void __launch_bounds__(512, 1) k_combine_z(const T *__restrict__ A, i
           } else {
 #pragma unroll
             for (int i = 0; i < V; ++i)
-              if (vb + i < n) out[(vb + i) * ldO + oc] = acc[zz][i];
+              if (orow[i]) orow[i][oc] = acc[zz][i];
           }
         }
       }
@@ -776,12 +813,26 @@ namespace {
 template <typename T, int ZS, int AS>
 int z_go(const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, const uint16_t *ztab, int nblocks,
          int zld, int64_t n, void *out, int64_t ldO, int num_sms, cudaStream_t s, const uint16_t *comp = nullptr,
-         double *per_vertex = nullptr) {
+         double *per_vertex = nullptr, bool kn_zglobal = true) {
   const size_t cap = 227 * 1024;
   const size_t tile = ((size_t)(WA + WN) * 33 * sizeof(T) + 15) / 16 * 16;
   // (+ the fused root's per-warp vertex sums: 16 warps x 32 doubles)
   const size_t zbytes = ((size_t)nblocks * zld * 4 + 7) / 8 * 8 + (per_vertex ? 16 * 32 * 8 : 0);
-  if (tile + zbytes > cap) return 0;
+  if (tile + zbytes > cap) {
+    // the cover in global memory (16-byte aligned blocks of zld entries): two
+    // single-buffered CTAs of 8 warps per SM when two tiles fit
+    if (!kn_zglobal || (zld * 2) % 16 != 0) return 0;
+    const size_t tb = (size_t)16 * 4 * zld * 2;  // per-warp raw double buffer + ready offsets
+    const size_t gz = (per_vertex ? 16 * 32 * 8 : 0) + tb;
+    if (tile + gz > cap) return 0;
+    const int threads = 2 * (tile + gz) <= cap ? 256 : 512;
+    auto kern = k_combine_z<T, ZS, AS, 1, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(tile + gz));
+    const int grid = persistent_grid(kern, threads, tile + gz, num_sms);
+    kern<<<grid, threads, tile + gz, s>>>(static_cast<const T *>(A), ldA, WA, static_cast<const T *>(N), ldN, WN, ztab,
+                                          nblocks, zld, n, static_cast<T *>(out), ldO, 1, comp, per_vertex);
+    return 1;
+  }
   // two single-buffered CTAs of 8 warps per SM when they fit (one computes
   // while the other stages or waits at its barrier; measured 5% faster on
   // config 3), else one CTA of 16 warps, double-buffered when it fits
@@ -805,12 +856,14 @@ int launch_combine_root(int elem, const void *A, int64_t ldA, int WA, const void
                         double *per_vertex, const Knobs &kn, int num_sms, cudaStream_t s) {
   if (n == 0 || !ztab || !comp || !per_vertex) return 0;
   if (kn.combine_impl >= 2) return 0;
+  if (const int l = launch_combine_static(elem, A, ldA, WA, N, ldN, WN, ts, as, n, nullptr, 0, per_vertex, kn, num_sms, s))
+    return l;
   if (elem == 4 && ts == 8 && as == 5)
-    return z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
+    return z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex, kn.combine_zglobal);
   if (elem == 4 && ts == 6 && as == 3)
-    return z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
+    return z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex, kn.combine_zglobal);
   if (elem == 8 && ts == 6 && as == 3)
-    return z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex);
+    return z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, nullptr, 0, num_sms, s, comp, per_vertex, kn.combine_zglobal);
   return 0;
 }
 
@@ -819,10 +872,11 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
                    int nblocks, int zld, int ts, int as, const Knobs &kn, int num_sms, cudaStream_t s) {
   if (n == 0) return 0;
   if (ztab && kn.combine_impl <= 1) {  // the Z-block kernel when the shape has one
-    int l = 0;
-    if (elem == 4 && ts == 8 && as == 5) l = z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
-    else if (elem == 4 && ts == 6 && as == 3) l = z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
-    else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s);
+    int l = launch_combine_static(elem, A, ldA, WA, N, ldN, WN, ts, as, n, out, ldO, nullptr, kn, num_sms, s);
+    if (l) return l;
+    if (elem == 4 && ts == 8 && as == 5) l = z_go<float, 9, 5>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s, nullptr, nullptr, kn.combine_zglobal);
+    else if (elem == 4 && ts == 6 && as == 3) l = z_go<float, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s, nullptr, nullptr, kn.combine_zglobal);
+    else if (elem == 8 && ts == 6 && as == 3) l = z_go<double, 7, 3>(A, ldA, WA, N, ldN, WN, ztab, nblocks, zld, n, out, ldO, num_sms, s, nullptr, nullptr, kn.combine_zglobal);
     if (l) return l;
   }
   if (elem == 8)

@@ -50,6 +50,12 @@ struct Knobs {
   int pair_gather = 0;     // CC_PAIR_GATHER: 1 = sibling narrow passives ready at the same time are summed
                            //   in one traversal (one rank); measured slower on configs[3] (33.7 ms for the
                            //   p = 2 + p = 3 pair against 25.1 ms unpaired, profiles/r2/SUMMARY.md)
+  int combine_static = 1;  // CC_COMBINE_STATIC: the Z-block combines of (K; K-3, a') shapes with the
+                           //   cover, columns and register indices fixed at compile time (combine_s.cu):
+                           //   1 = K = 9 (configs[2]), 2 = also K = 11 (configs[3]; measured slower:
+                           //   instruction-fetch bound), 0 = never
+  int combine_zglobal = 1; // CC_COMBINE_ZGLOBAL: Z-block covers too large for shared memory (configs[4]'s
+                           //   (7;4,3), 627 blocks) read from global memory (0: lane kernel instead)
   int combine_wreg = 1;    // CC_COMBINE_WREG: warp-per-vertex combines with 2-3 splits per output keep the
                            //   split pairs in registers (0: read them from shared memory per vertex)
   int wide_warps = 0;      // CC_WIDE_WARPS: > 0 = warps per CTA of the lean gather for N'' rows of > 8 KB
@@ -174,6 +180,12 @@ int launch_combine(int elem, const void *A, int64_t ldA, int WA, const void *N, 
                    const uint32_t *split, int nq, int64_t n, void *out, int64_t ldO, int WO, const uint16_t *ztab,
                    int nblocks, int zld, int ts, int as, const Knobs &kn, int num_sms, cudaStream_t s);
 bool combine_z_supported(int elem, int ts, int as);
+// The compile-time-cover combine (combine_s.cu) for outputs of ts = K - 3
+// colours of the compressed K-universe, fp32, colex columns; per_vertex !=
+// nullptr = fused root (T' not stored, X_v written).  0 = shape unsupported.
+int launch_combine_static(int elem, const void *A, int64_t ldA, int WA, const void *N, int64_t ldN, int WN, int ts,
+                          int as, int64_t n, void *out, int64_t ldO, double *per_vertex, const Knobs &kn, int num_sms,
+                          cudaStream_t s);
 // The combine restricted to the output columns [o_lo, o_hi) (a column chunk
 // of the output table): out is the chunk's virtual base (column o
 // of row v at out[v * ldO + o]); lane or V-tile kernel.

@@ -258,6 +258,40 @@ def test_fused_combine_root(ci):
                 assert_close_entries(root, want.root.reshape(-1, 1), tol, f"fused combine root X_v config {ci}")
 
 
+@pytest.mark.parametrize("ci", [2, 3])
+def test_static_cover_combine(ci):
+    """The compile-time-cover combine (combine_s.cu, knob combine_static) for
+    configs[2]'s (7;4,3) at k = 10 and configs[3]'s (9;6,3) at k = 12, fp32:
+    fused with the root (T' never stored, X_v in its epilogue) and stored
+    (fused_root = 0, the root step reads the table).  Count and every X_v
+    against the oracle, and against the run-time-cover Z-block kernel
+    (combine_static = 0), on a dense small graph, a twin with hubs and a
+    ragged last tile (n not a multiple of 32)."""
+    cc = lib()
+    cfg = synth.CONFIGS[ci]
+    parent, k = cfg.parent, cfg.k
+    graphs = [synth.gnp(77, 0.2, 7), synth.scaled_twin(cfg, 10, 16).graph()]
+    for gi, g in enumerate(graphs):
+        col = oracle.color(g.n, k, 90 + gi)
+        want = oracle.dp_count(g, parent, col, oracle.NUM_LONGDOUBLE, want_root=True)
+        got = {}
+        with context(g, parent, "fp32") as ctx:
+            cc.cc_set_colors(ctx, col)
+            for static in (2, 0):  # 2: the static kernel for both shapes
+                cc.cc_set_knob(ctx, "combine_static", static)
+                for fused in (1, 0):
+                    cc.cc_set_knob(ctx, "fused_root", fused)
+                    x = cc.cc_count_colorful(ctx)
+                    assert cc.cc_last_stats(ctx)["fused_root"] == (3 if fused else 0), (ci, static, fused)
+                    root = cc.cc_get_subtree_counts(ctx, parent.index(-1), g.n, k, k)
+                    assert rel_err(x, float(want.total)) <= TOL_FP32, (ci, gi, static, fused)
+                    assert_close_entries(root, want.root.reshape(-1, 1), TOL_FP32,
+                                         f"static={static} fused={fused} X_v config {ci}")
+                    got[static, fused] = x
+        for key, x in got.items():
+            assert rel_err(x, got[2, 1]) <= TOL_FP32, key
+
+
 def test_subtree_rows_match_the_full_dump_and_the_oracle():
     """cc_get_subtree_rows (the sampled-row hook used at configs[4] scale)
     returns the same rows as the full-table dump and the oracle, including
@@ -684,7 +718,8 @@ KNOB_SETTINGS = [("gather_impl", 1), ("gather_impl", 2), ("narrow_impl", 0), ("n
                  ("narrow_split", 0), ("narrow_split", 7), ("csort_small", 0), ("sector_skip", 0),
                  ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("combine_impl", 4), ("acc32", 0),
                  ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1), ("short_lists", 0), ("short_lists", 1), ("short_lists", 3), ("short_split", 1), ("lean_split", 2),
-                 ("pair_gather", 1), ("rows_variant", 2), ("short_lists", 4), ("combine_wreg", 0)]
+                 ("pair_gather", 1), ("rows_variant", 2), ("short_lists", 4), ("combine_wreg", 0),
+                 ("combine_static", 0), ("combine_static", 2), ("combine_zglobal", 0)]
 
 
 @pytest.mark.parametrize("ci", [2, 3, 4])
