@@ -27,6 +27,7 @@
 //                  optionally evaluates the root step in its epilogue.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "dev_common.cuh"
 
@@ -385,6 +386,16 @@ struct AccScale<float> {
   static constexpr double in = 0x1p-64, out = 0x1p64;
 };
 
+// A block sum into the row's scale.  fp32 block, fp32 row: one FMUL by the
+// power of two -- exact, bit-identical to the route through fp64 (two F2F on
+// the 16-lane conversion pipe and a DMUL per entry, which made the per-group
+// flush of the short-tail launches conversion-bound).
+template <typename AccT, typename T>
+__device__ __forceinline__ AccT scale_in(T x) {
+  if constexpr (std::is_same<AccT, float>::value && std::is_same<T, float>::value) return x * 0x1p-64f;
+  else return (AccT)((double)x * AccScale<AccT>::in);
+}
+
 template <typename T, int G, typename AccT = double>
 __device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const AccT *sacc, int64_t it, int32_t v,
                                                 bool heavy, int lane, unsigned gmask) {
@@ -392,6 +403,12 @@ __device__ __forceinline__ void gather_epilogue(const GatherArgs &a, const AccT 
   // a sibling pair's part 2 goes to its own N'' table (entries o2.. of the virtual row)
   T *drow2 = a.src2 ? static_cast<T *>(a.dst2) + (int64_t)v * a.ld_dst2 - a.o2 : drow;
   if (!heavy) {
+    if constexpr (std::is_same<AccT, float>::value && std::is_same<T, float>::value) {
+      if (!a.accumulate && !a.src2) {  // fp32 row to fp32 table: the same value without the fp64 round trip
+        for (int j = lane; j < a.W_out; j += G) drow[j] = sacc[j] * 0x1p64f;
+        return;
+      }
+    }
     for (int j = lane; j < a.W_out; j += G) {
       T *d = j < a.o2 ? drow + j : drow2 + j;
       double x = (double)sacc[j] * AccScale<AccT>::out;
@@ -516,13 +533,13 @@ __device__ __forceinline__ void root_epilogue(const GatherArgs &a, AccT *sacc, i
 // 16-bit entries, loaded when the group opened, so that its latency hides
 // behind the group's rows); rings of G <= 8 lanes send 0xFFFF entries to the
 // discard slot sacc[W_out] (all loads before the stores), G = 32 branches
-template <int NV, int VW, int G>
-__device__ __forceinline__ void expand_map(const GatherArgs &a, const uint32_t (&mp)[NV][2], double (&acc)[NV][VW],
-                                           double *sacc) {
+template <int NV, int VW, int G, typename AccT = double>
+__device__ __forceinline__ void expand_map(const GatherArgs &a, const uint32_t (&mp)[NV][2], AccT (&acc)[NV][VW],
+                                           AccT *sacc) {
   if constexpr (G <= 8) {
     const uint32_t discard = (uint32_t)a.W_out;
-    double *d[NV][VW];
-    double old[NV][VW];
+    AccT *d[NV][VW];
+    AccT old[NV][VW];
 #pragma unroll
     for (int j = 0; j < NV; ++j)
 #pragma unroll
@@ -535,7 +552,7 @@ __device__ __forceinline__ void expand_map(const GatherArgs &a, const uint32_t (
 #pragma unroll
       for (int q = 0; q < VW; ++q) {
         *d[j][q] = old[j][q] + acc[j][q];
-        acc[j][q] = 0.0;
+        acc[j][q] = (AccT)0;
       }
   } else {
 #pragma unroll
@@ -544,7 +561,7 @@ __device__ __forceinline__ void expand_map(const GatherArgs &a, const uint32_t (
       for (int q = 0; q < VW; ++q) {
         const uint32_t m = (mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
         if (m != 0xFFFFu) sacc[m] += acc[j][q];
-        acc[j][q] = 0.0;
+        acc[j][q] = (AccT)0;
       }
   }
 }
@@ -612,8 +629,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // fp32 rows are summed in blocks of up to 8 consecutive rows in fp32 and the
 // blocks in fp64 (relative error <= 7 u32 + O(n u64) per entry; DESIGN.md
 // reading C-6); fp64 rows are summed in fp64.
-template <typename T, int G, int NV, int D, int MINB, bool PAIR = false>
+// AccT = float (fp32 tables, launches whose items have <= 1024 neighbours):
+// the blocks are added in fp32, scaled by 2^-64, and the N'' row is kept in
+// fp32 as in the lean gather -- at most ceil(1024 / 8) + k - 1 fp32 additions
+// per entry (C-6), no fp64 conversions or additions in the loop.
+template <typename T, int G, int NV, int D, int MINB, bool PAIR = false, typename AccT = double>
 __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch) {
+  static_assert(std::is_same<AccT, double>::value || (!PAIR && sizeof(T) == 4), "fp32 rows: unpaired fp32 tables");
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;  // input columns per pass
@@ -626,8 +648,8 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
   const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
   const int groups_per_block = blockDim.x / G;
   V *ring = reinterpret_cast<V *>(smem_ring) + (int64_t)grp * D * NV * G;  // [D][NV][G]
-  double *sacc = reinterpret_cast<double *>(reinterpret_cast<V *>(smem_ring) + (int64_t)groups_per_block * D * NV * G) +
-                 (int64_t)grp * (a.W_out + 1);  // + the discard slot
+  AccT *sacc = reinterpret_cast<AccT *>(reinterpret_cast<V *>(smem_ring) + (int64_t)groups_per_block * D * NV * G) +
+               (int64_t)grp * (a.W_out + 1);  // + the discard slot
   const T *__restrict__ src = static_cast<const T *>(a.src);
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
 
@@ -642,7 +664,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
     const int32_t v = dx.z;
     const int n_s = dx.w, cv_lo = dy.x, skip = dy.y, cv = dy.z;
     const bool heavy = dy.w != 0;
-    for (int j = lane; j < a.W_out; j += G) sacc[j] = 0.0;
+    for (int j = lane; j < a.W_out; j += G) sacc[j] = (AccT)0;
     __syncwarp(gmask);
     const uint16_t *go = a.goff + it * 16;
     for (int ch = 0; ch < nch; ++ch) {
@@ -716,11 +738,11 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
         if constexpr (!PAIR) load_map<NV, VW, G>(a, gc, cv, c0, mp);
       };
       next_group();
-      double acc[NV][VW];
+      AccT acc[NV][VW];
 #pragma unroll
       for (int j = 0; j < NV; ++j)
 #pragma unroll
-        for (int q = 0; q < VW; ++q) acc[j][q] = 0.0;
+        for (int q = 0; q < VW; ++q) acc[j][q] = (AccT)0;
       float4 blk[NV];
       int nb = 0;
 #pragma unroll
@@ -742,18 +764,26 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
           if (++nb == BLK || gend) {
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
-              add_vec(acc[j], blk[j]);
+              if constexpr (std::is_same<AccT, float>::value) {
+                acc[j][0] = fmaf(blk[j].x, 0x1p-64f, acc[j][0]);
+                acc[j][1] = fmaf(blk[j].y, 0x1p-64f, acc[j][1]);
+                acc[j][2] = fmaf(blk[j].z, 0x1p-64f, acc[j][2]);
+                acc[j][3] = fmaf(blk[j].w, 0x1p-64f, acc[j][3]);
+              } else {
+                add_vec(acc[j], blk[j]);
+              }
               blk[j] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             nb = 0;
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < NV; ++j) add_vec(acc[j], slot[j * G]);
+          for (int j = 0; j < NV; ++j)
+            if constexpr (std::is_same<AccT, double>::value) add_vec(acc[j], slot[j * G]);
         }
         if (i + 1 == gend_s) {  // end of a colour group: expand into N''
           if constexpr (PAIR) expand_pair<NV, VW, G>(a, gc, cv, lane, acc, sacc);
-          else expand_map<NV, VW, G>(a, mp, acc, sacc);
+          else expand_map<NV, VW, G, AccT>(a, mp, acc, sacc);
           __syncwarp(gmask);
           next_group();
         }
@@ -761,7 +791,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
       cp_async_wait<0>();
       __syncwarp(gmask);
     }
-    gather_epilogue<T, G>(a, sacc, it, v, heavy, lane, gmask);
+    gather_epilogue<T, G, AccT>(a, sacc, it, v, heavy, lane, gmask);
     __syncwarp(gmask);
   }
 }
@@ -914,7 +944,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
 #pragma unroll
           for (int j = 0; j < NV; ++j)
 #pragma unroll
-            for (int q = 0; q < VW; ++q) *d[j][q] = old[j][q] + (AccT)((double)vec_at(blk[j], q) * AccScale<AccT>::in);
+            for (int q = 0; q < VW; ++q) *d[j][q] = old[j][q] + scale_in<AccT>(vec_at(blk[j], q));
         }
         __syncwarp();  // groups of different colours may map to the same N'' entries
       }
@@ -1081,7 +1111,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
 #pragma unroll
           for (int j = 0; j < NV; ++j)
 #pragma unroll
-            for (int q = 0; q < VW; ++q) *d[j][q] = old[j][q] + (AccT)((double)vec_at(blk[j], q) * AccScale<AccT>::in);
+            for (int q = 0; q < VW; ++q) *d[j][q] = old[j][q] + scale_in<AccT>(vec_at(blk[j], q));
         }
         __syncwarp();  // groups of different colours may map to the same N'' entries
       }
@@ -1275,12 +1305,18 @@ void ldg_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <typename T, int G, int NV, int D, int MINB = 1, bool PAIR = false>
-void ring_go(const GatherArgs &a, const Knobs &, int num_sms, cudaStream_t s) {
+template <typename T, int G, int NV, int D, int MINB = 1, bool PAIR = false, bool SHORT = false>
+void ring_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   constexpr int VW = Vec<T>::W;
   constexpr int CAP = G * NV * VW;
-  auto kern = k_gather_ring<T, G, NV, D, MINB, PAIR>;
-  const size_t per_group = (size_t)D * NV * G * 16 + (size_t)(a.W_out + 1) * sizeof(double);  // + discard slot
+  // SHORT (the short tail of narrow_impl = 4: items of <= 1024 neighbours): fp32 rows for fp32 tables
+  constexpr bool F32 = SHORT && !PAIR && sizeof(T) == 4;
+  if constexpr (F32) {
+    if (!kn.acc32) return ring_go<T, G, NV, D, MINB, PAIR, false>(a, kn, num_sms, s);
+  }
+  using AccT = typename std::conditional<F32, float, double>::type;
+  auto kern = k_gather_ring<T, G, NV, D, MINB, PAIR, AccT>;
+  const size_t per_group = (size_t)D * NV * G * 16 + (size_t)(a.W_out + 1) * sizeof(AccT);  // + discard slot
   int groups = 256 / G;
   // (sibling pairs: as many groups as MINB CTAs per SM allow)
   while (groups > 1 && (PAIR ? per_group * groups * MINB > 224 * 1024 : per_group * groups > 100 * 1024)) groups /= 2;
@@ -1413,9 +1449,9 @@ int gather_typed(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t
       ++launches;
     }
     if (t.item_from < t.item_to) {
-      if (wvec <= 4) ring_go<T, 4, 1, 4, 3>(t, kn, num_sms, s);
-      else if (wvec <= 8) ring_go<T, 8, 1, 4, 2>(t, kn, num_sms, s);
-      else ring_go<T, 8, 2, 4, 3>(t, kn, num_sms, s);
+      if (wvec <= 4) ring_go<T, 4, 1, 4, 3, false, true>(t, kn, num_sms, s);
+      else if (wvec <= 8) ring_go<T, 8, 1, 4, 2, false, true>(t, kn, num_sms, s);
+      else ring_go<T, 8, 2, 4, 3, false, true>(t, kn, num_sms, s);
       ++launches;
     }
     return launches;
