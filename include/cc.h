@@ -66,8 +66,9 @@ enum {
   CC_FP32 = 1  /* fp32 table storage.  Neighbour sums: fp32 over blocks of at
                   most 32 neighbour rows of one colour group, the blocks added
                   into the vertex's N'' row held in shared memory in fp32
-                  scaled by 2^-64 (acc32 knob, default) or fp64 (short-list
-                  kernels, acc32 = 0); heavy-segment partial rows and their
+                  scaled by 2^-64 (acc32 knob, default; the short-list rings
+                  sum blocks of 8 rows the same way) or fp64 (acc32 = 0);
+                  heavy-segment partial rows and their
                   sum in fp64; combine split sums fp32 FMA; root products and
                   the final reduction fp64.  Worst-case relative error of X
                   ~8e-5 (reading C-6), measured 1e-10..1e-9 */
