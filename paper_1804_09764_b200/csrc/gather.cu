@@ -386,6 +386,33 @@ struct AccScale<float> {
   static constexpr double in = 0x1p-64, out = 0x1p64;
 };
 
+// shared-memory loads / stores of an N'' row entry by its 32-bit shared address
+template <typename AccT>
+__device__ __forceinline__ AccT lds_acc(uint32_t addr);
+template <>
+__device__ __forceinline__ float lds_acc<float>(uint32_t addr) {
+  float x;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(addr) : "memory");
+  return x;
+}
+template <>
+__device__ __forceinline__ double lds_acc<double>(uint32_t addr) {
+  double x;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(addr) : "memory");
+  return x;
+}
+__device__ __forceinline__ void sts_acc_f(uint32_t addr, float x) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(x) : "memory");
+}
+__device__ __forceinline__ void sts_acc_d(uint32_t addr, double x) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(x) : "memory");
+}
+template <typename AccT>
+__device__ __forceinline__ void sts_acc(uint32_t addr, AccT x) {
+  if constexpr (std::is_same<AccT, float>::value) sts_acc_f(addr, x);
+  else sts_acc_d(addr, x);
+}
+
 // A block sum into the row's scale.  fp32 block, fp32 row: one FMUL by the
 // power of two -- exact, bit-identical to the route through fp64 (two F2F on
 // the 16-lane conversion pipe and a DMUL per entry, which made the per-group
@@ -824,6 +851,12 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
   // map's 0xFFFF entries, so that the block flush needs no branches
   AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)(a.W_out + 1);
   const uint32_t discard = (uint32_t)a.W_out;
+  // the row's shared-memory address, opaque to the compiler: under the 80-register
+  // cap of the short-tail launches it was rematerialised (S2R, shift, IMAD) for
+  // every entry of every flush
+  uint32_t sacc_sh = (uint32_t)__cvta_generic_to_shared(sacc);
+  asm volatile("mov.u32 %0, %0;" : "+r"(sacc_sh));
+  const bool noskip = !a.skip;
   const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const char *__restrict__ srcb = static_cast<const char *>(a.src);
@@ -852,7 +885,10 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
       bool valid[NV];
 #pragma unroll
       for (int j = 0; j < NV; ++j) valid[j] = c0 + j * 32 * VW < a.W_in;
-      const char *lbase = srcb + (size_t)c0 * sizeof(T);
+      // (opaque: otherwise rematerialised from the thread id for every row under the register cap)
+      uint64_t lbase_u = reinterpret_cast<uint64_t>(srcb + (size_t)c0 * sizeof(T));
+      asm volatile("mov.u64 %0, %0;" : "+l"(lbase_u));
+      const char *lbase = reinterpret_cast<const char *>(lbase_u);
       for (unsigned g = gm; g; g &= g - 1) {
         const int cu = __ffs(g) - 1;
         const int lo = cu == 0 ? 0 : __shfl_sync(0xffffffffu, hi_l, cu - 1);
@@ -883,7 +919,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
           bool live = false;
 #pragma unroll
           for (int q = 0; q < VW / 2; ++q) live |= mp[j][q] != 0xFFFFFFFFu;
-          use[j] = valid[j] && (live || !a.skip);
+          use[j] = valid[j] && (live || noskip);
         }
         for (int p = lo; p < hi; p += 32) {
           const int cnt = min(32, hi - p);
@@ -912,7 +948,17 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
 #pragma unroll
               for (int j = 0; j < NV; ++j) add_same(blk[j], x[uu][j]);
           }
-          if (r < cnt) {  // tail
+          if constexpr (U == 2) {
+            if (r < cnt) {  // tail: exactly one row
+              const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, r);
+              const V *row = reinterpret_cast<const V *>(lbase + (uint64_t)u * ld_bytes);
+#pragma unroll
+              for (int j = 0; j < NV; ++j)
+                if (use[j]) x[0][j] = __ldg(row + 32 * j);
+#pragma unroll
+              for (int j = 0; j < NV; ++j) add_same(blk[j], x[0][j]);
+            }
+          } else if (r < cnt) {  // tail
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
               const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, my_u, (r + uu) & 31);
@@ -932,19 +978,25 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ldg(GatherArgs a, int nch)
           // N'' row (C-6); 0xFFFF entries land in the discard slot.
           // All loads first, then all stores: the map is injective per colour
           // pair, so only discarded entries can alias
-          AccT *d[NV][VW];
+          // (the map words are pinned here so that the 4 NV entry addresses are
+          // computed after the row loops instead of living across them)
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int q = 0; q < VW / 2; ++q) asm volatile("" : "+r"(mp[j][q]));
+          uint32_t d[NV][VW];
           AccT old[NV][VW];
 #pragma unroll
           for (int j = 0; j < NV; ++j)
 #pragma unroll
             for (int q = 0; q < VW; ++q) {
-              d[j][q] = sacc + min((mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu, discard);
-              old[j][q] = *d[j][q];
+              d[j][q] = sacc_sh + (uint32_t)sizeof(AccT) * min((mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu, discard);
+              old[j][q] = lds_acc<AccT>(d[j][q]);
             }
 #pragma unroll
           for (int j = 0; j < NV; ++j)
 #pragma unroll
-            for (int q = 0; q < VW; ++q) *d[j][q] = old[j][q] + scale_in<AccT>(vec_at(blk[j], q));
+            for (int q = 0; q < VW; ++q) sts_acc<AccT>(d[j][q], old[j][q] + scale_in<AccT>(vec_at(blk[j], q)));
         }
         __syncwarp();  // groups of different colours may map to the same N'' entries
       }
