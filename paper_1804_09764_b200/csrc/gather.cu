@@ -1025,6 +1025,10 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
   const int lane = threadIdx.x & 31, vl = lane % G, rs = lane / G;
   AccT *sacc = reinterpret_cast<AccT *>(sacc_raw) + (threadIdx.x >> 5) * (int64_t)(a.W_out + 1);  // + discard slot
   const uint32_t discard = (uint32_t)a.W_out;
+  // (opaque registers for the row's shared address and the lane's row base, as in k_gather_ldg)
+  uint32_t sacc_sh = (uint32_t)__cvta_generic_to_shared(sacc);
+  asm volatile("mov.u32 %0, %0;" : "+r"(sacc_sh));
+  const bool noskip = !a.skip;
   const int64_t n_items = a.item_to >= 0 ? a.item_to : a.work.n_seg + a.work.n_light;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const char *__restrict__ srcb = static_cast<const char *>(a.src);
@@ -1050,13 +1054,16 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
       bool valid[NV];
 #pragma unroll
       for (int j = 0; j < NV; ++j) valid[j] = c0 + j * G * VW < a.W_in;
-      const char *lbase = srcb + (size_t)c0 * sizeof(T);
+      uint64_t lbase_u = reinterpret_cast<uint64_t>(srcb + (size_t)c0 * sizeof(T));
+      asm volatile("mov.u64 %0, %0;" : "+l"(lbase_u));
+      const char *lbase = reinterpret_cast<const char *>(lbase_u);
       for (unsigned g = gm; g; g &= g - 1) {
         const int cu = __ffs(g) - 1;
         const int lo = cu == 0 ? 0 : __shfl_sync(0xffffffffu, hi_l, cu - 1);
         const int hi = __shfl_sync(0xffffffffu, hi_l, cu);
         bool use[NV];
         uint16_t m[NV][VW];
+        uint32_t mw[NV][2];  // unpaired: the packed map words (entries taken at the flush)
         // sibling pair: per-vector row base and stride (part 1 or part 2)
         const char *jb[NV];
         uint32_t jld[NV];
@@ -1089,14 +1096,9 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
                 w0 = __ldg(reinterpret_cast<const uint32_t *>(mrow + c0 + j * G * VW));
               }
             }
-            use[j] = valid[j] && (!a.skip || w0 != 0xFFFFFFFFu || w1 != 0xFFFFFFFFu);
-            const bool mine = rs == j % RG;
-            m[j][0] = mine ? (uint16_t)(w0 & 0xFFFF) : (uint16_t)0xFFFF;
-            m[j][1 % VW] = mine ? (uint16_t)(w0 >> 16) : (uint16_t)0xFFFF;
-            if constexpr (VW == 4) {
-              m[j][2 % VW] = mine ? (uint16_t)(w1 & 0xFFFF) : (uint16_t)0xFFFF;
-              m[j][3 % VW] = mine ? (uint16_t)(w1 >> 16) : (uint16_t)0xFFFF;
-            }
+            use[j] = valid[j] && (noskip || w0 != 0xFFFFFFFFu || w1 != 0xFFFFFFFFu);
+            mw[j][0] = w0;
+            mw[j][1] = w1;
           }
         }
         int32_t u_next = lane < hi - lo ? __ldg(a.col + b + lo + lane) : 0;
@@ -1151,19 +1153,29 @@ __global__ void __launch_bounds__(256, MINB) k_gather_rows(GatherArgs a, int nch
               add_same(blk[j], o);
             }
           // into N'' (0xFFFF: the discard slot; all loads before the stores)
-          AccT *d[NV][VW];
+          uint32_t d[NV][VW];
           AccT old[NV][VW];
+          if constexpr (!PAIR) {  // (pinned: the entry addresses are computed here, not held across the loads)
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              asm volatile("" : "+r"(mw[j][0]));
+              asm volatile("" : "+r"(mw[j][1]));
+            }
+          }
 #pragma unroll
           for (int j = 0; j < NV; ++j)
 #pragma unroll
             for (int q = 0; q < VW; ++q) {
-              d[j][q] = sacc + min((uint32_t)m[j][q], discard);
-              old[j][q] = *d[j][q];
+              uint32_t idx;
+              if constexpr (PAIR) idx = min((uint32_t)m[j][q], discard);
+              else idx = rs == j % RG ? min((mw[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu, discard) : discard;
+              d[j][q] = sacc_sh + (uint32_t)sizeof(AccT) * idx;
+              old[j][q] = lds_acc<AccT>(d[j][q]);
             }
 #pragma unroll
           for (int j = 0; j < NV; ++j)
 #pragma unroll
-            for (int q = 0; q < VW; ++q) *d[j][q] = old[j][q] + scale_in<AccT>(vec_at(blk[j], q));
+            for (int q = 0; q < VW; ++q) sts_acc<AccT>(d[j][q], old[j][q] + scale_in<AccT>(vec_at(blk[j], q)));
         }
         __syncwarp();  // groups of different colours may map to the same N'' entries
       }
