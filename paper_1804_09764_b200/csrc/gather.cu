@@ -371,21 +371,6 @@ __global__ void __launch_bounds__(256) k_hist(const int64_t *__restrict__ beg, c
   }
 }
 
-// ------------------------------------------------------------------ shared epilogue
-// Write the item's N'' row (light vertex) or its partial (heavy segment; the
-// last arriving segment of the vertex sums all partials in segment order).
-// fp32 shared-memory N'' rows hold value x 2^-64 (an exact power-of-two
-// scale): integer counts up to 6e57 stay in range (configs[4]'s root row
-// reaches ~1e38 unscaled) and 1 stays a normal number.
-template <typename AccT>
-struct AccScale {
-  static constexpr double in = 1.0, out = 1.0;
-};
-template <>
-struct AccScale<float> {
-  static constexpr double in = 0x1p-64, out = 0x1p64;
-};
-
 // shared-memory loads / stores of an N'' row entry by its 32-bit shared address
 template <typename AccT>
 __device__ __forceinline__ AccT lds_acc(uint32_t addr);
@@ -412,6 +397,21 @@ __device__ __forceinline__ void sts_acc(uint32_t addr, AccT x) {
   if constexpr (std::is_same<AccT, float>::value) sts_acc_f(addr, x);
   else sts_acc_d(addr, x);
 }
+
+// ------------------------------------------------------------------ shared epilogue
+// Write the item's N'' row (light vertex) or its partial (heavy segment; the
+// last arriving segment of the vertex sums all partials in segment order).
+// fp32 shared-memory N'' rows hold value x 2^-64 (an exact power-of-two
+// scale): integer counts up to 6e57 stay in range (configs[4]'s root row
+// reaches ~1e38 unscaled) and 1 stays a normal number.
+template <typename AccT>
+struct AccScale {
+  static constexpr double in = 1.0, out = 1.0;
+};
+template <>
+struct AccScale<float> {
+  static constexpr double in = 0x1p-64, out = 0x1p64;
+};
 
 // A block sum into the row's scale.  fp32 block, fp32 row: one FMUL by the
 // power of two -- exact, bit-identical to the route through fp64 (two F2F on
@@ -562,23 +562,23 @@ __device__ __forceinline__ void root_epilogue(const GatherArgs &a, AccT *sacc, i
 // discard slot sacc[W_out] (all loads before the stores), G = 32 branches
 template <int NV, int VW, int G, typename AccT = double>
 __device__ __forceinline__ void expand_map(const GatherArgs &a, const uint32_t (&mp)[NV][2], AccT (&acc)[NV][VW],
-                                           AccT *sacc) {
+                                           AccT *sacc, uint32_t sacc_sh) {
   if constexpr (G <= 8) {
     const uint32_t discard = (uint32_t)a.W_out;
-    AccT *d[NV][VW];
+    uint32_t d[NV][VW];  // shared addresses from the row's (opaque) base: no per-entry rematerialisation
     AccT old[NV][VW];
 #pragma unroll
     for (int j = 0; j < NV; ++j)
 #pragma unroll
       for (int q = 0; q < VW; ++q) {
-        d[j][q] = sacc + min((mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu, discard);
-        old[j][q] = *d[j][q];
+        d[j][q] = sacc_sh + (uint32_t)sizeof(AccT) * min((mp[j][q >> 1] >> (16 * (q & 1))) & 0xFFFFu, discard);
+        old[j][q] = lds_acc<AccT>(d[j][q]);
       }
 #pragma unroll
     for (int j = 0; j < NV; ++j)
 #pragma unroll
       for (int q = 0; q < VW; ++q) {
-        *d[j][q] = old[j][q] + acc[j][q];
+        sts_acc<AccT>(d[j][q], old[j][q] + acc[j][q]);
         acc[j][q] = (AccT)0;
       }
   } else {
@@ -679,6 +679,8 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
                (int64_t)grp * (a.W_out + 1);  // + the discard slot
   const T *__restrict__ src = static_cast<const T *>(a.src);
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+  uint32_t sacc_sh = (uint32_t)__cvta_generic_to_shared(sacc);
+  asm volatile("mov.u32 %0, %0;" : "+r"(sacc_sh));
 
   for (int64_t it = a.item_from + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n_items;
        it += ngroups) {
@@ -810,7 +812,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ring(GatherArgs a, int nch
         }
         if (i + 1 == gend_s) {  // end of a colour group: expand into N''
           if constexpr (PAIR) expand_pair<NV, VW, G>(a, gc, cv, lane, acc, sacc);
-          else expand_map<NV, VW, G, AccT>(a, mp, acc, sacc);
+          else expand_map<NV, VW, G, AccT>(a, mp, acc, sacc, sacc_sh);
           __syncwarp(gmask);
           next_group();
         }
