@@ -100,6 +100,7 @@ int *knob_ptr(cc::dev::Knobs &k, const std::string &name) {
   if (name == "combine_zglobal") return &k.combine_zglobal;
   if (name == "wide_warps") return &k.wide_warps;
   if (name == "wide_nv") return &k.wide_nv;
+  if (name == "tail_warps") return &k.tail_warps;
   if (name == "nvtx_mark") return &k.nvtx_mark;
   if (name == "tail_recompute_cols") return &k.tail_recompute_cols;
   return nullptr;
@@ -110,7 +111,7 @@ void knobs_from_env(cc::dev::Knobs &k) {
   static const char *names[] = {"fused_root", "sector_skip", "gather_impl", "narrow_impl", "narrow_split",
                                 "csort_small", "combine_impl", "acc32", "phase_events", "hub_l2_pct", "grid_reserve",
                                 "tail_batches", "tail_recompute_cols", "layout", "nvtx_mark", "lean_split", "short_lists", "short_split", "rows_variant",
-                                "pair_gather", "combine_wreg", "combine_static", "combine_zglobal", "wide_warps", "wide_nv"};
+                                "pair_gather", "combine_wreg", "combine_static", "combine_zglobal", "wide_warps", "wide_nv", "tail_warps"};
   for (const char *n : names) {
     std::string env = "CC_";
     for (const char *q = n; *q; ++q) env += (char)std::toupper((unsigned char)*q);

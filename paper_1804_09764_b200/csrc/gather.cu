@@ -1362,6 +1362,8 @@ void ldg_go(const GatherArgs &a, const Knobs &kn, int num_sms, cudaStream_t s) {
   while (warps > 1 && row * warps > 200 * 1024) warps /= 2;
   // knob wide_warps: fewer warps per CTA for N'' rows of > 8 KB (more L1 left for the rows in flight)
   if (kn.wide_warps > 0 && row > 8 * 1024) warps = std::min(warps, kn.wide_warps);
+  // knob tail_warps: smaller CTAs for the short-tail launches (MINB = 3 variants)
+  if (MINB == 3 && kn.tail_warps > 0) warps = std::min(warps, kn.tail_warps);
   const int threads = warps * 32;
   const size_t smem = row * warps;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

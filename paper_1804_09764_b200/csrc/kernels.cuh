@@ -60,6 +60,8 @@ struct Knobs {
                            //   split pairs in registers (0: read them from shared memory per vertex)
   int wide_warps = 0;      // CC_WIDE_WARPS: > 0 = warps per CTA of the lean gather for N'' rows of > 8 KB
   int wide_nv = 4;         // CC_WIDE_NV: 16-byte vectors per lane per pass for rows of > 128 vectors (4 or 6)
+  int tail_warps = 4;      // CC_TAIL_WARPS: warps per CTA of the lean gather's short-tail launch (72 registers:
+                           //   7 CTAs of 4 warps = 28 warps per SM instead of 3 x 8 = 24)
   int tail_recompute_cols = 0;  // CC_TAIL_RECOMPUTE_COLS: > 0 forces the tail's passive to be recomputed
                                 //   per batch in column chunks of this width (0 = by memory)
 };

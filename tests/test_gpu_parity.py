@@ -719,7 +719,7 @@ KNOB_SETTINGS = [("gather_impl", 1), ("gather_impl", 2), ("narrow_impl", 0), ("n
                  ("combine_impl", 1), ("combine_impl", 2), ("combine_impl", 3), ("combine_impl", 4), ("acc32", 0),
                  ("fused_root", 0), ("phase_events", 0), ("hub_l2_pct", 0), ("grid_reserve", 32), ("layout", 1), ("short_lists", 0), ("short_lists", 1), ("short_lists", 3), ("short_split", 1), ("lean_split", 2),
                  ("pair_gather", 1), ("rows_variant", 2), ("short_lists", 4), ("combine_wreg", 0),
-                 ("combine_static", 0), ("combine_static", 2), ("combine_zglobal", 0)]
+                 ("combine_static", 0), ("combine_static", 2), ("combine_zglobal", 0), ("tail_warps", 8), ("tail_warps", 2)]
 
 
 @pytest.mark.parametrize("ci", [2, 3, 4])
